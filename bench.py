@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the latsum hot path on B200 (arXiv 1405.2270, BASELINE.json).
+
+One "step" = one pass of the hot path over the lattice: the rank-R erf
+generator (K1) for every distinct axis, the assembled O(N L R) lattice sum
+(K2) and the FP64 rank-R expansion of this rank's z-slabs onto the full grid
+in HBM (K3). Weak scaling over z-slabs: every rank owns 1024^3 points
+(N=1: configs[1], 1024^3; N=2: 1024x1024x2048; N=4: 1024x2048^2; N=8:
+configs[2], 2048^3 sharded in z), no inter-GPU traffic in the timed region.
+
+Prints ONE JSON line (rank 0). `value` = grid points/s of the whole job with
+inputs in HBM; `e2e` = the same metric through the host-level C-ABI call
+(ls_h_lattice_potential: host rule/charges in, full grid out into pinned host
+memory, every copy inside the timed region); `roofline` = the expansion
+kernel's achieved FP64 rate against the measured DMMA peak; `cpu_baseline` =
+the reference's own code (oracle/_ref, compiled unmodified) on the host cores.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "lattice potential Gpts/s (rank-R N^3 eval)"
+UNIT = "Gpts/s"
+B = 10.0          # unit-cell edge, bohr (BASELINE configs)
+n_CELL = 64       # grid points per cell per axis
+M_QUAD = 20       # R = 2M+1 = 41
+EPS = 1e-6        # sinc_quadrature(eps, h, sqrt(3) L b, M, C0) -- SURVEY 8(d)
+C0 = 1.0
+
+
+def lattice_for(world: int) -> tuple[int, int, int]:
+    """Weak-scaling lattice: 1024^3 points (L = 16^3) per rank, grown along z, then y, then x."""
+    table = {1: (16, 16, 16), 2: (16, 16, 32), 4: (16, 32, 32), 8: (32, 32, 32)}
+    if world in table:
+        return table[world]
+    return (16, 16, 16 * world)
+
+
+def fp64_peak_tflops() -> tuple[float, str]:
+    """Measured FP64 DMMA peak (tools/microbench/fp64_peak.cu on this pool's B200)."""
+    p = ROOT / "profiles" / "r01_fp64_peak_microbench.jsonl"
+    best = 0.0
+    if p.exists():
+        for line in p.read_text().splitlines():
+            try:
+                d = json.loads(line)
+            except json.JSONDecodeError:
+                continue
+            if str(d.get("bench", "")).startswith("dmma"):
+                best = max(best, float(d.get("tflops", 0.0)))
+    if best > 0:
+        return best, "measured (DMMA m8n8k4 microbench, profiles/r01_fp64_peak_microbench.jsonl)"
+    return 37.2, "nominal (148 SM x 64 FMA/clk x 1965 MHz)"
+
+
+def hbm_peak_gbs() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except (KeyError, ValueError):
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = Path(f"/tmp/latsum_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        if self.path.exists():
+            for line in self.path.read_text().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for name, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        power = [num(r[7]) for r in rows if num(r[7]) is not None]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(rows[0][1]),
+                "reasons": sorted(reasons), "samples": len(rows),
+                "power_w_max": max(power) if power else None}
+
+
+def make_problem(world: int):
+    import paper_1405_2270_b200 as L
+    Lx = lattice_for(world)
+    spec = L.LatticeSpec(Lx, L.GridSpec(B, n_CELL), [L.Charge((0.0, 0.0, 0.0), 1.0)])
+    Lmax = max(Lx)
+    rule = L.sinc_quadrature(EPS, spec.unit.h, math.sqrt(3.0) * Lmax * B, M_QUAD, C0)
+    return L, spec, rule
+
+
+def slab_range(N3: int, rank: int, world: int) -> tuple[int, int]:
+    per = N3 // world
+    return rank * per, (rank + 1) * per if rank < world - 1 else N3
+
+
+def workload_config(spec, world, rule) -> dict:
+    N = spec.target_dims()
+    return {
+        "workload": ("cfg1: n=64, L=16^3, N=1024 (1024^3 FP64 grid, 8 GiB) on 1 GPU" if world == 1 else
+                     f"weak z-slab scaling: lattice L={spec.L}, grid {N[0]}x{N[1]}x{N[2]}, 1024^3 points per GPU"
+                     + (" (= cfg2, 2048^3 sharded 8-way)" if world == 8 else "")),
+        "grid": list(N), "rank_R": rule.node_count(), "charges_per_cell": 1, "generator": "erf (newton.hpp:21-37)",
+        "box_b_bohr": B, "n_per_cell": n_CELL, "quadrature": f"sinc_quadrature({EPS}, h, sqrt(3)*L*b, M=20, C0=1)",
+        "parallelism": f"z-slab x{world}, no collective in the timed region",
+        "l2_policy": "output 8 GiB per GPU per step >> 126 MB L2; factors regenerated every step",
+    }
+
+
+# --------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    L, spec, rule = make_problem(world)
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    L.load_library().ls_set_device(local_rank)
+    N1, N2, N3 = spec.target_dims()
+    k0, k1 = slab_range(N3, rank, world)
+    pipe = L.DevicePipeline(spec, rule, mode="erf", device=dev)
+    out = torch.empty((k1 - k0, N2, N1), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    lib = L.load_library()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        pipe.step(out, k0, k1, stream)
+    torch.cuda.synchronize()
+
+    # Timed region: K steps, events around each expansion launch for the roofline.
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.ls_launch_count()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for s in range(args.steps):
+            pipe.generate(stream)
+            pipe.assemble(stream)
+            ev[s][0].record(stream)
+            pipe.expand(out, k0, k1, stream)
+            ev[s][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = lib.ls_launch_count() - launches0
+    ms_total = t_start.elapsed_time(t_end)
+    exp_ms = [a.elapsed_time(b) for a, b in ev]
+    if world > 1:
+        tt = torch.tensor([ms_total, statistics.mean(exp_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total, exp_mean = float(tt[0]), float(tt[1])
+    else:
+        exp_mean = statistics.mean(exp_ms)
+    ms_step = ms_total / args.steps
+    pts_total = float(N1) * N2 * N3
+    value = pts_total / (ms_step * 1e-3) / 1e9
+
+    # Roofline of the expansion kernel (per launch, this rank's slabs).
+    pts_rank = float(N1) * N2 * (k1 - k0)
+    flops = 2.0 * pipe.Rt * pts_rank
+    peak_tf, peak_src = fp64_peak_tflops()
+    achieved_tf = flops / (exp_mean * 1e-3) / 1e12
+    hbm_gbs, hbm_src = hbm_peak_gbs()
+    out_gbs = 8.0 * pts_rank / (exp_mean * 1e-3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_expand_traffic.json"
+    if tp.exists():
+        try:
+            tj = json.loads(tp.read_text())
+            if tj.get("grid") == [N1, N2, k1 - k0]:
+                traffic = tj.get("dram_bytes_per_launch")
+        except (ValueError, KeyError):
+            traffic = None
+    roofline = {
+        "bound": "tensor", "pipe": "fp64 DMMA (mma.sync m8n8k4.f64)", "achieved": round(achieved_tf, 3),
+        "peak": round(peak_tf, 3), "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4),
+        "peak_source": peak_src, "traffic": traffic,
+        "algorithmic": f"2*R*points FLOP = {flops:.4e} per launch (R={pipe.Rt}), 8 B/point written",
+        "kernel_ms": round(exp_mean, 4),
+        "hbm_leg": {"achieved_gbs": round(out_gbs, 1), "peak_gbs": hbm_gbs, "frac": round(out_gbs / hbm_gbs, 4),
+                    "peak_source": hbm_src},
+        "share_of_step": round(exp_mean / ms_step, 4),
+    }
+    del out
+    torch.cuda.empty_cache()
+
+    # e2e through the host-level C-ABI call: host rule/charges in, pinned host grid out.
+    e2e = run_e2e(L, spec, rule, k0, k1, args, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(spec, rule, budget_s=args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs; "
+            "unit charge at each cell centre; quadrature rule computed on the host)",
+            "config": workload_config(spec, world, rule), "roofline": roofline, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": cpu,
+            "assembly_note": "generator + assembly are inside every step (replicated per rank)",
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(L, spec, rule, k0, k1, args, world, dev):
+    import torch
+    import torch.distributed as dist
+    N1, N2, N3 = spec.target_dims()
+    steps = max(1, min(args.steps, args.e2e_steps))
+    host = torch.empty((k1 - k0) * N2 * N1, dtype=torch.float64, pin_memory=True)
+    buf = host.numpy().reshape((N1, N2, k1 - k0), order="F")
+    L.lattice_potential(spec, rule, mode="erf", k0=k0, k1=k1, out=buf)  # warm-up (pool, module load)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        L.lattice_potential(spec, rule, mode="erf", k0=k0, k1=k1, out=buf)
+    el = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([el], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt[0])
+    pts = float(N1) * N2 * N3
+    h2d = 8 * rule.node_count() * 2 + 8 * 4 * spec.charge_count()
+    d2h = 8 * N1 * N2 * (k1 - k0)
+    del host, buf
+    return {"value": round(pts / (el / steps) / 1e9, 4), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": steps,
+            "api": "ls_h_lattice_potential (host tau/w/charges in; full grid out to pinned host memory)"}
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_baseline(spec, rule, budget_s: float = 15.0, threads: int | None = None, sample_slabs: int | None = None):
+    """The reference's own code (oracle/_ref, headers compiled unmodified) on the host cores:
+    erf master + assembled_box_sum + densify_slab streamed over z-slabs into a reused slab buffer.
+    Bounded sample: slabs until `budget_s` of expansion time; reported per grid point."""
+    import ctypes as C
+    from oracle import ref_available, reference, restatement
+    kind = "reference" if ref_available() else "port"
+    lib = reference() if kind == "reference" else restatement()
+    cores = threads or os.cpu_count() or 1
+    if kind == "reference":
+        lib._set_threads(cores)
+    else:
+        cores = 1
+    N = spec.target_dims()
+    R = rule.node_count()
+    Lx = np.array(spec.L, dtype=np.int64)
+    tau = np.ascontiguousarray(rule.exponents)
+    w = np.ascontiguousarray(rule.weights)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        f = lib.lattice_master(1, Lx, spec.unit.n, spec.unit.b, tau, w)
+        dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+        fac = [np.zeros((N[l], R), order="F") for l in range(3)]
+        wout = np.zeros(R)
+        ch = np.array([0.0, 0.0, 0.0, 1.0])
+        lib._check(lib._assembled_sum(0, Lx.ctypes.data_as(C.POINTER(C.c_int64)), spec.unit.n, spec.unit.b, dp(ch), 1,
+                                      dp(f[0]), dp(f[1]), dp(f[2]), dp(w), R, dp(fac[0]), dp(fac[1]), dp(fac[2]),
+                                      dp(wout), None), "assembled_sum")
+    else:
+        raise RuntimeError("oracle/_ref not built; cpu baseline needs the compiled reference")
+    t_asm = time.perf_counter() - t0
+    chunk = max(1, min(N[2], cores * 2))
+    buf = np.empty((N[0], N[1], chunk), order="F")
+    done = 0
+    t_exp = 0.0
+    limit = sample_slabs if sample_slabs is not None else N[2]
+    while done < limit:
+        k1 = min(N[2], done + chunk, limit)
+        ms = C.c_double(0)
+        lib._check(lib._expand_into(N[0], N[1], N[2], R, dp(fac[0]), dp(fac[1]), dp(fac[2]), dp(wout), done, k1,
+                                    dp(buf), C.byref(ms)), "expand_into")
+        t_exp += ms.value * 1e-3
+        done = k1
+        if sample_slabs is None and t_exp > budget_s:
+            break
+    pts = float(N[0]) * N[1] * done
+    # per-point cost of the sampled slabs plus the (whole) generator+assembly, scaled to the full grid
+    full_s = t_exp * (N[2] / done) + t_asm
+    return {"value": round(float(N[0]) * N[1] * N[2] / full_s / 1e9, 5), "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"erf master + assembled_box_sum + densify_slab over {done}/{N[2]} z-slabs "
+                      f"({pts:.3e} points, {t_exp:.2f} s expansion, {t_asm * 1e3:.1f} ms master+assembly) "
+                      f"via oracle/_ref (reference headers + eigen_compat shim GEMM), LATSUM_THREADS={cores}",
+            "expansion_s_sampled": round(t_exp, 3), "assembly_ms": round(t_asm * 1e3, 3)}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from types import SimpleNamespace
+    from oracle import reference
+    Lx = lattice_for(world)
+    spec = SimpleNamespace(L=Lx, unit=SimpleNamespace(n=n_CELL, b=B, h=B / n_CELL), charges=[None],
+                           target_dims=lambda: tuple(l * n_CELL for l in Lx), charge_count=lambda: 1)
+    # The reference's own sinc_quadrature (quadrature.hpp:50-89) builds the rule on this arm.
+    _, tau, w, _ = reference().sinc_quadrature(EPS, B / n_CELL, math.sqrt(3.0) * max(Lx) * B, M_QUAD, C0)
+    rule = SimpleNamespace(exponents=tau, weights=w, node_count=lambda: len(tau))
+    vals = []
+    t_all = time.perf_counter()
+    for s in range(args.warmup + args.steps):
+        cb = cpu_baseline(spec, rule, budget_s=args.cpu_seconds / max(1, args.steps + args.warmup))
+        if s >= args.warmup:
+            vals.append(cb)
+    value = statistics.median(v["value"] for v in vals)
+    cb = dict(vals[-1])
+    cb["value"] = value
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(float(np.prod(spec.target_dims())) / (value * 1e9) * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (same inputs as the GPU arm)", "config": workload_config(spec, world, rule),
+        "impl": "reference", "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": round(time.perf_counter() - t_all, 2),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/* latsum_cuda.h -- C ABI of liblatsum_cuda.so, the B200 (sm_100a) engine behind
+ * the drop-in latsum C++ API (include/latsum/*.hpp).
+ *
+ * The reference (arXiv 1405.2270, /root/reference/proj) is a header-only C++
+ * library with no FFI; its "operator API" is the set of inline functions in
+ * proj/include/latsum/. Each entry point below names the reference function
+ * whose hot loop it replaces (file:line under proj/include/latsum/).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. `_d` pointers are device memory on the
+ *    current CUDA device, `_h` pointers are host memory. `stream` is a
+ *    cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Matrices are column-major with an explicit leading dimension (the
+ *    layout of Eigen::MatrixXd, canonical.hpp:17-19). Factor l of a rank-R
+ *    canonical tensor is dims[l] x R. Dense grids are i-fastest:
+ *    out[i + n1*(j + n2*k)] (DenseTensor3, canonical.hpp:94-99).
+ *  - All arithmetic is FP64.
+ *  - Return status: LS_OK, LS_EVALIDATION (reference validation_error,
+ *    errors.hpp:9-12), LS_EGUARD (resource_guard_error, errors.hpp:17-20),
+ *    LS_ECUDA (CUDA runtime failure). ls_last_error() returns a thread-local
+ *    message for the last failing call on the calling thread.
+ *  - Device-level calls are asynchronous on `stream`; host-level (`ls_h_*`)
+ *    calls are synchronous and own their device buffers.
+ *  - There is no CPU fallback: without a usable sm_100 device every call
+ *    returns LS_ECUDA.
+ */
+#ifndef LATSUM_CUDA_H
+#define LATSUM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LS_OK 0
+#define LS_EVALIDATION 2
+#define LS_EGUARD 4
+#define LS_ECUDA 5
+
+#define LS_GEN_MIDPOINT 0 /* gaussian_sample_vector, newton.hpp:43-52 */
+#define LS_GEN_ERF 1      /* gaussian_moment_vector, newton.hpp:21-37 */
+
+/* ---- lifecycle / diagnostics -------------------------------------------- */
+int ls_abi_version(void);
+const char* ls_last_error(void);
+/* Sets the CUDA device used by the host-level calls of this thread. */
+int ls_set_device(int device);
+/* Number of kernel launches this library issued since load (all threads). */
+int64_t ls_launch_count(void);
+
+/* ---- host-side quadrature rule (no device work) -------------------------
+ * sinc_quadrature(eps, a_min, a_max, M, C0) (quadrature.hpp:50-89): writes
+ * the 2M+1 substitution nodes (may be NULL), exponents tau_q (ascending) and
+ * weights w_q, and the node spacing (*step, may be NULL). */
+int ls_sinc_quadrature(double eps, double a_min, double a_max, int M, double C0, double* nodes_h,
+                       double* exponents_h, double* weights_h, double* step);
+
+/* ---- K1: rank-R Newton-kernel generator --------------------------------
+ * Replaces the column loop of build_newton_master (newton.hpp:57-75) with
+ * gaussian_sample_vector (mode LS_GEN_MIDPOINT, newton.hpp:43-52) or
+ * gaussian_moment_vector(GridSpec, t, doubled) (mode LS_GEN_ERF,
+ * newton.hpp:21-37): out_d[i + ld*q], i < len, q < R. One thread per (q, i).
+ * len must be even (>= 2); h > 0; tau_d[q] >= 0 finite. */
+int ls_gen_master(int mode, const double* tau_d, int R, int64_t len, double h, double* out_d,
+                  int64_t ld, void* stream);
+
+/* ---- K2: assembled lattice summation ----------------------------------
+ * Replaces detail::assembled_axis_columns (lattice.hpp:220-274) for one
+ * axis: column c = nu*R + q of out_d (out_len x M0*R, leading dim ld_out) is
+ * sum_{k=0}^{L-1} master[s0(nu) - k*n + i], accumulated in ascending k
+ * (bit-identical to the reference's blocked left-to-right adds), with
+ * s0 = window_start_box(N, n, i_a, 0) (lattice.hpp:98) or
+ * window_start_periodic(N, n, i_a, 0, L) (lattice.hpp:104-106), N = L*n.
+ * master_d is (2N x R, leading dim ld_master); ia_d holds the M0 charge grid
+ * indices on this axis (LatticeSpec::charge_grid_index, lattice.hpp:57-68).
+ * out_len = n when periodic, else N. */
+int ls_assemble_axis(const double* master_d, int64_t ld_master, int R, int M0, const int64_t* ia_d,
+                     int64_t n, int64_t L, int periodic, double* out_d, int64_t ld_out, void* stream);
+
+/* ---- K3: rank-R expansion onto the full grid -----------------------------
+ * Replaces densify / detail::densify_slab (canonical.hpp:241-266) for the
+ * z-slab range [k0, k1): V(i,j,k) = sum_q (A(i,q) * (w_q*C(k,q))) * B(j,q),
+ * written to out_d[(k-k0)*ldz + j*ldy + i] (ldy >= N1, ldz >= ldy*N2; pass
+ * 0 for the dense defaults ldy = N1, ldz = N1*N2). FP64 DMMA tensor-core
+ * tiles; one z-shard per call, no inter-GPU traffic.
+ * Optional fused epilogue (BASELINE functional): when rho1_d
+ * is non-NULL, partial_d[u] receives the separable-rho weighted sum
+ *     sum_{i,j in unit u} V(i,j,k) * rho1(i) * rho2(j) * rho3(k)
+ * for every work unit u (deterministic order); reduce with
+ * ls_sum_partials. out_d may be NULL to skip storing the grid.
+ * ls_expand_partial_count() gives the number of units for a shape. */
+int ls_expand(const double* A_d, int64_t lda, const double* B_d, int64_t ldb, const double* C_d,
+              int64_t ldc, const double* w_d, int64_t N1, int64_t N2, int64_t N3, int R, int64_t k0,
+              int64_t k1, double* out_d, int64_t ldy, int64_t ldz, const double* rho1_d,
+              const double* rho2_d, const double* rho3_d, double* partial_d, void* stream);
+int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_t k0, int64_t k1);
+/* Deterministic fixed-order sum of count doubles into *out_d (device). */
+int ls_sum_partials(const double* partial_d, int64_t count, double* out_d, void* stream);
+
+/* ---- K4: functionals and point evaluation -------------------------------
+ * eval_point (canonical.hpp:304-314) for P index triples idx_d[3*p+{0,1,2}]:
+ * out_d[p] = sum_q w_q*A(i,q)*B(j,q)*C(k,q), accumulated in rank order. */
+int ls_eval_points(const double* A_d, int64_t lda, const double* B_d, int64_t ldb,
+                   const double* C_d, int64_t ldc, const double* w_d, int R, const int64_t* idx_d,
+                   int64_t P, double* out_d, void* stream);
+/* Gram matrix G = X^T Y (Rx x Ry) of two n-row column-major matrices: the
+ * per-axis products of scalar_product (canonical.hpp:130). Deterministic
+ * fixed-order dot products, one warp per entry. G_d is Rx x Ry, ld = Rx. */
+int ls_gram(const double* X_d, int64_t ldx, int Rx, const double* Y_d, int64_t ldy, int Ry, int64_t n,
+            double* G_d, void* stream);
+/* scalar_product(a, b) (canonical.hpp:126-136) from the three Gram matrices
+ * (each Ra x Rb, ld Ra): out_d[0] = sum_i sum_j wa_i*wb_j*G0*G1*G2 in the
+ * reference's rank-major order. */
+int ls_gram_reduce(const double* G0_d, const double* G1_d, const double* G2_d, const double* wa_d,
+                   int Ra, const double* wb_d, int Rb, double* out_d, void* stream);
+/* Batched 1D functional: for F rank-1 densities rho_f = x_f (x) y_f (x) z_f
+ * (columns of X_d, Y_d, Z_d; n1/n2/n3 rows), out_d[f] = scalar_product(P, rho_f)
+ * (canonical.hpp:126-136 with Rb = 1), optionally times `scale`
+ * (potential_matrix's h^3 volume element, project.hpp:74). Workspace-free:
+ * Gram columns are formed in shared memory per f. */
+int ls_functional_batch(const double* A_d, int64_t lda, const double* B_d, int64_t ldb,
+                        const double* C_d, int64_t ldc, const double* w_d, int R, int64_t n1,
+                        int64_t n2, int64_t n3, const double* X_d, int64_t ldx, const double* Y_d,
+                        int64_t ldy, const double* Z_d, int64_t ldz, int F, double scale,
+                        double* out_d, void* stream);
+
+/* ---- host-level entry points (drop-in headers, e2e path) ----------------
+ * Synchronous; all pointers host memory; results copied back. */
+/* build_lattice_master (lattice.hpp:109-113) / erf master: f_h[l] is
+ * (2*L[l]*n x R), column-major. */
+int ls_h_lattice_master(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h,
+                        int R, double* f0_h, double* f1_h, double* f2_h);
+/* gaussian_sample_vector / gaussian_moment_vector for one column. */
+int ls_h_gen_column(int mode, double t, int64_t len, double h, double* out_h);
+/* detail::assembled_axis_columns (lattice.hpp:220-274) on a host master. */
+int ls_h_assemble_axis(const double* master_h, int64_t master_len, int R, int M0,
+                       const int64_t* ia_h, int64_t n, int64_t L, int periodic, double* out_h);
+/* densify_slab over [k0, k1) (canonical.hpp:241-266) into a host grid;
+ * device compute overlapped with chunked device->host copies. */
+int ls_h_expand(const int64_t dims[3], int R, const double* A_h, const double* B_h,
+                const double* C_h, const double* w_h, int64_t k0, int64_t k1, double* out_h);
+/* eval_point batch (canonical.hpp:304-314). */
+int ls_h_eval_points(const int64_t dims[3], int R, const double* A_h, const double* B_h,
+                     const double* C_h, const double* w_h, const int64_t* idx_h, int64_t P,
+                     double* out_h);
+/* scalar_product (canonical.hpp:126-136). */
+int ls_h_scalar_product(const int64_t dims[3], int Ra, const double* A0_h, const double* A1_h,
+                        const double* A2_h, const double* wa_h, int Rb, const double* B0_h,
+                        const double* B1_h, const double* B2_h, const double* wb_h, double* out_h);
+/* Full-grid functional sum V * rho over slabs [k0,k1) without storing V. */
+int ls_h_grid_functional(const int64_t dims[3], int R, const double* A_h, const double* B_h,
+                         const double* C_h, const double* w_h, const double* r1_h,
+                         const double* r2_h, const double* r3_h, int64_t k0, int64_t k1,
+                         double* out_h);
+
+/* End-to-end lattice potential (the e2e path of bench.py): generator (mode),
+ * assembled box (periodic = 0) or periodic (periodic = 1) sum for the charges
+ * (M0 x 4 rows: x, y, z, Z in unit-cell coordinates [-b/2, b/2]), then the
+ * expansion of slabs [k0, k1) of the assembled tensor into grid_h (host).
+ * Optionally also returns the assembled factors (f*_h may be NULL) and
+ * weights. Inputs/outputs are host memory; all copies are inside the call. */
+int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h,
+                           const double* w_h, int R, const double* charges_h, int M0, int periodic,
+                           int64_t k0, int64_t k1, double* grid_h, double* f0_h, double* f1_h,
+                           double* f2_h, double* wout_h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LATSUM_CUDA_H */

@@ -1,0 +1,449 @@
+// abi.cu -- lifecycle, diagnostics and the synchronous host-level entry points
+// (ls_h_*) of liblatsum_cuda.so. The host-level calls are what the drop-in
+// C++ headers (include/latsum/*.hpp) and the end-to-end bench path use: host
+// buffers in, host buffers out, every device buffer owned and released here
+// (stream-ordered pool allocations, so repeated calls do not hit cudaMalloc).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ls {
+
+std::string& last_error() {
+    thread_local std::string msg;
+    return msg;
+}
+
+std::atomic<int64_t>& launch_counter() {
+    static std::atomic<int64_t> n{0};
+    return n;
+}
+
+int sm_count() {
+    static std::mutex mu;
+    static std::vector<int> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= static_cast<int>(cache.size())) cache.resize(dev + 1, 0);
+    if (cache[dev] == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = v > 0 ? v : 148;
+    }
+    return cache[dev];
+}
+
+namespace {
+
+// Per-thread compute + copy streams on the current device, and a pool that
+// keeps freed blocks cached between calls.
+struct Streams {
+    int device = -1;
+    cudaStream_t compute = nullptr;
+    cudaStream_t copy = nullptr;
+};
+
+int get_streams(Streams*& out) {
+    thread_local Streams s;
+    int dev = 0;
+    LS_CUDA(cudaGetDevice(&dev));
+    if (s.device != dev) {
+        LS_CUDA(cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking));
+        LS_CUDA(cudaStreamCreateWithFlags(&s.copy, cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        s.device = dev;
+    }
+    out = &s;
+    return LS_OK;
+}
+
+// Stream-ordered device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    int alloc(size_t bytes, cudaStream_t stream) {
+        s = stream;
+        if (bytes == 0) bytes = 16;
+        cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            return cuda_fail(e, "cudaMallocAsync");
+        }
+        return LS_OK;
+    }
+    double* d() const { return static_cast<double*>(p); }
+    int64_t* i() const { return static_cast<int64_t*>(p); }
+};
+
+#define LS_TRY(expr)                 \
+    do {                             \
+        int _rc = (expr);            \
+        if (_rc != LS_OK) return _rc; \
+    } while (0)
+
+int upload(DevBuf& b, const void* host, size_t bytes, cudaStream_t s) {
+    LS_TRY(b.alloc(bytes, s));
+    if (bytes) LS_CUDA(cudaMemcpyAsync(b.p, host, bytes, cudaMemcpyHostToDevice, s));
+    return LS_OK;
+}
+
+// lattice.hpp:57-68: grid-point index of coordinate p on the unit cell (b, n).
+int charge_grid_index(double b, int64_t n, double p, int64_t& out) {
+    const double h = b / static_cast<double>(n);
+    const double x = (p + b / 2.0) / h;
+    const double r = std::round(x);
+    if (std::abs(x - r) > 1e-9 * static_cast<double>(n) || r < 0.0 || r > static_cast<double>(n))
+        return fail(LS_EVALIDATION, "lattice: charge coordinate " + std::to_string(p) +
+                                        " does not lie on a grid point of the unit cell");
+    out = static_cast<int64_t>(r);
+    return LS_OK;
+}
+
+// Expands slabs [k0, k1) of a device-resident tensor into host memory: the
+// compute stream fills chunk buffers, the copy stream drains them, and two
+// chunk buffers alternate so compute of chunk c+1 overlaps the copy of c.
+int expand_to_host(const double* A, const double* B, const double* C, const double* w,
+                   const int64_t d[3], int R, int64_t k0, int64_t k1, double* out_h, Streams& st) {
+    const int64_t slab = d[0] * d[1];
+    if (k1 <= k0 || slab == 0) return LS_OK;
+    const int64_t slab_bytes = slab * static_cast<int64_t>(sizeof(double));
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, (256ll << 20) / slab_bytes));
+    DevBuf buf[2];
+    cudaEvent_t done_compute[2], done_copy[2];
+    for (int b = 0; b < 2; ++b) {
+        LS_TRY(buf[b].alloc(static_cast<size_t>(chunk * slab_bytes), st.compute));
+        LS_CUDA(cudaEventCreateWithFlags(&done_compute[b], cudaEventDisableTiming));
+        LS_CUDA(cudaEventCreateWithFlags(&done_copy[b], cudaEventDisableTiming));
+    }
+    int rc = LS_OK;
+    int64_t c = 0;
+    for (int64_t ks = k0; ks < k1 && rc == LS_OK; ks += chunk, ++c) {
+        const int b = static_cast<int>(c & 1);
+        const int64_t ke = std::min(k1, ks + chunk);
+        if (c >= 2) cudaStreamWaitEvent(st.compute, done_copy[b], 0);
+        rc = ls_expand(A, d[0], B, d[1], C, d[2], w, d[0], d[1], d[2], R, ks, ke, buf[b].d(), 0, 0,
+                       nullptr, nullptr, nullptr, nullptr, st.compute);
+        if (rc != LS_OK) break;
+        cudaEventRecord(done_compute[b], st.compute);
+        cudaStreamWaitEvent(st.copy, done_compute[b], 0);
+        cudaError_t e = cudaMemcpyAsync(out_h + (ks - k0) * slab, buf[b].p,
+                                        static_cast<size_t>((ke - ks) * slab_bytes),
+                                        cudaMemcpyDeviceToHost, st.copy);
+        if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync D2H");
+        cudaEventRecord(done_copy[b], st.copy);
+    }
+    cudaError_t e1 = cudaStreamSynchronize(st.copy);
+    cudaError_t e2 = cudaStreamSynchronize(st.compute);
+    for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(done_compute[b]);
+        cudaEventDestroy(done_copy[b]);
+    }
+    if (rc != LS_OK) return rc;
+    if (e1 != cudaSuccess) return cuda_fail(e1, "copy stream");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "compute stream");
+    return LS_OK;
+}
+
+}  // namespace
+}  // namespace ls
+
+using ls::DevBuf;
+using ls::Streams;
+
+extern "C" {
+
+int ls_abi_version(void) { return 1; }
+
+const char* ls_last_error(void) { return ls::last_error().c_str(); }
+
+int ls_set_device(int device) {
+    LS_CUDA(cudaSetDevice(device));
+    return LS_OK;
+}
+
+int64_t ls_launch_count(void) { return ls::launch_counter().load(); }
+
+// quadrature.hpp:50-89 (host arithmetic; the rule is 2M+1 scalars shared by
+// every stage): window [s1, s2] from the two tail bisections
+// (quadrature.hpp:35-46, :62-66), then tau_j = 2 G(s_j) / a_max and
+// w_j = step (4/sqrt(pi)) cosh(s_j) / (1 + e^{-min(sinh s_j, 700)}) / a_max,
+// G(s) = log(1 + e^{sinh s}) (sinh s itself above 30).
+}  // extern "C"
+namespace {
+template <class F>
+double bisect_tail(F f, double target, double hi) {
+    double lo = 1e-3;
+    while (f(hi) > target) hi *= 1.5;
+    for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        (f(mid) <= target ? hi : lo) = mid;
+    }
+    return hi;
+}
+}  // namespace
+extern "C" {
+
+int ls_sinc_quadrature(double eps, double a_min, double a_max, int M, double C0, double* nodes,
+                       double* exponents, double* weights, double* step_out) {
+    if (M < 1) return ls::fail(LS_EVALIDATION, "quadrature: M must be >= 1, got " + std::to_string(M));
+    if (!(eps > 0.0) || !(eps < 1.0)) return ls::fail(LS_EVALIDATION, "quadrature: eps must lie in (0, 1)");
+    if (!(a_min > 0.0) || !(a_min < a_max))
+        return ls::fail(LS_EVALIDATION, "quadrature: need 0 < a_min < a_max");
+    const double tol = eps * std::pow(10.0, -C0);
+    const double ratio = a_min / a_max;
+    const double t_lo = bisect_tail([](double t) { return 2.0 * t * std::exp(-t); }, tol, 5.0);
+    const double t_hi = bisect_tail([](double t) { return std::sqrt(t) * std::exp(-t); }, tol * ratio, 5.0);
+    const double s_begin = -std::log(2.0 * t_lo);
+    const double s_end = 0.5 * std::log(t_hi / (ratio * ratio));
+    const int count = 2 * M + 1;
+    const double step = (s_end - s_begin) / static_cast<double>(count - 1);
+    const double c = 4.0 / std::sqrt(M_PI);
+    for (int j = 0; j < count; ++j) {
+        const double s = s_begin + step * static_cast<double>(j);
+        const double sh = std::sinh(s);
+        const double G = sh > 30.0 ? sh : std::log1p(std::exp(sh));
+        if (nodes) nodes[j] = s;
+        exponents[j] = 2.0 * G / a_max;
+        weights[j] = step * c * std::cosh(s) / (1.0 + std::exp(-std::min(sh, 700.0))) / a_max;
+    }
+    if (step_out) *step_out = step;
+    return LS_OK;
+}
+
+int ls_h_gen_column(int mode, double t, int64_t len, double h, double* out_h) {
+    if (!(t >= 0.0) || !std::isfinite(t))
+        return ls::fail(LS_EVALIDATION, "generator: t must be finite and >= 0");
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    DevBuf tau, out;
+    LS_TRY(ls::upload(tau, &t, sizeof(double), st->compute));
+    LS_TRY(out.alloc(sizeof(double) * static_cast<size_t>(std::max<int64_t>(len, 1)), st->compute));
+    LS_TRY(ls_gen_master(mode, tau.d(), 1, len, h, out.d(), len, st->compute));
+    LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double) * len, cudaMemcpyDeviceToHost, st->compute));
+    LS_CUDA(cudaStreamSynchronize(st->compute));
+    return LS_OK;
+}
+
+int ls_h_lattice_master(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h,
+                        int R, double* f0_h, double* f1_h, double* f2_h) {
+    if (n < 2 || n % 2 != 0 || !(b > 0.0) || !std::isfinite(b))
+        return ls::fail(LS_EVALIDATION, "grid: need b > 0 and even n >= 2");
+    for (int l = 0; l < 3; ++l)
+        if (L[l] < 1) return ls::fail(LS_EVALIDATION, "lattice: cell counts must be >= 1");
+    for (int q = 0; q < R; ++q)
+        if (!(tau_h[q] >= 0.0) || !std::isfinite(tau_h[q]))
+            return ls::fail(LS_EVALIDATION, "generator: exponents must be finite and >= 0");
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    const double h = b / static_cast<double>(n);
+    DevBuf tau;
+    LS_TRY(ls::upload(tau, tau_h, sizeof(double) * R, st->compute));
+    double* outs[3] = {f0_h, f1_h, f2_h};
+    for (int l = 0; l < 3; ++l) {
+        const int64_t len = 2 * L[l] * n;
+        // Axes of equal length share one factor (newton.hpp:60-69).
+        int same = -1;
+        for (int m = 0; m < l; ++m)
+            if (L[m] == L[l]) same = m;
+        if (same >= 0) {
+            LS_CUDA(cudaStreamSynchronize(st->compute));
+            std::memcpy(outs[l], outs[same], sizeof(double) * static_cast<size_t>(len * R));
+            continue;
+        }
+        DevBuf f;
+        LS_TRY(f.alloc(sizeof(double) * static_cast<size_t>(len * R), st->compute));
+        LS_TRY(ls_gen_master(mode, tau.d(), R, len, h, f.d(), len, st->compute));
+        LS_CUDA(cudaMemcpyAsync(outs[l], f.p, sizeof(double) * len * R, cudaMemcpyDeviceToHost, st->compute));
+        LS_CUDA(cudaStreamSynchronize(st->compute));
+    }
+    return LS_OK;
+}
+
+int ls_h_assemble_axis(const double* master_h, int64_t master_len, int R, int M0,
+                       const int64_t* ia_h, int64_t n, int64_t L, int periodic, double* out_h) {
+    if (master_len != 2 * L * n)
+        return ls::fail(LS_EVALIDATION, "lattice: master axis length does not match the doubled target grid");
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    const int64_t out_len = periodic ? n : L * n;
+    DevBuf m, ia, out;
+    LS_TRY(ls::upload(m, master_h, sizeof(double) * master_len * R, st->compute));
+    LS_TRY(ls::upload(ia, ia_h, sizeof(int64_t) * M0, st->compute));
+    LS_TRY(out.alloc(sizeof(double) * out_len * M0 * R, st->compute));
+    LS_TRY(ls_assemble_axis(m.d(), master_len, R, M0, ia.i(), n, L, periodic, out.d(), out_len, st->compute));
+    LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double) * out_len * M0 * R, cudaMemcpyDeviceToHost, st->compute));
+    LS_CUDA(cudaStreamSynchronize(st->compute));
+    return LS_OK;
+}
+
+int ls_h_expand(const int64_t dims[3], int R, const double* A_h, const double* B_h,
+                const double* C_h, const double* w_h, int64_t k0, int64_t k1, double* out_h) {
+    if (k0 < 0 || k1 > dims[2] || k0 > k1) return ls::fail(LS_EVALIDATION, "expand: slab range outside [0, N3]");
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    DevBuf A, B, C, w;
+    LS_TRY(ls::upload(A, A_h, sizeof(double) * dims[0] * R, st->compute));
+    LS_TRY(ls::upload(B, B_h, sizeof(double) * dims[1] * R, st->compute));
+    LS_TRY(ls::upload(C, C_h, sizeof(double) * dims[2] * R, st->compute));
+    LS_TRY(ls::upload(w, w_h, sizeof(double) * R, st->compute));
+    return ls::expand_to_host(A.d(), B.d(), C.d(), w.d(), dims, R, k0, k1, out_h, *st);
+}
+
+int ls_h_eval_points(const int64_t dims[3], int R, const double* A_h, const double* B_h,
+                     const double* C_h, const double* w_h, const int64_t* idx_h, int64_t P,
+                     double* out_h) {
+    for (int64_t p = 0; p < P; ++p)
+        for (int l = 0; l < 3; ++l)
+            if (idx_h[3 * p + l] < 0 || idx_h[3 * p + l] >= dims[l])
+                return ls::fail(LS_EVALIDATION, "eval_point: index out of range");
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    DevBuf A, B, C, w, idx, out;
+    LS_TRY(ls::upload(A, A_h, sizeof(double) * dims[0] * R, st->compute));
+    LS_TRY(ls::upload(B, B_h, sizeof(double) * dims[1] * R, st->compute));
+    LS_TRY(ls::upload(C, C_h, sizeof(double) * dims[2] * R, st->compute));
+    LS_TRY(ls::upload(w, w_h, sizeof(double) * R, st->compute));
+    LS_TRY(ls::upload(idx, idx_h, sizeof(int64_t) * 3 * P, st->compute));
+    LS_TRY(out.alloc(sizeof(double) * P, st->compute));
+    LS_TRY(ls_eval_points(A.d(), dims[0], B.d(), dims[1], C.d(), dims[2], w.d(), R, idx.i(), P, out.d(), st->compute));
+    LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double) * P, cudaMemcpyDeviceToHost, st->compute));
+    LS_CUDA(cudaStreamSynchronize(st->compute));
+    return LS_OK;
+}
+
+int ls_h_scalar_product(const int64_t dims[3], int Ra, const double* A0_h, const double* A1_h,
+                        const double* A2_h, const double* wa_h, int Rb, const double* B0_h,
+                        const double* B1_h, const double* B2_h, const double* wb_h, double* out_h) {
+    if (Ra == 0 || Rb == 0) {
+        *out_h = 0.0;  // canonical.hpp:128
+        return LS_OK;
+    }
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    const double* ah[3] = {A0_h, A1_h, A2_h};
+    const double* bh[3] = {B0_h, B1_h, B2_h};
+    DevBuf a[3], bb[3], G[3], wa, wb, out;
+    for (int l = 0; l < 3; ++l) {
+        LS_TRY(ls::upload(a[l], ah[l], sizeof(double) * dims[l] * Ra, st->compute));
+        LS_TRY(ls::upload(bb[l], bh[l], sizeof(double) * dims[l] * Rb, st->compute));
+        LS_TRY(G[l].alloc(sizeof(double) * static_cast<size_t>(Ra) * Rb, st->compute));
+        LS_TRY(ls_gram(a[l].d(), dims[l], Ra, bb[l].d(), dims[l], Rb, dims[l], G[l].d(), st->compute));
+    }
+    LS_TRY(ls::upload(wa, wa_h, sizeof(double) * Ra, st->compute));
+    LS_TRY(ls::upload(wb, wb_h, sizeof(double) * Rb, st->compute));
+    LS_TRY(out.alloc(sizeof(double), st->compute));
+    LS_TRY(ls_gram_reduce(G[0].d(), G[1].d(), G[2].d(), wa.d(), Ra, wb.d(), Rb, out.d(), st->compute));
+    LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double), cudaMemcpyDeviceToHost, st->compute));
+    LS_CUDA(cudaStreamSynchronize(st->compute));
+    return LS_OK;
+}
+
+int ls_h_grid_functional(const int64_t dims[3], int R, const double* A_h, const double* B_h,
+                         const double* C_h, const double* w_h, const double* r1_h,
+                         const double* r2_h, const double* r3_h, int64_t k0, int64_t k1,
+                         double* out_h) {
+    if (k0 < 0 || k1 > dims[2] || k0 > k1) return ls::fail(LS_EVALIDATION, "functional: slab range outside [0, N3]");
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    DevBuf A, B, C, w, r1, r2, r3, part, out;
+    LS_TRY(ls::upload(A, A_h, sizeof(double) * dims[0] * R, st->compute));
+    LS_TRY(ls::upload(B, B_h, sizeof(double) * dims[1] * R, st->compute));
+    LS_TRY(ls::upload(C, C_h, sizeof(double) * dims[2] * R, st->compute));
+    LS_TRY(ls::upload(w, w_h, sizeof(double) * std::max(R, 1), st->compute));
+    LS_TRY(ls::upload(r1, r1_h, sizeof(double) * dims[0], st->compute));
+    LS_TRY(ls::upload(r2, r2_h, sizeof(double) * dims[1], st->compute));
+    LS_TRY(ls::upload(r3, r3_h, sizeof(double) * dims[2], st->compute));
+    const int64_t np = ls_expand_partial_count(dims[0], dims[1], std::max(R, 4), k0, k1);
+    if (np < 0) return ls::fail(LS_EGUARD, "functional: rank too large");
+    LS_TRY(part.alloc(sizeof(double) * std::max<int64_t>(np, 1), st->compute));
+    LS_TRY(out.alloc(sizeof(double), st->compute));
+    LS_CUDA(cudaMemsetAsync(part.p, 0, sizeof(double) * std::max<int64_t>(np, 1), st->compute));
+    LS_TRY(ls_expand(A.d(), dims[0], B.d(), dims[1], C.d(), dims[2], w.d(), dims[0], dims[1], dims[2], R,
+                     k0, k1, nullptr, 0, 0, r1.d(), r2.d(), r3.d(), part.d(), st->compute));
+    LS_TRY(ls_sum_partials(part.d(), np, out.d(), st->compute));
+    LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double), cudaMemcpyDeviceToHost, st->compute));
+    LS_CUDA(cudaStreamSynchronize(st->compute));
+    return LS_OK;
+}
+
+int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h,
+                           const double* w_h, int R, const double* charges_h, int M0, int periodic,
+                           int64_t k0, int64_t k1, double* grid_h, double* f0_h, double* f1_h,
+                           double* f2_h, double* wout_h) {
+    if (n < 2 || n % 2 != 0 || !(b > 0.0) || !std::isfinite(b))
+        return ls::fail(LS_EVALIDATION, "grid: need b > 0 and even n >= 2");
+    if (M0 < 1) return ls::fail(LS_EVALIDATION, "lattice: at least one charge required");
+    if (R < 1) return ls::fail(LS_EVALIDATION, "lattice: master tensor has rank 0");
+    for (int l = 0; l < 3; ++l)
+        if (L[l] < 1) return ls::fail(LS_EVALIDATION, "lattice: cell counts must be >= 1");
+    // Charge snapping and weights Z_nu * w_q (lattice.hpp:57-68, :284-287) on the host.
+    std::vector<int64_t> ia(static_cast<size_t>(3 * M0));
+    std::vector<double> wt(static_cast<size_t>(M0) * R);
+    for (int nu = 0; nu < M0; ++nu) {
+        const double Z = charges_h[4 * nu + 3];
+        if (!(Z > 0.0) || !std::isfinite(Z))
+            return ls::fail(LS_EVALIDATION, "lattice: charge must have positive finite Z");
+        for (int l = 0; l < 3; ++l)
+            LS_TRY(ls::charge_grid_index(b, n, charges_h[4 * nu + l], ia[static_cast<size_t>(l * M0 + nu)]));
+        for (int q = 0; q < R; ++q) wt[static_cast<size_t>(nu) * R + q] = Z * w_h[q];
+    }
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    const cudaStream_t s = st->compute;
+    const double h = b / static_cast<double>(n);
+    const int Rt = M0 * R;
+    int64_t d[3];
+    for (int l = 0; l < 3; ++l) d[l] = periodic ? n : L[l] * n;
+    if (k0 < 0 || k1 > d[2] || k0 > k1) return ls::fail(LS_EVALIDATION, "lattice potential: slab range outside the grid");
+    DevBuf tau, iad, wd, master[3], fac[3];
+    LS_TRY(ls::upload(tau, tau_h, sizeof(double) * R, s));
+    LS_TRY(ls::upload(iad, ia.data(), sizeof(int64_t) * ia.size(), s));
+    LS_TRY(ls::upload(wd, wt.data(), sizeof(double) * wt.size(), s));
+    const double* fptr[3];
+    double* fh[3] = {f0_h, f1_h, f2_h};
+    for (int l = 0; l < 3; ++l) {
+        // Axes with equal L and equal charge indices yield bit-identical factors.
+        int same = -1;
+        for (int m = 0; m < l && same < 0; ++m)
+            if (L[m] == L[l] &&
+                std::equal(ia.begin() + m * M0, ia.begin() + (m + 1) * M0, ia.begin() + l * M0))
+                same = m;
+        if (same >= 0) {
+            fptr[l] = fptr[same];
+            continue;
+        }
+        const int64_t len = 2 * L[l] * n;
+        LS_TRY(master[l].alloc(sizeof(double) * len * R, s));
+        LS_TRY(ls_gen_master(mode, tau.d(), R, len, h, master[l].d(), len, s));
+        LS_TRY(fac[l].alloc(sizeof(double) * d[l] * Rt, s));
+        LS_TRY(ls_assemble_axis(master[l].d(), len, R, M0, iad.i() + l * M0, n, L[l], periodic,
+                                fac[l].d(), d[l], s));
+        fptr[l] = fac[l].d();
+    }
+    for (int l = 0; l < 3; ++l)
+        if (fh[l]) LS_CUDA(cudaMemcpyAsync(fh[l], fptr[l], sizeof(double) * d[l] * Rt, cudaMemcpyDeviceToHost, s));
+    if (wout_h) std::memcpy(wout_h, wt.data(), sizeof(double) * wt.size());
+    if (grid_h) {
+        LS_TRY(ls::expand_to_host(fptr[0], fptr[1], fptr[2], wd.d(), d, Rt, k0, k1, grid_h, *st));
+    } else {
+        LS_CUDA(cudaStreamSynchronize(s));
+    }
+    return LS_OK;
+}
+
+}  // extern "C"

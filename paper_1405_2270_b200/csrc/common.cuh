@@ -1,0 +1,54 @@
+// common.cuh -- shared plumbing for liblatsum_cuda.so: status codes, the
+// thread-local error message, launch accounting and FP64 helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "latsum_cuda.h"
+
+namespace ls {
+
+std::string& last_error();
+std::atomic<int64_t>& launch_counter();
+
+inline int fail(int code, const std::string& msg) {
+    last_error() = msg;
+    return code;
+}
+inline int cuda_fail(cudaError_t e, const char* where) {
+    return fail(LS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define LS_CUDA(expr)                                                   \
+    do {                                                                \
+        cudaError_t _e = (expr);                                        \
+        if (_e != cudaSuccess) return ::ls::cuda_fail(_e, #expr);       \
+    } while (0)
+
+// After a kernel launch: count it and surface launch-configuration errors.
+#define LS_LAUNCHED(name)                                               \
+    do {                                                                \
+        ::ls::launch_counter().fetch_add(1, std::memory_order_relaxed); \
+        cudaError_t _e = cudaGetLastError();                            \
+        if (_e != cudaSuccess) return ::ls::cuda_fail(_e, name);        \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Number of SMs of the current device (cached per device).
+int sm_count();
+
+}  // namespace ls
+
+// Rounded FP64 primitives that the compiler can never contract into FMA:
+// used wherever the reference's operation order must be reproduced.
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rn_sub(double a, double b) { return __dsub_rn(a, b); }

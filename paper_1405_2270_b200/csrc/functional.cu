@@ -1,0 +1,157 @@
+// functional.cu -- K4: functionals of the canonical tensor and point evaluation.
+//
+// References: scalar_product (canonical.hpp:126-136) = per-axis Gram matrices
+// then a rank-major reduction; potential_matrix (project.hpp:65-97) = batched
+// scalar products against rank-1 Gaussian pairs; eval_point
+// (canonical.hpp:304-314). Dot products use a fixed lane-strided order and a
+// fixed xor tree, so every result is bitwise reproducible run to run.
+#include "common.cuh"
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+__device__ __forceinline__ double warp_dot(const double* __restrict__ x, const double* __restrict__ y,
+                                           int64_t n, int lane) {
+    double s = 0.0;
+    for (int64_t i = lane; i < n; i += 32) s = fma(x[i], y[i], s);
+    return warp_sum(s);
+}
+
+// eval_point: sum += w_q * A(i,q) * B(j,q) * C(k,q), left to right, rank order.
+__global__ void eval_points_kernel(const double* __restrict__ A, int64_t lda,
+                                   const double* __restrict__ B, int64_t ldb,
+                                   const double* __restrict__ C, int64_t ldc,
+                                   const double* __restrict__ w, int R,
+                                   const int64_t* __restrict__ idx, int64_t P,
+                                   double* __restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx[3 * p], j = idx[3 * p + 1], k = idx[3 * p + 2];
+        double sum = 0.0;
+        for (int q = 0; q < R; ++q)
+            sum = rn_add(sum, rn_mul(rn_mul(rn_mul(w[q], A[i + lda * q]), B[j + ldb * q]), C[k + ldc * q]));
+        out[p] = sum;
+    }
+}
+
+// G(x, y) = <X[:, x], Y[:, y]>, one warp per entry.
+__global__ void gram_kernel(const double* __restrict__ X, int64_t ldx, int Rx,
+                            const double* __restrict__ Y, int64_t ldy, int Ry, int64_t n,
+                            double* __restrict__ G) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= (int64_t)Rx * Ry) return;
+    const int x = static_cast<int>(warp % Rx);
+    const int y = static_cast<int>(warp / Rx);
+    const double s = warp_dot(X + ldx * x, Y + ldy * y, n, lane);
+    if (lane == 0) G[x + (int64_t)Rx * y] = s;
+}
+
+// canonical.hpp:131-135: i outer (rank of a), j inner (rank of b).
+__global__ void gram_reduce_kernel(const double* __restrict__ G0, const double* __restrict__ G1,
+                                   const double* __restrict__ G2, const double* __restrict__ wa,
+                                   int Ra, const double* __restrict__ wb, int Rb,
+                                   double* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double sum = 0.0;
+    for (int i = 0; i < Ra; ++i)
+        for (int j = 0; j < Rb; ++j) {
+            const int64_t e = i + (int64_t)Ra * j;
+            sum = rn_add(sum, rn_mul(rn_mul(rn_mul(rn_mul(wa[i], wb[j]), G0[e]), G1[e]), G2[e]));
+        }
+    out[0] = sum;
+}
+
+// One block per density f: 3R Gram entries <P_l[:,q], rho_l[:,f]> by warps into
+// shared memory, then thread 0 forms scale * sum_q ((w_q * 1) * G0) * G1 * G2.
+__global__ void functional_batch_kernel(const double* __restrict__ A, int64_t lda,
+                                        const double* __restrict__ B, int64_t ldb,
+                                        const double* __restrict__ C, int64_t ldc,
+                                        const double* __restrict__ w, int R, int64_t n1,
+                                        int64_t n2, int64_t n3, const double* __restrict__ X,
+                                        int64_t ldx, const double* __restrict__ Y, int64_t ldy,
+                                        const double* __restrict__ Z, int64_t ldz, double scale,
+                                        double* __restrict__ out) {
+    extern __shared__ double gsh[];  // [3][R]
+    const int f = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    for (int e = warp; e < 3 * R; e += nwarps) {
+        const int l = e / R, q = e % R;
+        double s;
+        if (l == 0)
+            s = warp_dot(A + lda * q, X + ldx * f, n1, lane);
+        else if (l == 1)
+            s = warp_dot(B + ldb * q, Y + ldy * f, n2, lane);
+        else
+            s = warp_dot(C + ldc * q, Z + ldz * f, n3, lane);
+        if (lane == 0) gsh[e] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int q = 0; q < R; ++q)
+            sum = rn_add(sum, rn_mul(rn_mul(rn_mul(rn_mul(w[q], 1.0), gsh[q]), gsh[R + q]), gsh[2 * R + q]));
+        out[f] = rn_mul(scale, sum);
+    }
+}
+
+}  // namespace
+
+extern "C" int ls_eval_points(const double* A_d, int64_t lda, const double* B_d, int64_t ldb,
+                              const double* C_d, int64_t ldc, const double* w_d, int R,
+                              const int64_t* idx_d, int64_t P, double* out_d, void* stream) {
+    if (P < 0 || R < 0) return ls::fail(LS_EVALIDATION, "eval_points: negative count");
+    if (P == 0) return LS_OK;
+    const int64_t blocks = std::min<int64_t>(ls::ceil_div(P, 256), 65535);
+    eval_points_kernel<<<(unsigned)blocks, 256, 0, ls::as_stream(stream)>>>(A_d, lda, B_d, ldb, C_d,
+                                                                           ldc, w_d, R, idx_d, P, out_d);
+    LS_LAUNCHED("eval_points_kernel");
+    return LS_OK;
+}
+
+extern "C" int ls_gram(const double* X_d, int64_t ldx, int Rx, const double* Y_d, int64_t ldy,
+                       int Ry, int64_t n, double* G_d, void* stream) {
+    if (Rx < 0 || Ry < 0 || n < 0 || ldx < n || ldy < n)
+        return ls::fail(LS_EVALIDATION, "gram: bad shape");
+    const int64_t warps = (int64_t)Rx * Ry;
+    if (warps == 0) return LS_OK;
+    const int64_t blocks = ls::ceil_div(warps * 32, 256);
+    gram_kernel<<<(unsigned)blocks, 256, 0, ls::as_stream(stream)>>>(X_d, ldx, Rx, Y_d, ldy, Ry, n, G_d);
+    LS_LAUNCHED("gram_kernel");
+    return LS_OK;
+}
+
+extern "C" int ls_gram_reduce(const double* G0_d, const double* G1_d, const double* G2_d,
+                              const double* wa_d, int Ra, const double* wb_d, int Rb,
+                              double* out_d, void* stream) {
+    if (Ra < 0 || Rb < 0) return ls::fail(LS_EVALIDATION, "gram_reduce: negative rank");
+    gram_reduce_kernel<<<1, 32, 0, ls::as_stream(stream)>>>(G0_d, G1_d, G2_d, wa_d, Ra, wb_d, Rb, out_d);
+    LS_LAUNCHED("gram_reduce_kernel");
+    return LS_OK;
+}
+
+extern "C" int ls_functional_batch(const double* A_d, int64_t lda, const double* B_d, int64_t ldb,
+                                   const double* C_d, int64_t ldc, const double* w_d, int R,
+                                   int64_t n1, int64_t n2, int64_t n3, const double* X_d,
+                                   int64_t ldx, const double* Y_d, int64_t ldy, const double* Z_d,
+                                   int64_t ldz, int F, double scale, double* out_d, void* stream) {
+    if (R < 1 || F < 0 || n1 < 1 || n2 < 1 || n3 < 1 || lda < n1 || ldb < n2 || ldc < n3 ||
+        ldx < n1 || ldy < n2 || ldz < n3)
+        return ls::fail(LS_EVALIDATION, "functional_batch: bad shape");
+    if (F == 0) return LS_OK;
+    const size_t smem = sizeof(double) * 3 * static_cast<size_t>(R);
+    if (smem > 200 * 1024) return ls::fail(LS_EGUARD, "functional_batch: rank too large");
+    auto kern = functional_batch_kernel;
+    if (smem > 48 * 1024)
+        LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<F, 256, smem, ls::as_stream(stream)>>>(A_d, lda, B_d, ldb, C_d, ldc, w_d, R, n1, n2, n3, X_d,
+                                                   ldx, Y_d, ldy, Z_d, ldz, scale, out_d);
+    LS_LAUNCHED("functional_batch_kernel");
+    return LS_OK;
+}

@@ -1,0 +1,544 @@
+"""Python mirror of the reference latsum hot-path API (arXiv 1405.2270).
+
+Same names, argument meaning and error behaviour as the reference's C++
+headers (/root/reference/proj/include/latsum/*.hpp, cited per function), so
+parity tests read like the reference's own tests. Every numeric stage runs in
+liblatsum_cuda.so on the GPU; this module only validates, converts layouts
+and calls the C ABI. Factor matrices are numpy arrays of shape (n_l, R) in
+Fortran (column-major) order, exactly Eigen::MatrixXd's layout.
+
+Host-level functions (numpy in, numpy out) go through the synchronous
+``ls_h_*`` entry points. :class:`DevicePipeline` keeps every stage resident in
+HBM (torch tensors as device memory and streams) for the benchmark path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import GEN_ERF, GEN_MIDPOINT, ResourceGuardError, ValidationError, call
+
+DEFAULT_DENSIFY_GUARD = 1 << 27  # canonical.hpp:237
+MODES = {"midpoint": GEN_MIDPOINT, "erf": GEN_ERF}
+
+
+def _p(a: np.ndarray | None):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _f64(a, order="F"):
+    return np.require(np.asarray(a, dtype=np.float64), requirements=[order, "A"])
+
+
+# --------------------------------------------------------------------- grid.hpp
+@dataclass(frozen=True)
+class GridSpec:
+    """grid.hpp:14-36: n x n x n cells over [-b/2, b/2]^3, mesh h = b/n."""
+    b: float
+    n: int
+
+    def __post_init__(self):
+        if not (self.b > 0.0) or not math.isfinite(self.b):
+            raise ValidationError(f"grid: box edge must be positive, got {self.b}")
+        if self.n < 2 or self.n % 2 != 0:
+            raise ValidationError(f"grid: n must be even and at least 2, got {self.n}")
+
+    @property
+    def h(self) -> float:
+        return self.b / float(self.n)
+
+    @staticmethod
+    def midpoint_of(i: int, length: int, h: float) -> float:
+        return (float(i) + 0.5 - float(length) / 2.0) * h
+
+    def midpoint(self, i: int) -> float:
+        return self.midpoint_of(i, self.n, self.h)
+
+
+# --------------------------------------------------------------- quadrature.hpp
+@dataclass
+class QuadratureRule:
+    """quadrature.hpp:20-29."""
+    M: int
+    C0: float
+    step: float
+    nodes: np.ndarray
+    exponents: np.ndarray
+    weights: np.ndarray
+
+    def node_count(self) -> int:
+        return 2 * self.M + 1
+
+
+def sinc_quadrature(eps: float, a_min: float, a_max: float, M: int, C0: float = 1.0) -> QuadratureRule:
+    """quadrature.hpp:50-89 (computed by the library's host code)."""
+    R = 2 * M + 1 if M >= 1 else 1
+    nodes, tau, w = np.zeros(R), np.zeros(R), np.zeros(R)
+    step = C.c_double(0.0)
+    call("ls_sinc_quadrature", eps, a_min, a_max, M, C0, _p(nodes), _p(tau), _p(w), C.byref(step))
+    return QuadratureRule(M, C0, step.value, nodes, tau, w)
+
+
+def quadrature_value(rule: QuadratureRule, r: float) -> float:
+    """quadrature.hpp:93-100 (host scalar; sequential accumulation)."""
+    s = 0.0
+    for t, w in zip(rule.exponents, rule.weights):
+        tr = t * r
+        s += w * math.exp(-tr * tr)
+    return s
+
+
+# --------------------------------------------------------------- canonical.hpp
+class CanonicalTensor3:
+    """canonical.hpp:33-82: entry (i,j,k) = sum_q w_q A1(i,q) A2(j,q) A3(k,q)."""
+
+    def __init__(self, factors: Sequence[np.ndarray], weights: np.ndarray, trusted: bool = False):
+        fs = [_f64(f) for f in factors]
+        w = _f64(weights).ravel()
+        if len(fs) != 3:
+            raise ValidationError("canonical tensor: need three factor matrices")
+        r = w.shape[0]
+        for l, f in enumerate(fs):
+            if f.ndim != 2 or f.shape[1] != r:
+                raise ValidationError(f"canonical tensor: factor {l} has {f.shape[1] if f.ndim == 2 else '?'} "
+                                      f"columns, expected rank {r}")
+            if not trusted and not np.all(np.isfinite(f)):
+                raise ValidationError(f"canonical tensor: factor {l} contains a non-finite value")
+        if not trusted and not np.all(np.isfinite(w)):
+            raise ValidationError("canonical tensor: weights contain a non-finite value")
+        self._f = fs
+        self._w = w
+
+    def rank(self) -> int:
+        return int(self._w.shape[0])
+
+    def dim(self, axis: int) -> int:
+        return int(self._f[axis].shape[0])
+
+    def dims(self) -> tuple[int, int, int]:
+        return (self.dim(0), self.dim(1), self.dim(2))
+
+    def factor(self, axis: int) -> np.ndarray:
+        return self._f[axis]
+
+    def weights(self) -> np.ndarray:
+        return self._w
+
+
+def _dims_arr(t: CanonicalTensor3) -> np.ndarray:
+    return np.array(t.dims(), dtype=np.int64)
+
+
+def densify(t: CanonicalTensor3, guard: int = DEFAULT_DENSIFY_GUARD) -> np.ndarray:
+    """canonical.hpp:251-266: dense (n1, n2, n3) Fortran-ordered grid, computed on the GPU."""
+    d = t.dims()
+    total = d[0] * d[1] * d[2]
+    if total > guard:
+        raise ResourceGuardError(f"densify: {total} entries exceed the guard of {guard}")
+    return expand_slabs(t, 0, d[2])
+
+
+def expand_slabs(t: CanonicalTensor3, k0: int, k1: int, out: np.ndarray | None = None) -> np.ndarray:
+    """densify_slab over slabs [k0, k1) (canonical.hpp:241-246) into host memory (no guard)."""
+    d = t.dims()
+    if out is None:
+        out = np.empty((d[0], d[1], k1 - k0), order="F")
+    assert out.flags["F_CONTIGUOUS"] and out.dtype == np.float64
+    call("ls_h_expand", _p(_dims_arr(t)), t.rank(), _p(t.factor(0)), _p(t.factor(1)), _p(t.factor(2)),
+         _p(t.weights()), k0, k1, _p(out))
+    return out
+
+
+def eval_points(t: CanonicalTensor3, idx: np.ndarray) -> np.ndarray:
+    """eval_point (canonical.hpp:304-314) for a (P, 3) array of indices."""
+    idx = np.ascontiguousarray(idx, dtype=np.int64).reshape(-1, 3)
+    out = np.zeros(idx.shape[0])
+    call("ls_h_eval_points", _p(_dims_arr(t)), t.rank(), _p(t.factor(0)), _p(t.factor(1)), _p(t.factor(2)),
+         _p(t.weights()), _p(idx), idx.shape[0], _p(out))
+    return out
+
+
+def eval_point(t: CanonicalTensor3, i: int, j: int, k: int) -> float:
+    return float(eval_points(t, np.array([[i, j, k]]))[0])
+
+
+def scalar_product(a: CanonicalTensor3, b: CanonicalTensor3) -> float:
+    """canonical.hpp:126-136."""
+    if a.dims() != b.dims():
+        raise ValidationError(f"scalar_product: dimension mismatch {a.dims()} vs {b.dims()}")
+    out = np.zeros(1)
+    call("ls_h_scalar_product", _p(_dims_arr(a)), a.rank(), _p(a.factor(0)), _p(a.factor(1)), _p(a.factor(2)),
+         _p(a.weights()), b.rank(), _p(b.factor(0)), _p(b.factor(1)), _p(b.factor(2)), _p(b.weights()), _p(out))
+    return float(out[0])
+
+
+def grid_functional(t: CanonicalTensor3, rho: Sequence[np.ndarray], k0: int = 0, k1: int | None = None) -> float:
+    """Full-grid sum_{ijk} V(i,j,k) rho1(i) rho2(j) rho3(k) over slabs [k0, k1), V never stored."""
+    k1 = t.dim(2) if k1 is None else k1
+    r = [_f64(x).ravel() for x in rho]
+    out = np.zeros(1)
+    call("ls_h_grid_functional", _p(_dims_arr(t)), t.rank(), _p(t.factor(0)), _p(t.factor(1)), _p(t.factor(2)),
+         _p(t.weights()), _p(r[0]), _p(r[1]), _p(r[2]), k0, k1, _p(out))
+    return float(out[0])
+
+
+# ------------------------------------------------------------------ newton.hpp
+def gaussian_sample_vector(length: int, h: float, t: float) -> np.ndarray:
+    """newton.hpp:43-52 (midpoint samples), one GPU column."""
+    if length < 2 or length % 2 != 0:
+        raise ValidationError("gaussian_sample_vector: length must be even and >= 2")
+    out = np.zeros(length)
+    call("ls_h_gen_column", GEN_MIDPOINT, t, length, h, _p(out))
+    return out
+
+
+def gaussian_moment_vector(grid: GridSpec, t: float, doubled: bool) -> np.ndarray:
+    """newton.hpp:21-37 (erf-difference cell integrals), one GPU column."""
+    if not (t >= 0.0) or not math.isfinite(t):
+        raise ValidationError("gaussian_moment_vector: t must be finite and >= 0")
+    length = 2 * grid.n if doubled else grid.n
+    out = np.zeros(length)
+    call("ls_h_gen_column", GEN_ERF, t, length, grid.h, _p(out))
+    return out
+
+
+def build_newton_master(lens: Sequence[int], h: float, rule: QuadratureRule,
+                        mode: str = "midpoint") -> CanonicalTensor3:
+    """newton.hpp:57-75: rank-R master, axes of equal length share factors."""
+    factors: list[np.ndarray] = []
+    for l, n_l in enumerate(lens):
+        for m in range(l):
+            if lens[m] == n_l:
+                factors.append(factors[m].copy(order="F"))
+                break
+        else:
+            f = np.zeros((n_l, rule.node_count()), order="F")
+            for q, t in enumerate(rule.exponents):
+                f[:, q] = (gaussian_sample_vector(n_l, h, float(t)) if mode == "midpoint"
+                           else gaussian_moment_vector(GridSpec(n_l * h, n_l), float(t), False))
+            factors.append(f)
+    return CanonicalTensor3(factors, rule.weights.copy())
+
+
+# ----------------------------------------------------------------- lattice.hpp
+@dataclass
+class Charge:
+    """lattice.hpp:21-24."""
+    pos: tuple[float, float, float] = (0.0, 0.0, 0.0)
+    Z: float = 1.0
+
+
+@dataclass
+class LatticeSpec:
+    """lattice.hpp:28-69."""
+    L: tuple[int, int, int] = (1, 1, 1)
+    unit: GridSpec = field(default_factory=lambda: GridSpec(1.0, 2))
+    charges: list[Charge] = field(default_factory=list)
+
+    def validate(self) -> None:
+        for l in range(3):
+            if self.L[l] < 1:
+                raise ValidationError(f"lattice: cell count on axis {l} must be >= 1")
+        if not self.charges:
+            raise ValidationError("lattice: at least one charge required")
+        for nu, c in enumerate(self.charges):
+            if not (c.Z > 0.0) or not math.isfinite(c.Z):
+                raise ValidationError(f"lattice: charge {nu} must have positive finite Z")
+            for l in range(3):
+                self.charge_grid_index(l, nu)
+
+    def target_cells(self, axis: int) -> int:
+        return self.L[axis] * self.unit.n
+
+    def target_dims(self) -> tuple[int, int, int]:
+        return (self.target_cells(0), self.target_cells(1), self.target_cells(2))
+
+    def charge_count(self) -> int:
+        return len(self.charges)
+
+    def cell_count(self) -> int:
+        return self.L[0] * self.L[1] * self.L[2]
+
+    def charge_grid_index(self, axis: int, nu: int) -> int:
+        h = self.unit.h
+        p = self.charges[nu].pos[axis]
+        x = (p + self.unit.b / 2.0) / h
+        r = float(np.round(x))  # half-away vs half-even only differs off-grid (rejected below)
+        if abs(x - r) > 1e-9 * self.unit.n or r < 0.0 or r > self.unit.n:
+            raise ValidationError(f"lattice: charge {nu} coordinate {p} on axis {axis} does not lie on a grid "
+                                  "point of the unit cell")
+        return int(r)
+
+
+def window_start_box(N: int, n: int, i_a: int, k: int) -> int:
+    """lattice.hpp:98."""
+    return N - i_a - k * n
+
+
+def window_start_periodic(N: int, n: int, i_a: int, k: int, L: int) -> int:
+    """lattice.hpp:104-106."""
+    return N + (L // 2 - k) * n - i_a
+
+
+def build_lattice_master(spec: LatticeSpec, rule: QuadratureRule, mode: str = "midpoint") -> CanonicalTensor3:
+    """lattice.hpp:109-113 (mode='midpoint', the reference); mode='erf' is the BASELINE
+    erf-difference generator on the same doubled target grid."""
+    spec.validate()
+    L = np.array(spec.L, dtype=np.int64)
+    R = rule.node_count()
+    f = [np.zeros((2 * spec.target_cells(l), R), order="F") for l in range(3)]
+    tau = _f64(rule.exponents).ravel()
+    call("ls_h_lattice_master", MODES[mode], _p(L), spec.unit.n, spec.unit.b, _p(tau), R, _p(f[0]), _p(f[1]),
+         _p(f[2]))
+    return CanonicalTensor3(f, rule.weights.copy(), trusted=True)
+
+
+@dataclass
+class SumResult:
+    """lattice.hpp:130-135."""
+    tensor: CanonicalTensor3
+    grid_dims: tuple[int, int, int]
+    rank: int
+    time_ms: float
+
+
+def _require_master_matches(spec: LatticeSpec, master: CanonicalTensor3) -> None:
+    """lattice.hpp:139-148."""
+    N = spec.target_dims()
+    for l in range(3):
+        if master.dim(l) != 2 * N[l]:
+            raise ValidationError(f"lattice: master axis {l} has {master.dim(l)} cells, expected doubled target "
+                                  f"grid {2 * N[l]}")
+    if master.rank() < 1:
+        raise ValidationError("lattice: master tensor has rank 0")
+
+
+def assembled_axis_columns(spec: LatticeSpec, master: CanonicalTensor3, axis: int, periodic: bool) -> np.ndarray:
+    """lattice.hpp:220-274 on the GPU (bit-identical ascending-k adds)."""
+    n = spec.unit.n
+    Ll = spec.L[axis]
+    out_len = n if periodic else Ll * n
+    R = master.rank()
+    ia = np.array([spec.charge_grid_index(axis, nu) for nu in range(spec.charge_count())], dtype=np.int64)
+    out = np.zeros((out_len, spec.charge_count() * R), order="F")
+    call("ls_h_assemble_axis", _p(master.factor(axis)), master.dim(axis), R, spec.charge_count(), _p(ia), n, Ll,
+         int(periodic), _p(out))
+    return out
+
+
+def _assembled_sum(spec: LatticeSpec, master: CanonicalTensor3, periodic: bool) -> SumResult:
+    """lattice.hpp:276-296."""
+    import time
+    t0 = time.perf_counter()
+    spec.validate()
+    _require_master_matches(spec, master)
+    R = master.rank()
+    factors = [assembled_axis_columns(spec, master, l, periodic) for l in range(3)]
+    w = np.array([c.Z * wq for c in spec.charges for wq in master.weights()])
+    t = CanonicalTensor3(factors, w, trusted=True)
+    n = spec.unit.n
+    dims = (n, n, n) if periodic else spec.target_dims()
+    return SumResult(t, dims, t.rank(), (time.perf_counter() - t0) * 1e3)
+
+
+def assembled_box_sum(spec: LatticeSpec, master: CanonicalTensor3) -> SumResult:
+    """lattice.hpp:303-305."""
+    return _assembled_sum(spec, master, False)
+
+
+def assembled_periodic_sum(spec: LatticeSpec, master: CanonicalTensor3) -> SumResult:
+    """lattice.hpp:310-312."""
+    return _assembled_sum(spec, master, True)
+
+
+def lattice_potential(spec: LatticeSpec, rule: QuadratureRule, mode: str = "erf", periodic: bool = False,
+                      k0: int = 0, k1: int | None = None, out: np.ndarray | None = None,
+                      return_factors: bool = False):
+    """End-to-end: generator -> assembled sum -> expansion of slabs [k0, k1) into host memory,
+    one C-ABI call (ls_h_lattice_potential). `out` may be a pinned buffer."""
+    spec.validate()
+    n = spec.unit.n
+    dims = (n, n, n) if periodic else spec.target_dims()
+    k1 = dims[2] if k1 is None else k1
+    if out is None:
+        out = np.empty((dims[0], dims[1], k1 - k0), order="F")
+    M0, R = spec.charge_count(), rule.node_count()
+    ch = np.array([[*c.pos, c.Z] for c in spec.charges], dtype=np.float64)
+    L = np.array(spec.L, dtype=np.int64)
+    f = [np.zeros((dims[l], M0 * R), order="F") for l in range(3)] if return_factors else [None] * 3
+    wout = np.zeros(M0 * R)
+    call("ls_h_lattice_potential", MODES[mode], _p(L), n, spec.unit.b, _p(_f64(rule.exponents).ravel()),
+         _p(_f64(rule.weights).ravel()), R, _p(ch), M0, int(periodic), k0, k1, _p(out), _p(f[0]), _p(f[1]),
+         _p(f[2]), _p(wout))
+    if return_factors:
+        return out, CanonicalTensor3(f, wout, trusted=True)
+    return out
+
+
+# ----------------------------------------------------------------- project.hpp
+@dataclass
+class GaussianBasisSpec:
+    """project.hpp:15-18."""
+    center: tuple[float, float, float] = (0.0, 0.0, 0.0)
+    sigma: float = 1.0
+
+
+def sample_gaussian_basis(grid: GridSpec, specs: Sequence[GaussianBasisSpec]) -> list[list[np.ndarray]]:
+    """project.hpp:30-57 (host; n samples per axis per function)."""
+    if not specs:
+        raise ValidationError("basis: at least one function required")
+    mids = (np.arange(grid.n, dtype=np.float64) + 0.5 - grid.n / 2.0) * grid.h
+    out = []
+    for f, s in enumerate(specs):
+        if not (s.sigma > 0.0) or not math.isfinite(s.sigma):
+            raise ValidationError(f"basis: function {f} needs positive finite sigma")
+        axes = []
+        for l in range(3):
+            if not math.isfinite(s.center[l]):
+                raise ValidationError(f"basis: function {f} has a non-finite center")
+            d = mids - s.center[l]
+            axes.append(np.exp(-d * d / (2.0 * s.sigma * s.sigma)))
+        out.append(axes)
+    return out
+
+
+def functional_batch(P: CanonicalTensor3, rho: Sequence[np.ndarray], scale: float = 1.0) -> np.ndarray:
+    """scale * scalar_product(P, rho_f) for F rank-1 densities; rho = (X, Y, Z) each (n_l, F)."""
+    import torch
+    dev = torch.device("cuda")
+    X, Y, Z = (torch.as_tensor(_f64(r), device=dev) for r in rho)
+    F = X.shape[1]
+    out = DevicePipeline.functional_batch_device(
+        [torch.as_tensor(P.factor(l), device=dev) for l in range(3)],
+        torch.as_tensor(P.weights(), device=dev), [X, Y, Z], scale)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()[:F]
+
+
+# ---------------------------------------------------------- device pipeline
+class DevicePipeline:
+    """Generator -> assembly -> expansion with every stage resident in HBM.
+
+    Device memory and streams come from torch (plumbing only); all compute is
+    liblatsum_cuda.so. Factors are kept as (R, len) row-major tensors, i.e.
+    column-major (len x R) matrices with leading dimension len.
+    """
+
+    def __init__(self, spec: LatticeSpec, rule: QuadratureRule, mode: str = "erf", periodic: bool = False,
+                 device=None):
+        import torch
+        spec.validate()
+        self.torch = torch
+        self.spec, self.rule, self.mode, self.periodic = spec, rule, mode, periodic
+        self.dev = torch.device("cuda") if device is None else torch.device(device)
+        n = spec.unit.n
+        self.h = spec.unit.h
+        self.R = rule.node_count()
+        self.M0 = spec.charge_count()
+        self.Rt = self.M0 * self.R
+        self.dims = (n, n, n) if periodic else spec.target_dims()
+        t = lambda a, dt=torch.float64: torch.as_tensor(np.asarray(a), dtype=dt, device=self.dev)  # noqa: E731
+        self.tau = t(rule.exponents)
+        self.w = t([c.Z * wq for c in spec.charges for wq in rule.weights])
+        self.ia = [t([spec.charge_grid_index(l, nu) for nu in range(self.M0)], torch.int64) for l in range(3)]
+        # Distinct axes (equal L and equal charge indices give bit-identical factors).
+        self.axis_src = []
+        for l in range(3):
+            src = l
+            for m in range(l):
+                if spec.L[m] == spec.L[l] and torch.equal(self.ia[m], self.ia[l]):
+                    src = m
+                    break
+            self.axis_src.append(src)
+        self.master = [torch.empty((self.R, 2 * spec.L[l] * n), dtype=torch.float64, device=self.dev)
+                       if self.axis_src[l] == l else None for l in range(3)]
+        self.fac = [torch.empty((self.Rt, self.dims[l]), dtype=torch.float64, device=self.dev)
+                    if self.axis_src[l] == l else None for l in range(3)]
+        self.launches = 0
+
+    @staticmethod
+    def _ptr(x):
+        return C.c_void_p(x.data_ptr()) if x is not None else None
+
+    def factor(self, l):
+        return self.fac[self.axis_src[l]]
+
+    def _stream(self, stream):
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.dev)
+        return C.c_void_p(s.cuda_stream)
+
+    def generate(self, stream=None):
+        s = self._stream(stream)
+        for l in range(3):
+            if self.master[l] is not None:
+                length = self.master[l].shape[1]
+                call("ls_gen_master", MODES[self.mode], self._ptr(self.tau), self.R, length, self.h,
+                     self._ptr(self.master[l]), length, s)
+                self.launches += 1
+
+    def assemble(self, stream=None):
+        s = self._stream(stream)
+        n = self.spec.unit.n
+        for l in range(3):
+            if self.fac[l] is not None:
+                call("ls_assemble_axis", self._ptr(self.master[l]), self.master[l].shape[1], self.R, self.M0,
+                     self._ptr(self.ia[l]), n, self.spec.L[l], int(self.periodic), self._ptr(self.fac[l]),
+                     self.dims[l], s)
+                self.launches += 1
+
+    def expand(self, out, k0=0, k1=None, stream=None, rho=None, partial=None):
+        """Writes slabs [k0, k1) into `out` (a (k1-k0, N2, N1) float64 tensor) or, with rho, only
+        the per-unit functional partials."""
+        k1 = self.dims[2] if k1 is None else k1
+        N1, N2, N3 = self.dims
+        A, B, Cf = (self.factor(l) for l in range(3))
+        r = rho if rho is not None else (None, None, None)
+        call("ls_expand", self._ptr(A), N1, self._ptr(B), N2, self._ptr(Cf), N3, self._ptr(self.w), N1, N2, N3,
+             self.Rt, k0, k1, self._ptr(out), 0, 0, self._ptr(r[0]), self._ptr(r[1]), self._ptr(r[2]),
+             self._ptr(partial), self._stream(stream))
+        self.launches += 1
+
+    def step(self, out, k0=0, k1=None, stream=None):
+        """One pass of the hot path: generate, assemble, expand into `out`."""
+        self.generate(stream)
+        self.assemble(stream)
+        self.expand(out, k0, k1, stream)
+
+    def partial_count(self, k0=0, k1=None):
+        k1 = self.dims[2] if k1 is None else k1
+        return int(_abi.load().ls_expand_partial_count(self.dims[0], self.dims[1], self.Rt, k0, k1))
+
+    def grid_functional(self, rho, k0=0, k1=None, stream=None):
+        """sum V*rho over slabs [k0, k1) fused into the expansion (V not stored); returns a
+        1-element device tensor."""
+        torch = self.torch
+        npart = self.partial_count(k0, k1)
+        partial = torch.zeros(max(npart, 1), dtype=torch.float64, device=self.dev)
+        out = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.expand(None, k0, k1, stream, rho=rho, partial=partial)
+        call("ls_sum_partials", self._ptr(partial), npart, self._ptr(out), self._stream(stream))
+        self.launches += 1
+        return out
+
+    @staticmethod
+    def functional_batch_device(factors, w, rho, scale=1.0, stream=None):
+        """scale * scalar_product(P, rho_f) for every column f of rho = (X, Y, Z) (device tensors,
+        X is (n1, F) column-major i.e. a (F, n1) row-major tensor or a Fortran-ordered view)."""
+        import torch
+        X, Y, Z = rho
+        F = X.shape[1]
+        Xt, Yt, Zt = (r.T.contiguous() for r in (X, Y, Z))  # (F, n) rows = columns
+        ft = [f.T.contiguous() if f.shape[0] != w.shape[0] else f for f in factors]  # (R, n)
+        R = w.shape[0]
+        n = [ft[l].shape[1] for l in range(3)]
+        out = torch.zeros(F, dtype=torch.float64, device=w.device)
+        s = stream if stream is not None else torch.cuda.current_stream(w.device)
+        p = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+        call("ls_functional_batch", p(ft[0]), n[0], p(ft[1]), n[1], p(ft[2]), n[2], p(w), R, n[0], n[1], n[2],
+             p(Xt), n[0], p(Yt), n[1], p(Zt), n[2], F, float(scale), p(out), C.c_void_p(s.cuda_stream))
+        return out
