@@ -36,9 +36,6 @@ constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kTM = 4;            // j tiles (of 8) per warp
 constexpr int kTN = 4;            // i tiles (of 8) per warp
-// k-steps (of 4 ranks) per staged K-chunk of A2: the whole rank-41 operand in
-// one chunk for the wide tile, short chunks for the narrow large-rank tile.
-template <int WI> __host__ __device__ constexpr int kc_of() { return WI == 4 ? 11 : 4; }
 
 struct ExpandArgs {
     const double* A;
@@ -47,7 +44,9 @@ struct ExpandArgs {
     const double* w;
     int64_t lda, ldb, ldc;
     int64_t N1, N2, N3;
-    int R, KS;        // rank, k-steps = ceil(R/4)
+    int R;            // rank
+    int KD;           // DMMA k-steps (4 ranks each); ranks >= 4*KD go to the DFMA tail
+    int n_tail;       // R - 4*KD in {0, 1, 2}, or 0 when the last k-step is zero-padded
     int64_t k0, k1;
     double* out;
     int64_t ldy, ldz;
@@ -58,8 +57,6 @@ struct ExpandArgs {
     double* partial;
     int64_t n_ichunks;
     int64_t n_units;
-    int64_t n_jchunks;
-    int n_kchunks;
 };
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -68,52 +65,22 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                  : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async_8(double* smem_dst, const double* gmem_src, bool valid) {
-    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-    const int src_bytes = valid ? 8 : 0;  // 0 -> zero-fill
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(gmem_src),
-                 "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
-
-// Stage s of the A2 pipeline: j-chunk jc = s / n_kchunks, K-chunk kc = s % n_kchunks.
-// Shared layout [jt][ks][lane], lane = g*4 + t <-> A2(jc*JC + jt*8 + g, (kc*KC + ks)*4 + t).
-template <int WI>
-__device__ __forceinline__ void issue_b_stage(const ExpandArgs& p, double* bs, int64_t stage) {
-    constexpr int JC = 8 * kTM * (kWarps / WI);
-    constexpr int kKC = kc_of<WI>();
-    const int64_t jc = stage / p.n_kchunks;
-    const int kc = static_cast<int>(stage % p.n_kchunks);
-    constexpr int kElems = JC * kKC * 4;
-    for (int e = threadIdx.x; e < kElems; e += kThreads) {
-        const int lane = e & 31;
-        const int ks = (e >> 5) % kKC;
-        const int jt = (e >> 5) / kKC;
-        const int64_t j = jc * JC + jt * 8 + (lane >> 2);
-        const int q = (kc * kKC + ks) * 4 + (lane & 3);
-        const bool valid = j < p.N2 && q < p.R;
-        const double* src = valid ? p.B + j + p.ldb * q : p.B;
-        cp_async_8(bs + e, src, valid);
-    }
-    cp_async_commit();
+// A2 fragment element for lane (g, t) of j-tile starting at j, k-step ks: A2(j + g, 4 ks + t).
+__device__ __forceinline__ double load_b_frag(const ExpandArgs& p, int64_t j, int q) {
+    return (j < p.N2 && q < p.R) ? __ldg(p.B + j + p.ldb * q) : 0.0;
 }
 
 template <int WI, bool STORE, bool FUNC>
-__global__ void __launch_bounds__(kThreads, (WI == 4) ? 2 : 1)
+__global__ void __launch_bounds__(kThreads, 2)
 expand_dmma_kernel(const ExpandArgs p) {
     constexpr int WJ = kWarps / WI;
     constexpr int IC = 8 * kTN * WI;
-    constexpr int JC = 8 * kTM * WJ;
-    constexpr int kKC = kc_of<WI>();
-    constexpr int kBStage = JC * kKC * 4;
 
     extern __shared__ __align__(16) double smem[];
-    const int KS = p.KS;
-    double* as = smem;                              // [IC/8][KS][32]
-    double* bs = as + static_cast<int64_t>(IC) * KS * 4;  // [2][JC/8][KC][32]
-    double* scale = bs + 2 * kBStage;               // [KS*4]
+    const int KD = p.KD;
+    double* as = smem;                                       // [IC/8][KD][32] fragment order
+    double* tail = as + static_cast<int64_t>(IC) * KD * 4;   // [n_tail][IC]
+    double* scale = tail + 2 * IC;                           // [4*KD + n_tail]
     __shared__ double red[kWarps];
 
     const int warp = threadIdx.x >> 5;
@@ -122,7 +89,8 @@ expand_dmma_kernel(const ExpandArgs p) {
     const int t = lane & 3;
     const int wi = warp % WI;
     const int wj = warp / WI;
-    const int64_t n_stages = p.n_jchunks * p.n_kchunks;
+    const int q_tail0 = 4 * KD;
+    const int n_scale = q_tail0 + p.n_tail;
 
     for (int64_t unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
         const int64_t ic = unit % p.n_ichunks;
@@ -130,95 +98,113 @@ expand_dmma_kernel(const ExpandArgs p) {
         const int64_t k = p.k0 + kk;
         const int64_t i_base = ic * IC;
 
-        __syncthreads();  // previous unit finished reading as / bs
-        // First A2 stage of this unit goes out before the A1k fill so the two overlap.
-        issue_b_stage<WI>(p, bs, 0);
+        __syncthreads();  // previous unit finished reading as / tail / scale
         // scale_q = w_q * A3(k, q)   (canonical.hpp:244)
-        for (int q = threadIdx.x; q < KS * 4; q += kThreads)
+        for (int q = threadIdx.x; q < n_scale; q += kThreads)
             scale[q] = q < p.R ? rn_mul(p.w[q], p.C[k + p.ldc * q]) : 0.0;
         __syncthreads();
-        // as = A1(i, q) * scale_q in fragment order (Eigen's A1 * scale.asDiagonal()).
-        for (int e = threadIdx.x; e < IC * KS * 4; e += kThreads) {
+        // A1k(i, q) = A1(i, q) * scale_q, Eigen's A1 * scale.asDiagonal(): DMMA part in fragment
+        // order (lane (g, t) of i-tile it, k-step ks <-> A1k(8 it + g, 4 ks + t)), tail row-wise.
+        for (int e = threadIdx.x; e < IC * KD * 4; e += kThreads) {
             const int ln = e & 31;
-            const int ks = (e >> 5) % KS;
-            const int it = (e >> 5) / KS;
+            const int ks = (e >> 5) % KD;
+            const int it = (e >> 5) / KD;
             const int64_t i = i_base + it * 8 + (ln >> 2);
             const int q = ks * 4 + (ln & 3);
             as[e] = (i < p.N1 && q < p.R) ? rn_mul(p.A[i + p.lda * q], scale[q]) : 0.0;
         }
+        for (int e = threadIdx.x; e < p.n_tail * IC; e += kThreads) {
+            const int q = q_tail0 + e / IC;
+            const int64_t i = i_base + e % IC;
+            tail[e] = i < p.N1 ? rn_mul(p.A[i + p.lda * q], scale[q]) : 0.0;
+        }
+        __syncthreads();
 
         double fsum = 0.0;  // FUNC: this thread's rho-weighted partial over the unit
-        double acc[kTM][kTN][2];
+        const double* asw = as + (wi * kTN) * (KD * 32) + lane;
+        const int64_t ibase = i_base + wi * (8 * kTN);
 
-        for (int64_t st = 0; st < n_stages; ++st) {
-            const int buf = static_cast<int>(st & 1);
-            const int kc = static_cast<int>(st % p.n_kchunks);
-            const int64_t jc = st / p.n_kchunks;
-            if (st + 1 < n_stages) {
-                issue_b_stage<WI>(p, bs + (buf ^ 1) * kBStage, st + 1);
-                cp_async_wait_1();
-            } else {
-                cp_async_wait_all();
-            }
-            __syncthreads();
+        // Each warp sweeps its own j-blocks: no block-level synchronisation until the next unit.
+        for (int64_t jb = static_cast<int64_t>(wj) * (8 * kTM); jb < p.N2; jb += WJ * (8 * kTM)) {
+            double acc[kTM][kTN][2];
+#pragma unroll
+            for (int m = 0; m < kTM; ++m)
+#pragma unroll
+                for (int nn = 0; nn < kTN; ++nn) acc[m][nn][0] = acc[m][nn][1] = 0.0;
 
-            if (kc == 0) {
+            // Register double-buffering: fragments of k-step ks+1 load while ks multiplies.
+            double a_nx[kTM], b_nx[kTN];
 #pragma unroll
-                for (int m = 0; m < kTM; ++m)
+            for (int m = 0; m < kTM; ++m) a_nx[m] = load_b_frag(p, jb + 8 * m + g, t);
 #pragma unroll
-                    for (int nn = 0; nn < kTN; ++nn) acc[m][nn][0] = acc[m][nn][1] = 0.0;
-            }
-            const double* bsb = bs + buf * kBStage + (wj * kTM) * (kKC * 32) + lane;
-            const double* asb = as + (wi * kTN) * (KS * 32) + (kc * kKC) * 32 + lane;
-            const int ks_len = min(kKC, KS - kc * kKC);
-#pragma unroll 1
-            for (int ks = 0; ks < ks_len; ++ks) {
+            for (int nn = 0; nn < kTN; ++nn) b_nx[nn] = asw[nn * (KD * 32)];
+#pragma unroll 2
+            for (int ks = 0; ks < KD; ++ks) {
                 double a[kTM], b[kTN];
 #pragma unroll
-                for (int m = 0; m < kTM; ++m) a[m] = bsb[m * (kKC * 32) + ks * 32];
+                for (int m = 0; m < kTM; ++m) a[m] = a_nx[m];
 #pragma unroll
-                for (int nn = 0; nn < kTN; ++nn) b[nn] = asb[nn * (KS * 32) + ks * 32];
+                for (int nn = 0; nn < kTN; ++nn) b[nn] = b_nx[nn];
+                if (ks + 1 < KD) {
+#pragma unroll
+                    for (int m = 0; m < kTM; ++m) a_nx[m] = load_b_frag(p, jb + 8 * m + g, 4 * (ks + 1) + t);
+#pragma unroll
+                    for (int nn = 0; nn < kTN; ++nn) b_nx[nn] = asw[nn * (KD * 32) + (ks + 1) * 32];
+                }
 #pragma unroll
                 for (int m = 0; m < kTM; ++m)
 #pragma unroll
                     for (int nn = 0; nn < kTN; ++nn) dmma_884(acc[m][nn][0], acc[m][nn][1], a[m], b[nn]);
             }
-
-            if (kc == p.n_kchunks - 1) {
-                // Epilogue for this j-chunk: lane owns (j = jbase + 8m + g, i = ibase + 8nn + 2t + {0,1}).
-                const int64_t jbase = jc * JC + wj * (8 * kTM);
-                const int64_t ibase = i_base + wi * (8 * kTN);
+            // Rank remainder (R mod 4 <= 2) on the DFMA path instead of a zero-padded k-step:
+            // lane (g, t) owns V(i = ibase + 8 nn + 2t + {0,1}, j = jb + 8 m + g).
+            for (int qt = 0; qt < p.n_tail; ++qt) {
+                const int q = q_tail0 + qt;
+                double bt[kTM];
 #pragma unroll
-                for (int m = 0; m < kTM; ++m) {
-                    const int64_t j = jbase + 8 * m + g;
-                    if (j >= p.N2) continue;
-                    double* row = STORE ? p.out + kk * p.ldz + j * p.ldy : nullptr;
-                    double r2 = 0.0;
-                    if (FUNC) r2 = p.rho2[j];
+                for (int m = 0; m < kTM; ++m) bt[m] = load_b_frag(p, jb + 8 * m + g, q);
 #pragma unroll
-                    for (int nn = 0; nn < kTN; ++nn) {
-                        const int64_t i = ibase + 8 * nn + 2 * t;
-                        if (i + 1 < p.N1) {
-                            if (STORE) {
-                                if (p.vec_store) {
-                                    __stcs(reinterpret_cast<double2*>(row + i),
-                                           make_double2(acc[m][nn][0], acc[m][nn][1]));
-                                } else {
-                                    row[i] = acc[m][nn][0];
-                                    row[i + 1] = acc[m][nn][1];
-                                }
-                            }
-                            if (FUNC)
-                                fsum += rn_mul(rn_mul(acc[m][nn][0], p.rho1[i]), r2) +
-                                        rn_mul(rn_mul(acc[m][nn][1], p.rho1[i + 1]), r2);
-                        } else if (i < p.N1) {
-                            if (STORE) row[i] = acc[m][nn][0];
-                            if (FUNC) fsum += rn_mul(rn_mul(acc[m][nn][0], p.rho1[i]), r2);
-                        }
+                for (int nn = 0; nn < kTN; ++nn) {
+                    const double2 at = *reinterpret_cast<const double2*>(
+                        tail + qt * IC + wi * (8 * kTN) + 8 * nn + 2 * t);
+#pragma unroll
+                    for (int m = 0; m < kTM; ++m) {
+                        acc[m][nn][0] = fma(at.x, bt[m], acc[m][nn][0]);
+                        acc[m][nn][1] = fma(at.y, bt[m], acc[m][nn][1]);
                     }
                 }
             }
-            __syncthreads();  // everyone done with bs[buf] before it is refilled
+
+            // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
+#pragma unroll
+            for (int m = 0; m < kTM; ++m) {
+                const int64_t j = jb + 8 * m + g;
+                if (j >= p.N2) continue;
+                double* row = STORE ? p.out + kk * p.ldz + j * p.ldy : nullptr;
+                double r2 = 0.0;
+                if (FUNC) r2 = p.rho2[j];
+#pragma unroll
+                for (int nn = 0; nn < kTN; ++nn) {
+                    const int64_t i = ibase + 8 * nn + 2 * t;
+                    if (i + 1 < p.N1) {
+                        if (STORE) {
+                            if (p.vec_store) {
+                                __stcs(reinterpret_cast<double2*>(row + i),
+                                       make_double2(acc[m][nn][0], acc[m][nn][1]));
+                            } else {
+                                row[i] = acc[m][nn][0];
+                                row[i + 1] = acc[m][nn][1];
+                            }
+                        }
+                        if (FUNC)
+                            fsum += rn_mul(rn_mul(acc[m][nn][0], p.rho1[i]), r2) +
+                                    rn_mul(rn_mul(acc[m][nn][1], p.rho1[i + 1]), r2);
+                    } else if (i < p.N1) {
+                        if (STORE) row[i] = acc[m][nn][0];
+                        if (FUNC) fsum += rn_mul(rn_mul(acc[m][nn][0], p.rho1[i]), r2);
+                    }
+                }
+            }
         }
 
         if (FUNC) {
@@ -251,35 +237,43 @@ __global__ void sum_partials_kernel(const double* __restrict__ part, int64_t cou
     if (threadIdx.x == 0) out[0] = sh[0];
 }
 
-template <int WI>
-size_t smem_bytes(int KS) {
-    constexpr int IC = 8 * kTN * WI;
-    constexpr int JC = 8 * kTM * (kWarps / WI);
-    return sizeof(double) * (static_cast<size_t>(IC) * KS * 4 + 2 * static_cast<size_t>(JC) * kc_of<WI>() * 4 +
-                             static_cast<size_t>(KS) * 4);
+// DMMA k-steps and DFMA tail for rank R: a remainder of 1 or 2 ranks is cheaper on DFMA
+// (2 FMA-lanes per output each) than a zero-padded 4-rank DMMA step.
+void split_rank(int R, int& KD, int& n_tail) {
+    KD = R / 4;
+    n_tail = R % 4;
+    if (n_tail == 3) {
+        KD += 1;
+        n_tail = 0;
+    }
 }
 
-// Shared-memory budget per CTA (B200: 227 KB opt-in).
+template <int WI>
+size_t smem_bytes(int KD) {
+    constexpr int IC = 8 * kTN * WI;
+    return sizeof(double) * (static_cast<size_t>(IC) * KD * 4 + 2 * static_cast<size_t>(IC) +
+                             static_cast<size_t>(KD) * 4 + 4);
+}
+
+// Shared-memory budget per CTA (B200: 227 KB opt-in; two CTAs per SM share 228 KB).
 constexpr size_t kSmemLimit = 227 * 1024;
 
-int choose_wi(int KS) {
-    if (smem_bytes<4>(KS) * 2 <= kSmemLimit) return 4;  // two CTAs per SM
-    if (smem_bytes<1>(KS) <= kSmemLimit) return 1;
+int choose_wi(int KD) {
+    if (smem_bytes<4>(KD) * 2 <= kSmemLimit - 2048) return 4;  // two CTAs per SM
+    if (smem_bytes<1>(KD) * 2 <= kSmemLimit - 2048) return 1;
+    if (smem_bytes<1>(KD) <= kSmemLimit) return 1;
     return 0;
 }
 
 template <int WI, bool STORE, bool FUNC>
 int launch(ExpandArgs& a, cudaStream_t s) {
     constexpr int IC = 8 * kTN * WI;
-    constexpr int JC = 8 * kTM * (kWarps / WI);
     a.n_ichunks = ls::ceil_div(a.N1, IC);
-    a.n_jchunks = ls::ceil_div(a.N2, JC);
-    a.n_kchunks = static_cast<int>(ls::ceil_div(a.KS, kc_of<WI>()));
     a.n_units = a.n_ichunks * (a.k1 - a.k0);
-    const size_t smem = smem_bytes<WI>(a.KS);
+    const size_t smem = smem_bytes<WI>(a.KD);
     auto kern = expand_dmma_kernel<WI, STORE, FUNC>;
     LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int per_sm = (WI == 4) ? 2 : 1;
+    const int per_sm = (2 * smem + 2048 <= kSmemLimit) ? 2 : 1;
     const int64_t grid = std::min<int64_t>(a.n_units, (int64_t)ls::sm_count() * per_sm);
     if (grid <= 0) return LS_OK;
     kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
@@ -291,8 +285,9 @@ int launch(ExpandArgs& a, cudaStream_t s) {
 
 extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_t k0, int64_t k1) {
     (void)N2;
-    const int KS = static_cast<int>(ls::ceil_div(R, 4));
-    const int wi = choose_wi(KS);
+    int KD, n_tail;
+    split_rank(std::max(R, 1), KD, n_tail);
+    const int wi = choose_wi(KD);
     if (wi == 0 || k1 < k0) return -1;
     const int64_t IC = 8 * kTN * wi;
     return ls::ceil_div(N1, IC) * (k1 - k0);
@@ -328,12 +323,13 @@ extern "C" int ls_expand(const double* A_d, int64_t lda, const double* B_d, int6
     a.A = A_d; a.B = B_d; a.C = C_d; a.w = w_d;
     a.lda = lda; a.ldb = ldb; a.ldc = ldc;
     a.N1 = N1; a.N2 = N2; a.N3 = N3;
-    a.R = R; a.KS = static_cast<int>(ls::ceil_div(R, 4));
+    a.R = R;
+    split_rank(R, a.KD, a.n_tail);
     a.k0 = k0; a.k1 = k1;
     a.out = out_d; a.ldy = ldy; a.ldz = ldz;
     a.vec_store = (ldy % 2 == 0 && ldz % 2 == 0 && (reinterpret_cast<uintptr_t>(out_d) & 15) == 0) ? 1 : 0;
     a.rho1 = rho1_d; a.rho2 = rho2_d; a.rho3 = rho3_d; a.partial = partial_d;
-    const int wi = choose_wi(a.KS);
+    const int wi = choose_wi(a.KD);
     if (wi == 0) return ls::fail(LS_EGUARD, "expand: rank too large for the shared-memory tile");
     const bool store = out_d != nullptr;
     if (wi == 4) {
