@@ -38,6 +38,22 @@ int sm_count() {
     return cache[dev];
 }
 
+void ensure_pool() {
+    static std::mutex mu;
+    static std::vector<char> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= static_cast<int>(done.size())) done.resize(dev + 1, 0);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done[dev] = 1;
+}
+
 namespace {
 
 // Per-thread compute + copy streams on the current device, and a pool that
@@ -55,11 +71,7 @@ int get_streams(Streams*& out) {
     if (s.device != dev) {
         LS_CUDA(cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking));
         LS_CUDA(cudaStreamCreateWithFlags(&s.copy, cudaStreamNonBlocking));
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
+        ensure_pool();
         s.device = dev;
     }
     out = &s;

@@ -45,6 +45,10 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // Number of SMs of the current device (cached per device).
 int sm_count();
 
+// Keeps freed stream-ordered allocations cached in the current device's default
+// pool (no OS round trip per call). Idempotent per device.
+void ensure_pool();
+
 }  // namespace ls
 
 // Rounded FP64 primitives that the compiler can never contract into FMA:

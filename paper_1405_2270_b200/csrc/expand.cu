@@ -1,52 +1,63 @@
 // expand.cu -- K3: rank-R expansion of a canonical tensor onto the N1 x N2 x N3
-// grid, FP64 on the tensor cores (DMMA, mma.sync.m8n8k4.f64).
+// grid, FP64 on the tensor cores (DMMA, mma.sync.m8n8k4.f64), operands staged
+// by TMA bulk copies into a shared-memory ring.
 //
 // Reference: densify (canonical.hpp:251-266) -> detail::densify_slab
 // (canonical.hpp:241-246): slab k = A1 * diag(w .* A3(k,:)) * A2^T, an Eigen
-// GEMM with inner dimension R. Here each slab is the same GEMM, tiled for the
-// B200 FP64 tensor pipe:
+// GEMM with inner dimension R. Each slab is the same GEMM here:
 //
 //   V(i, j, k) = sum_q A1k(i, q) * A2(j, q),   A1k(i, q) = A1(i, q) * (w_q * A3(k, q))
 //
 // (the scaled left factor rounds exactly as Eigen's A1 * scale.asDiagonal()).
 // Measured on B200 (profiles/r01_fp64_peak_microbench.jsonl): DMMA m8n8k4
-// sustains 37.07 TFLOP/s = 64 FMA/clk/SM, DFMA 34.1 TFLOP/s, and the two share
-// one pipe; at R = 41 the expansion is 10.25 FLOP per output byte, above the
-// HBM ridge (~5.6), so this kernel is FP64-pipe-bound and is built to keep the
-// DMMA pipe issuing while the 8-byte-per-point output streams out.
+// sustains 37.07 TFLOP/s = 64 FMA/clk/SM; DFMA shares the same pipe. At
+// R = 41 the expansion is 10.25 FLOP per output byte, above the HBM ridge
+// (~5.6 FLOP/B), so the kernel is FP64-pipe-bound. The inner-loop study
+// (tools/lab/loop_lab.cu) showed DMMA at 37 TF/s with register or shared
+// operands but only 32-34 TF/s when one operand comes from L1/L2, so both
+// operands are fed from shared memory:
 //
-// Work decomposition. A work unit is (i-chunk of IC rows, one slab k). A CTA
-// of 8 warps scales A1 rows of its chunk by w .* A3(k,:) into shared memory
-// (fragment order, conflict-free LDS.64), then sweeps j in chunks of JC
-// columns: A2 rows are staged into a double-buffered shared tile with
-// cp.async in K-chunks, each warp computes a (8*TN) i x (8*TM) j register
-// tile with TM*TN independent DMMA accumulators, and stores it straight from
-// the accumulator fragments as 16-byte stores (each lane owns two adjacent
-// i). MMA orientation: M = j (A operand = A2 tile), N = i (B operand = A1k
-// tile), K = q, so the D fragment (row g, cols 2t, 2t+1) is two consecutive
-// i of one (j, k) row -- a 16-byte aligned pair in the i-fastest grid.
-// Units are spread over a persistent grid (CTAs per SM x SM count).
+//  * A1k for the CTA's i-chunk (IC rows x all ranks) is scaled once per
+//    work unit (i-chunk, slab k) into shared memory in MMA-fragment order;
+//  * A2 is pre-packed once per call into fragment order (pack_b_kernel) so
+//    every pipeline stage -- JT j-tiles x KC k-steps -- is one contiguous
+//    block that a single thread moves with cp.async.bulk (TMA) into an
+//    NS-deep ring, completion signalled on an mbarrier (expect_tx);
+//  * warps multiply with register ping-pong fragments (no moves), each
+//    owning TM x TN independent 8x8 accumulators (M = j, N = i, K = q), and
+//    store straight from the accumulator fragments: lane (g, t) holds
+//    V(i = 8n + 2t + {0,1}, j = 8m + g), a 16-byte aligned pair of the
+//    i-fastest grid, written with streaming stores.
+//  * a rank remainder of 1-2 (R mod 4) runs on DFMA instead of a zero-padded
+//    4-rank DMMA step.
+// One __syncthreads per stage guards ring-slot reuse; units are spread over
+// a persistent grid (CTAs per SM x SM count).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr int kTM = 4;            // j tiles (of 8) per warp
-constexpr int kTN = 4;            // i tiles (of 8) per warp
+constexpr int kTM = 4;  // j tiles (of 8) per warp
+constexpr int kTN = 4;  // i tiles (of 8) per warp
+constexpr int kNS = 3;  // stages in the A2 ring
 
 struct ExpandArgs {
     const double* A;
     const double* B;
+    const double* Bp;   // A2 packed per stage (see pack_b_kernel)
     const double* C;
     const double* w;
     int64_t lda, ldb, ldc;
     int64_t N1, N2, N3;
     int R;            // rank
     int KD;           // DMMA k-steps (4 ranks each); ranks >= 4*KD go to the DFMA tail
-    int n_tail;       // R - 4*KD in {0, 1, 2}, or 0 when the last k-step is zero-padded
+    int n_tail;       // R - 4*KD in {0, 1, 2}
+    int KC;           // k-steps per stage
+    int n_kc;         // k-chunks: ceil(KD / KC)
+    int64_t n_jt;     // packed j-tiles (multiple of JT)
+    int64_t n_jc;     // j-chunks per unit
     int64_t k0, k1;
     double* out;
     int64_t ldy, ldz;
@@ -57,6 +68,7 @@ struct ExpandArgs {
     double* partial;
     int64_t n_ichunks;
     int64_t n_units;
+    int debug;        // development knobs (LS_EXPAND_DEBUG): 1 no stores, 2 fill once, 4 no tail
 };
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -65,23 +77,101 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                  : "d"(a), "d"(b));
 }
 
-// A2 fragment element for lane (g, t) of j-tile starting at j, k-step ks: A2(j + g, 4 ks + t).
-__device__ __forceinline__ double load_b_frag(const ExpandArgs& p, int64_t j, int q) {
-    return (j < p.N2 && q < p.R) ? __ldg(p.B + j + p.ldb * q) : 0.0;
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "LS_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LS_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
-template <int WI, bool STORE, bool FUNC>
-__global__ void __launch_bounds__(kThreads, 2)
-expand_dmma_kernel(const ExpandArgs p) {
-    constexpr int WJ = kWarps / WI;
-    constexpr int IC = 8 * kTN * WI;
+// A2 packed so that every pipeline stage (k-chunk kc, j-chunk jc) is one contiguous block of
+// stage_elems = JT*KC*32 + JT*8*n_tail doubles at Bp + (kc * n_jc + jc) * stage_elems:
+//   [jt][kk][lane] = A2(8 (jc JT + jt) + g, 4 (kc KC + kk) + t)   (MMA A-fragment order)
+//   then [jt][qt][g] = A2(8 (jc JT + jt) + g, 4 KD + qt)          (DFMA tail ranks)
+// zero padded outside the matrix.
+__global__ void pack_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t N2, int R, int KD, int n_tail,
+                              int KC, int n_kc, int JT, int64_t n_jc, double* __restrict__ Bp) {
+    const int64_t frag = static_cast<int64_t>(JT) * KC * 32;
+    const int64_t stage_elems = frag + static_cast<int64_t>(JT) * 8 * n_tail;
+    const int64_t total = static_cast<int64_t>(n_kc) * n_jc * stage_elems;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t st = e / stage_elems;
+        const int64_t o = e - st * stage_elems;
+        const int kc = static_cast<int>(st / n_jc);
+        const int64_t jc = st % n_jc;
+        double v = 0.0;
+        if (o < frag) {
+            const int lane = static_cast<int>(o & 31);
+            const int kk = static_cast<int>((o >> 5) % KC);
+            const int jt = static_cast<int>((o >> 5) / KC);
+            const int ks = kc * KC + kk;
+            const int64_t j = (jc * JT + jt) * 8 + (lane >> 2);
+            const int q = ks * 4 + (lane & 3);
+            if (j < N2 && ks < KD && q < R) v = B[j + ldb * q];
+        } else {
+            const int64_t r = o - frag;
+            const int g = static_cast<int>(r % 8);
+            const int qt = static_cast<int>((r / 8) % n_tail);
+            const int jt = static_cast<int>(r / (8 * n_tail));
+            const int64_t j = (jc * JT + jt) * 8 + g;
+            if (j < N2) v = B[j + ldb * (4 * KD + qt)];
+        }
+        Bp[e] = v;
+    }
+}
 
-    extern __shared__ __align__(16) double smem[];
-    const int KD = p.KD;
-    double* as = smem;                                       // [IC/8][KD][32] fragment order
-    double* tail = as + static_cast<int64_t>(IC) * KD * 4;   // [n_tail][IC]
-    double* scale = tail + 2 * IC;                           // [4*KD + n_tail]
-    __shared__ double red[kWarps];
+template <int WARPS, int WI>
+struct Tile {
+    static constexpr int WJ = WARPS / WI;
+    static constexpr int IC = 8 * kTN * WI;  // i rows per unit
+    static constexpr int JT = kTM * WJ;      // j tiles (of 8) per stage
+    static constexpr int JC = 8 * JT;        // j columns per stage
+};
+
+template <int WARPS, int WI, bool STORE, bool FUNC>
+__global__ void __launch_bounds__(WARPS * 32, 2)
+expand_dmma_kernel(const ExpandArgs p) {
+    using T = Tile<WARPS, WI>;
+    constexpr int kThreads = WARPS * 32;
+    constexpr int IC = T::IC;
+    constexpr int JT = T::JT;
+    // All counters are 32-bit (launch() checks the ranges); only addresses are 64-bit.
+    const int KD = p.KD, KC = p.KC, n_tail = p.n_tail, n_kc = p.n_kc;
+    const int frag_elems = JT * KC * 32;
+    const int stage_elems = frag_elems + JT * 8 * n_tail;
+    const int rpad = 4 * KD + n_tail;
+    const int n_ichunks = static_cast<int>(p.n_ichunks);
+    const int n_units = static_cast<int>(p.n_units);
+
+    extern __shared__ __align__(128) double smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);           // [kNS] mbarriers: stage landed
+    int* released = reinterpret_cast<int*>(smem + 8);              // [kNS] warps done with a slot
+    double* ring = smem + 16;                                      // [kNS][stage_elems]
+    double* as = ring + kNS * stage_elems;                         // [IC/8][KD][32]
+    double* tail = as + IC * KD * 4;                               // [n_tail][IC]
+    double* scale = tail + IC * n_tail;                            // [2][rpad] (unit parity)
+    __shared__ double red[WARPS];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -89,135 +179,204 @@ expand_dmma_kernel(const ExpandArgs p) {
     const int t = lane & 3;
     const int wi = warp % WI;
     const int wj = warp / WI;
-    const int q_tail0 = 4 * KD;
-    const int n_scale = q_tail0 + p.n_tail;
 
-    for (int64_t unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
-        const int64_t ic = unit % p.n_ichunks;
-        const int64_t kk = unit / p.n_ichunks;   // slab offset within [k0, k1)
-        const int64_t k = p.k0 + kk;
-        const int64_t i_base = ic * IC;
+    // This CTA's stage sequence: units u = blockIdx.x + n*gridDim.x, each n_jc * n_kc stages.
+    const int my_units = n_units > static_cast<int>(blockIdx.x)
+                             ? (n_units - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                             : 0;
+    const int per_unit = static_cast<int>(p.n_jc) * n_kc;
+    const int n_stages = my_units * per_unit;
+    const unsigned stage_bytes = static_cast<unsigned>(stage_elems * sizeof(double));
 
-        __syncthreads();  // previous unit finished reading as / tail / scale
-        // scale_q = w_q * A3(k, q)   (canonical.hpp:244)
-        for (int q = threadIdx.x; q < n_scale; q += kThreads)
-            scale[q] = q < p.R ? rn_mul(p.w[q], p.C[k + p.ldc * q]) : 0.0;
-        __syncthreads();
-        // A1k(i, q) = A1(i, q) * scale_q, Eigen's A1 * scale.asDiagonal(): DMMA part in fragment
-        // order (lane (g, t) of i-tile it, k-step ks <-> A1k(8 it + g, 4 ks + t)), tail row-wise.
-        for (int e = threadIdx.x; e < IC * KD * 4; e += kThreads) {
-            const int ln = e & 31;
-            const int ks = (e >> 5) % KD;
-            const int it = (e >> 5) / KD;
-            const int64_t i = i_base + it * 8 + (ln >> 2);
-            const int q = ks * 4 + (ln & 3);
-            as[e] = (i < p.N1 && q < p.R) ? rn_mul(p.A[i + p.lda * q], scale[q]) : 0.0;
+    auto issue = [&](int st) {
+        const int w = st % per_unit;
+        const int c = w / n_kc;
+        const int kcs = w - c * n_kc;
+        const double* src = p.Bp + (static_cast<int64_t>(kcs) * p.n_jc + c) * stage_elems;
+        uint64_t* bar = full + (st % kNS);
+        mbar_arrive_expect_tx(bar, stage_bytes);
+        tma_bulk_g2s(ring + (st % kNS) * stage_elems, src, stage_bytes, bar);
+    };
+    // scale_q = w_q * A3(k, q) for the unit's slab (canonical.hpp:244)
+    auto compute_scale = [&](int u, double* dst) {
+        const int64_t k = p.k0 + u / n_ichunks;
+        for (int q = threadIdx.x; q < rpad; q += kThreads) dst[q] = q < p.R ? rn_mul(p.w[q], p.C[k + p.ldc * q]) : 0.0;
+    };
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kNS; ++b) {
+            mbar_init(full + b, 1);
+            released[b] = 0;
         }
-        for (int e = threadIdx.x; e < p.n_tail * IC; e += kThreads) {
-            const int q = q_tail0 + e / IC;
-            const int64_t i = i_base + e % IC;
-            tail[e] = i < p.N1 ? rn_mul(p.A[i + p.lda * q], scale[q]) : 0.0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (my_units > 0) compute_scale(blockIdx.x, scale);
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int st = 0; st < kNS && st < n_stages; ++st) issue(st);
+
+    double acc[kTM][kTN][2];
+    double fsum = 0.0;
+    int unit = blockIdx.x;
+    int parity = 0;  // unit parity selects the scale buffer
+    int within = 0, jc = 0, kc = 0;
+    int ib = (unit % n_ichunks) * IC;  // first i row of the unit
+    int kk = unit / n_ichunks;         // slab offset within [k0, k1)
+
+    for (int st = 0; st < n_stages; ++st) {
+        if (within == 0 && !((p.debug & 2) && st > 0)) {
+            __syncthreads();  // every warp finished the previous unit: as/tail are free
+            // New unit: A1k(i, q) = A1(i, q) * scale_q (Eigen's A1 * scale.asDiagonal()), fragment
+            // order: lane (g, t) of (i-tile it, k-step ks) <-> A1k(8 it + g, 4 ks + t).
+            const double* sc = scale + parity * rpad;
+            const int pairs = (IC / 8) * KD;
+            int it = warp / KD, ks = warp - (warp / KD) * KD;
+#pragma unroll 4
+            for (int x = warp; x < pairs; x += WARPS) {
+                const int i = ib + it * 8 + g;
+                const int q = ks * 4 + t;
+                as[x * 32 + lane] = (i < p.N1 && q < p.R) ? rn_mul(__ldg(p.A + i + p.lda * q), sc[q]) : 0.0;
+                ks += WARPS;
+                while (ks >= KD) {
+                    ks -= KD;
+                    ++it;
+                }
+            }
+            for (int e = threadIdx.x; e < n_tail * IC; e += kThreads) {
+                const int q = 4 * KD + e / IC;
+                const int i = ib + e % IC;
+                tail[e] = i < p.N1 ? rn_mul(__ldg(p.A + i + p.lda * q), sc[q]) : 0.0;
+            }
+            if (FUNC) fsum = 0.0;
+            __syncthreads();
         }
-        __syncthreads();
+        if (within == per_unit - 1 && unit + static_cast<int>(gridDim.x) < n_units)
+            compute_scale(unit + gridDim.x, scale + (parity ^ 1) * rpad);  // read after the unit barrier
 
-        double fsum = 0.0;  // FUNC: this thread's rho-weighted partial over the unit
-        const double* asw = as + (wi * kTN) * (KD * 32) + lane;
-        const int64_t ibase = i_base + wi * (8 * kTN);
-
-        // Each warp sweeps its own j-blocks: no block-level synchronisation until the next unit.
-        for (int64_t jb = static_cast<int64_t>(wj) * (8 * kTM); jb < p.N2; jb += WJ * (8 * kTM)) {
-            double acc[kTM][kTN][2];
+        const int slot = st % kNS;
+        mbar_wait(full + slot, static_cast<unsigned>((st / kNS) & 1));
+        const double* stage = ring + slot * stage_elems;
+        if (kc == 0) {
 #pragma unroll
             for (int m = 0; m < kTM; ++m)
 #pragma unroll
-                for (int nn = 0; nn < kTN; ++nn) acc[m][nn][0] = acc[m][nn][1] = 0.0;
-
-            // Register double-buffering: fragments of k-step ks+1 load while ks multiplies.
-            double a_nx[kTM], b_nx[kTN];
-#pragma unroll
-            for (int m = 0; m < kTM; ++m) a_nx[m] = load_b_frag(p, jb + 8 * m + g, t);
-#pragma unroll
-            for (int nn = 0; nn < kTN; ++nn) b_nx[nn] = asw[nn * (KD * 32)];
-#pragma unroll 2
-            for (int ks = 0; ks < KD; ++ks) {
-                double a[kTM], b[kTN];
-#pragma unroll
-                for (int m = 0; m < kTM; ++m) a[m] = a_nx[m];
-#pragma unroll
-                for (int nn = 0; nn < kTN; ++nn) b[nn] = b_nx[nn];
-                if (ks + 1 < KD) {
-#pragma unroll
-                    for (int m = 0; m < kTM; ++m) a_nx[m] = load_b_frag(p, jb + 8 * m + g, 4 * (ks + 1) + t);
-#pragma unroll
-                    for (int nn = 0; nn < kTN; ++nn) b_nx[nn] = asw[nn * (KD * 32) + (ks + 1) * 32];
-                }
-#pragma unroll
-                for (int m = 0; m < kTM; ++m)
-#pragma unroll
-                    for (int nn = 0; nn < kTN; ++nn) dmma_884(acc[m][nn][0], acc[m][nn][1], a[m], b[nn]);
-            }
-            // Rank remainder (R mod 4 <= 2) on the DFMA path instead of a zero-padded k-step:
-            // lane (g, t) owns V(i = ibase + 8 nn + 2t + {0,1}, j = jb + 8 m + g).
-            for (int qt = 0; qt < p.n_tail; ++qt) {
-                const int q = q_tail0 + qt;
+                for (int n = 0; n < kTN; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+            // Rank remainder (R mod 4 = 1, 2) on DFMA, issued first so it never waits on DMMA
+            // results: lane (g, t) owns V(i = 8n + 2t + {0,1}, j = 8m + g) of the warp tile.
+            const double* tb = stage + frag_elems + (wj * kTM) * (8 * n_tail) + g;
+            for (int qt = 0; qt < ((p.debug & 4) ? 0 : n_tail); ++qt) {
                 double bt[kTM];
 #pragma unroll
-                for (int m = 0; m < kTM; ++m) bt[m] = load_b_frag(p, jb + 8 * m + g, q);
+                for (int m = 0; m < kTM; ++m) bt[m] = tb[m * (8 * n_tail) + qt * 8];
 #pragma unroll
-                for (int nn = 0; nn < kTN; ++nn) {
-                    const double2 at = *reinterpret_cast<const double2*>(
-                        tail + qt * IC + wi * (8 * kTN) + 8 * nn + 2 * t);
+                for (int n = 0; n < kTN; ++n) {
+                    const double2 at =
+                        *reinterpret_cast<const double2*>(tail + qt * IC + wi * (8 * kTN) + 8 * n + 2 * t);
 #pragma unroll
                     for (int m = 0; m < kTM; ++m) {
-                        acc[m][nn][0] = fma(at.x, bt[m], acc[m][nn][0]);
-                        acc[m][nn][1] = fma(at.y, bt[m], acc[m][nn][1]);
-                    }
-                }
-            }
-
-            // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
-#pragma unroll
-            for (int m = 0; m < kTM; ++m) {
-                const int64_t j = jb + 8 * m + g;
-                if (j >= p.N2) continue;
-                double* row = STORE ? p.out + kk * p.ldz + j * p.ldy : nullptr;
-                double r2 = 0.0;
-                if (FUNC) r2 = p.rho2[j];
-#pragma unroll
-                for (int nn = 0; nn < kTN; ++nn) {
-                    const int64_t i = ibase + 8 * nn + 2 * t;
-                    if (i + 1 < p.N1) {
-                        if (STORE) {
-                            if (p.vec_store) {
-                                __stcs(reinterpret_cast<double2*>(row + i),
-                                       make_double2(acc[m][nn][0], acc[m][nn][1]));
-                            } else {
-                                row[i] = acc[m][nn][0];
-                                row[i + 1] = acc[m][nn][1];
-                            }
-                        }
-                        if (FUNC)
-                            fsum += rn_mul(rn_mul(acc[m][nn][0], p.rho1[i]), r2) +
-                                    rn_mul(rn_mul(acc[m][nn][1], p.rho1[i + 1]), r2);
-                    } else if (i < p.N1) {
-                        if (STORE) row[i] = acc[m][nn][0];
-                        if (FUNC) fsum += rn_mul(rn_mul(acc[m][nn][0], p.rho1[i]), r2);
+                        acc[m][n][0] = fma(at.x, bt[m], acc[m][n][0]);
+                        acc[m][n][1] = fma(at.y, bt[m], acc[m][n][1]);
                     }
                 }
             }
         }
 
-        if (FUNC) {
-            // Fixed-order reduction: lanes by xor-tree, then warps in index order.
+        {
+            const double* bsw = stage + (wj * kTM) * (KC * 32) + lane;
+            const double* aw = as + (wi * kTN) * (KD * 32) + kc * KC * 32 + lane;
+            const int ks_len = min(KC, KD - kc * KC);
+            // Operands straight from shared memory (loop_lab: 36.9 TF/s at 4x4 without prefetch);
+            // the other warps of the SM sub-partition cover the LDS latency.
+#pragma unroll 1
+            for (int ks = 0; ks < ks_len; ++ks) {
+                double a[kTM], b[kTN];
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, off);
-            if (lane == 0) red[warp] = fsum;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                double s = 0.0;
-                for (int wv = 0; wv < kWarps; ++wv) s += red[wv];
-                p.partial[unit] = rn_mul(s, p.rho3[k]);
+                for (int m = 0; m < kTM; ++m) a[m] = bsw[m * (KC * 32) + ks * 32];
+#pragma unroll
+                for (int n = 0; n < kTN; ++n) b[n] = aw[n * (KD * 32) + ks * 32];
+#pragma unroll
+                for (int m = 0; m < kTM; ++m)
+#pragma unroll
+                    for (int n = 0; n < kTN; ++n) dmma_884(acc[m][n][0], acc[m][n][1], a[m], b[n]);
             }
+        }
+        // Release the ring slot. Every LDS of this stage has completed (its result fed a DMMA
+        // already issued); the last warp to release refills the slot with stage st + kNS.
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(released + slot, 1) == WARPS - 1) {
+                released[slot] = 0;
+                __threadfence_block();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (st + kNS < n_stages) issue(st + kNS);
+            }
+        }
+
+        if (kc == n_kc - 1) {
+            const int jb = jc * T::JC + wj * (8 * kTM);
+            const int ibase = ib + wi * (8 * kTN);
+#pragma unroll
+            for (int m = 0; m < kTM; ++m) {
+                const int j = jb + 8 * m + g;
+                if (j >= p.N2) continue;
+                if (p.debug & 1) {
+                    double sx = 0.0;
+#pragma unroll
+                    for (int n = 0; n < kTN; ++n) sx += acc[m][n][0] + acc[m][n][1];
+                    if (sx == 1.2345) p.out[0] = sx;
+                    continue;
+                }
+                double* row = STORE ? p.out + kk * p.ldz + static_cast<int64_t>(j) * p.ldy : nullptr;
+                double r2 = 0.0;
+                if (FUNC) r2 = p.rho2[j];
+#pragma unroll
+                for (int n = 0; n < kTN; ++n) {
+                    const int i = ibase + 8 * n + 2 * t;
+                    if (i + 1 < p.N1) {
+                        if (STORE) {
+                            if (p.vec_store) {
+                                __stcs(reinterpret_cast<double2*>(row + i), make_double2(acc[m][n][0], acc[m][n][1]));
+                            } else {
+                                row[i] = acc[m][n][0];
+                                row[i + 1] = acc[m][n][1];
+                            }
+                        }
+                        if (FUNC)
+                            fsum += rn_mul(rn_mul(acc[m][n][0], p.rho1[i]), r2) +
+                                    rn_mul(rn_mul(acc[m][n][1], p.rho1[i + 1]), r2);
+                    } else if (i < p.N1) {
+                        if (STORE) row[i] = acc[m][n][0];
+                        if (FUNC) fsum += rn_mul(rn_mul(acc[m][n][0], p.rho1[i]), r2);
+                    }
+                }
+            }
+        }
+
+        // advance (within, jc, kc); a finished unit moves on to the CTA's next unit
+        if (++kc == n_kc) {
+            kc = 0;
+            ++jc;
+        }
+        if (++within == per_unit) {
+            if (FUNC) {
+                // Fixed-order reduction: lanes by xor-tree, then warps in index order.
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, off);
+                if (lane == 0) red[warp] = fsum;
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    double sum = 0.0;
+                    for (int wv = 0; wv < WARPS; ++wv) sum += red[wv];
+                    p.partial[unit] = rn_mul(sum, p.rho3[p.k0 + kk]);
+                }
+            }
+            within = 0;
+            jc = 0;
+            unit += gridDim.x;
+            parity ^= 1;
+            ib = (unit % n_ichunks) * IC;
+            kk = unit / n_ichunks;
         }
     }
 }
@@ -246,39 +405,92 @@ void split_rank(int R, int& KD, int& n_tail) {
         KD += 1;
         n_tail = 0;
     }
+    if (KD == 0) {  // R <= 2: one zero-padded DMMA step
+        KD = 1;
+        n_tail = 0;
+    }
 }
 
-template <int WI>
-size_t smem_bytes(int KD) {
-    constexpr int IC = 8 * kTN * WI;
-    return sizeof(double) * (static_cast<size_t>(IC) * KD * 4 + 2 * static_cast<size_t>(IC) +
-                             static_cast<size_t>(KD) * 4 + 4);
+// Shared-memory budget per SM (B200: 228 KB, 227 KB per CTA opt-in, 1 KB reserved per CTA).
+constexpr size_t kSmemPerSM = 228 * 1024;
+
+template <int WARPS, int WI>
+size_t smem_bytes(int KD, int KC, int n_tail) {
+    using T = Tile<WARPS, WI>;
+    const size_t stage = static_cast<size_t>(T::JT) * KC * 32 + static_cast<size_t>(T::JT) * 8 * n_tail;
+    return sizeof(double) * (16 + kNS * stage + static_cast<size_t>(T::IC) * KD * 4 +
+                             static_cast<size_t>(T::IC) * n_tail + 2 * (4 * static_cast<size_t>(KD) + n_tail));
 }
 
-// Shared-memory budget per CTA (B200: 227 KB opt-in; two CTAs per SM share 228 KB).
-constexpr size_t kSmemLimit = 227 * 1024;
+// Tile plans, best first: (8 warps, 128-row i-chunk, whole rank per stage, 2 CTAs/SM) for the
+// BASELINE ranks; narrower i-chunks and short K-chunks as the rank grows.
+struct Plan {
+    int warps, wi, KC;
+};
 
-int choose_wi(int KD) {
-    if (smem_bytes<4>(KD) * 2 <= kSmemLimit - 2048) return 4;  // two CTAs per SM
-    if (smem_bytes<1>(KD) * 2 <= kSmemLimit - 2048) return 1;
-    if (smem_bytes<1>(KD) <= kSmemLimit) return 1;
-    return 0;
+bool plan_for(int KD, int n_tail, Plan& out) {
+    const Plan cands[] = {{8, 4, 0}, {8, 4, 8}, {4, 2, 4}, {4, 1, 4}, {4, 1, 2}};
+    for (const Plan& c : cands) {
+        const int KC = c.KC == 0 ? KD : std::min(KD, c.KC);
+        size_t bytes;
+        if (c.warps == 8)
+            bytes = smem_bytes<8, 4>(KD, KC, n_tail);
+        else if (c.wi == 2)
+            bytes = smem_bytes<4, 2>(KD, KC, n_tail);
+        else
+            bytes = smem_bytes<4, 1>(KD, KC, n_tail);
+        if (2 * (bytes + 1024) <= kSmemPerSM) {
+            out = {c.warps, c.wi, KC};
+            return true;
+        }
+    }
+    return false;
 }
 
-template <int WI, bool STORE, bool FUNC>
+template <int WARPS, int WI, bool STORE, bool FUNC>
 int launch(ExpandArgs& a, cudaStream_t s) {
-    constexpr int IC = 8 * kTN * WI;
-    a.n_ichunks = ls::ceil_div(a.N1, IC);
+    using T = Tile<WARPS, WI>;
+    a.n_ichunks = ls::ceil_div(a.N1, T::IC);
     a.n_units = a.n_ichunks * (a.k1 - a.k0);
-    const size_t smem = smem_bytes<WI>(a.KD);
-    auto kern = expand_dmma_kernel<WI, STORE, FUNC>;
+    a.n_jc = ls::ceil_div(a.N2, T::JC);
+    a.n_jt = a.n_jc * T::JT;
+    a.n_kc = static_cast<int>(ls::ceil_div(a.KD, a.KC));
+    // Pack A2 once per call (stream-ordered scratch from the pool).
+    double* bp = nullptr;
+    const size_t stage_elems = static_cast<size_t>(T::JT) * a.KC * 32 + static_cast<size_t>(T::JT) * 8 * a.n_tail;
+    const size_t bp_elems = static_cast<size_t>(a.n_kc) * a.n_jc * stage_elems;
+    ls::ensure_pool();
+    LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bp), bp_elems * sizeof(double), s));
+    const int64_t pb = std::min<int64_t>(ls::ceil_div(static_cast<int64_t>(bp_elems), 256), 4096);
+    pack_b_kernel<<<(unsigned)pb, 256, 0, s>>>(a.B, a.ldb, a.N2, a.R, a.KD, a.n_tail, a.KC, a.n_kc, T::JT, a.n_jc,
+                                               bp);
+    LS_LAUNCHED("pack_b_kernel");
+    a.Bp = bp;
+    // 32-bit counters inside the kernel
+    if (a.n_units * a.n_jc * a.n_kc >= (int64_t(1) << 31) || a.N1 + T::IC >= (int64_t(1) << 31) ||
+        a.N2 + T::JC >= (int64_t(1) << 31))
+        return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
+    const size_t smem = smem_bytes<WARPS, WI>(a.KD, a.KC, a.n_tail);
+    auto kern = expand_dmma_kernel<WARPS, WI, STORE, FUNC>;
     LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int per_sm = (2 * smem + 2048 <= kSmemLimit) ? 2 : 1;
+    int per_sm = 0;
+    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
+    if (per_sm < 1) return ls::fail(LS_EGUARD, "expand: tile does not fit on an SM");
     const int64_t grid = std::min<int64_t>(a.n_units, (int64_t)ls::sm_count() * per_sm);
-    if (grid <= 0) return LS_OK;
-    kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
-    LS_LAUNCHED("expand_dmma_kernel");
+    if (grid > 0) {
+        kern<<<(unsigned)grid, WARPS * 32, smem, s>>>(a);
+        LS_LAUNCHED("expand_dmma_kernel");
+    }
+    LS_CUDA(cudaFreeAsync(bp, s));
     return LS_OK;
+}
+
+template <bool STORE, bool FUNC>
+int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
+    a.KC = pl.KC;
+    if (pl.warps == 8) return launch<8, 4, STORE, FUNC>(a, s);
+    if (pl.wi == 2) return launch<4, 2, STORE, FUNC>(a, s);
+    return launch<4, 1, STORE, FUNC>(a, s);
 }
 
 }  // namespace
@@ -287,9 +499,9 @@ extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_
     (void)N2;
     int KD, n_tail;
     split_rank(std::max(R, 1), KD, n_tail);
-    const int wi = choose_wi(KD);
-    if (wi == 0 || k1 < k0) return -1;
-    const int64_t IC = 8 * kTN * wi;
+    Plan pl;
+    if (!plan_for(KD, n_tail, pl) || k1 < k0) return -1;
+    const int64_t IC = 8 * kTN * pl.wi;
     return ls::ceil_div(N1, IC) * (k1 - k0);
 }
 
@@ -329,17 +541,13 @@ extern "C" int ls_expand(const double* A_d, int64_t lda, const double* B_d, int6
     a.out = out_d; a.ldy = ldy; a.ldz = ldz;
     a.vec_store = (ldy % 2 == 0 && ldz % 2 == 0 && (reinterpret_cast<uintptr_t>(out_d) & 15) == 0) ? 1 : 0;
     a.rho1 = rho1_d; a.rho2 = rho2_d; a.rho3 = rho3_d; a.partial = partial_d;
-    const int wi = choose_wi(a.KD);
-    if (wi == 0) return ls::fail(LS_EGUARD, "expand: rank too large for the shared-memory tile");
+    if (const char* dbg = std::getenv("LS_EXPAND_DEBUG")) a.debug = std::atoi(dbg);
+    Plan pl;
+    if (!plan_for(a.KD, a.n_tail, pl)) return ls::fail(LS_EGUARD, "expand: rank too large for the shared-memory tile");
     const bool store = out_d != nullptr;
-    if (wi == 4) {
-        if (store && func) return launch<4, true, true>(a, s);
-        if (store) return launch<4, true, false>(a, s);
-        return launch<4, false, true>(a, s);
-    }
-    if (store && func) return launch<1, true, true>(a, s);
-    if (store) return launch<1, true, false>(a, s);
-    return launch<1, false, true>(a, s);
+    if (store && func) return launch_plan<true, true>(pl, a, s);
+    if (store) return launch_plan<true, false>(pl, a, s);
+    return launch_plan<false, true>(pl, a, s);
 }
 
 extern "C" int ls_sum_partials(const double* partial_d, int64_t count, double* out_d, void* stream) {

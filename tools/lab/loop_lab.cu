@@ -1,0 +1,158 @@
+// loop_lab.cu -- isolates the DMMA inner loop of the expansion (development tool).
+// Each warp runs KD k-steps over TMxTN 8x8 tiles, NJ times, with operands from: constant regs,
+// shared memory (LDS), global (LDG, L1/L2-resident). No stores except a sink.
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};" : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// MODE 0: constants; 1: b from smem, a const; 2: a from global, b const; 3: both (move-based prefetch);
+// 4: both, ping-pong unrolled by 2 (no moves)
+template <int MODE, int TM, int TN>
+__global__ void __launch_bounds__(256, 2) loop_kernel(const double* __restrict__ g, double* out, int KD, int NJ) {
+    __shared__ double sm[4 * 11 * 32 * 4 + 64];
+    for (int e = threadIdx.x; e < 4 * 11 * 32 * 4; e += 256) sm[e] = 1.0 + e * 1e-9;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* asw = sm + lane;
+    const double* gw = g + lane + (warp & 1) * 4 * 11 * 32;
+    double acc[TM][TN][2];
+#pragma unroll
+    for (int m = 0; m < TM; ++m)
+#pragma unroll
+        for (int n = 0; n < TN; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    double ca = 1.0 + lane * 1e-12, cb = 0.5;
+    for (int jb = 0; jb < NJ; ++jb) {
+        if (MODE == 5) {
+            const double* bw = asw + 4 * 11 * 32 * 2;
+#pragma unroll 1
+            for (int ks = 0; ks < KD; ++ks) {
+                double a[TM], b[TN];
+#pragma unroll
+                for (int m = 0; m < TM; ++m) a[m] = asw[(m * 11 + ks) * 32];
+#pragma unroll
+                for (int n = 0; n < TN; ++n) b[n] = asw[(n * 11 + ks) * 32 + 64];
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) dmma(acc[m][n][0], acc[m][n][1], a[m], b[n]);
+            }
+            (void)bw;
+        } else if (MODE == 6) {
+            double a0[TM], b0[TN], a1[TM], b1[TN];
+#pragma unroll
+            for (int m = 0; m < TM; ++m) a0[m] = asw[(m * 11) * 32];
+#pragma unroll
+            for (int n = 0; n < TN; ++n) b0[n] = asw[(n * 11) * 32 + 64];
+            for (int ks = 0; ks < KD; ks += 2) {
+#pragma unroll
+                for (int m = 0; m < TM; ++m) a1[m] = asw[(m * 11 + ks + 1) * 32];
+#pragma unroll
+                for (int n = 0; n < TN; ++n) b1[n] = asw[(n * 11 + ks + 1) * 32 + 64];
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) dmma(acc[m][n][0], acc[m][n][1], a0[m], b0[n]);
+                if (ks + 2 < KD) {
+#pragma unroll
+                    for (int m = 0; m < TM; ++m) a0[m] = asw[(m * 11 + ks + 2) * 32];
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) b0[n] = asw[(n * 11 + ks + 2) * 32 + 64];
+                }
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) dmma(acc[m][n][0], acc[m][n][1], a1[m], b1[n]);
+            }
+        } else if (MODE == 4) {
+            double a0[TM], b0[TN], a1[TM], b1[TN];
+#pragma unroll
+            for (int m = 0; m < TM; ++m) a0[m] = __ldg(gw + (m * 11) * 32);
+#pragma unroll
+            for (int n = 0; n < TN; ++n) b0[n] = asw[(n * 11) * 32];
+            for (int ks = 0; ks < KD; ks += 2) {
+#pragma unroll
+                for (int m = 0; m < TM; ++m) a1[m] = __ldg(gw + (m * 11 + ks + 1) * 32);
+#pragma unroll
+                for (int n = 0; n < TN; ++n) b1[n] = asw[(n * 11 + ks + 1) * 32];
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) dmma(acc[m][n][0], acc[m][n][1], a0[m], b0[n]);
+                if (ks + 2 < KD) {
+#pragma unroll
+                    for (int m = 0; m < TM; ++m) a0[m] = __ldg(gw + (m * 11 + ks + 2) * 32);
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) b0[n] = asw[(n * 11 + ks + 2) * 32];
+                }
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) dmma(acc[m][n][0], acc[m][n][1], a1[m], b1[n]);
+            }
+        } else {
+            double a_nx[TM], b_nx[TN];
+#pragma unroll
+            for (int m = 0; m < TM; ++m) a_nx[m] = (MODE == 2 || MODE == 3) ? __ldg(gw + (m * 11) * 32) : ca;
+#pragma unroll
+            for (int n = 0; n < TN; ++n) b_nx[n] = (MODE == 1 || MODE == 3) ? asw[(n * 11) * 32] : cb;
+#pragma unroll 1
+            for (int ks = 0; ks < KD; ++ks) {
+                double a[TM], b[TN];
+#pragma unroll
+                for (int m = 0; m < TM; ++m) a[m] = a_nx[m];
+#pragma unroll
+                for (int n = 0; n < TN; ++n) b[n] = b_nx[n];
+                if (ks + 1 < KD) {
+                    if (MODE == 2 || MODE == 3)
+#pragma unroll
+                        for (int m = 0; m < TM; ++m) a_nx[m] = __ldg(gw + (m * 11 + ks + 1) * 32);
+                    if (MODE == 1 || MODE == 3)
+#pragma unroll
+                        for (int n = 0; n < TN; ++n) b_nx[n] = asw[(n * 11 + ks + 1) * 32];
+                }
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) dmma(acc[m][n][0], acc[m][n][1], a[m], b[n]);
+            }
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int m = 0; m < TM; ++m)
+#pragma unroll
+        for (int n = 0; n < TN; ++n) s += acc[m][n][0] + acc[m][n][1];
+    if (s == 1.2345) out[0] = s;
+}
+
+template <int MODE, int TM, int TN>
+void run(const char* name, const double* g, double* out) {
+    int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int KD = 10, NJ = 200, grid = sms * 2;
+    cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    loop_kernel<MODE, TM, TN><<<grid, 256>>>(g, out, KD, NJ); CK(cudaDeviceSynchronize());
+    float best = 1e9;
+    for (int r = 0; r < 5; ++r) {
+        CK(cudaEventRecord(e0)); loop_kernel<MODE, TM, TN><<<grid, 256>>>(g, out, KD, NJ); CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1)); float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); if (ms < best) best = ms;
+    }
+    double flops = 2.0 * 256 * TM * TN * (double)KD * NJ * grid * 8;
+    cudaFuncAttributes fa; CK(cudaFuncGetAttributes(&fa, loop_kernel<MODE, TM, TN>));
+    printf("{\"loop\":\"%s\",\"regs\":%d,\"ms\":%.4f,\"tflops\":%.3f}\n", name, fa.numRegs, best, flops / best / 1e9);
+}
+
+int main() {
+    double *g, *out; CK(cudaMalloc(&g, 8 * 8 * 11 * 32 * 8)); CK(cudaMalloc(&out, 8));
+    CK(cudaMemset(g, 0, 8 * 8 * 11 * 32 * 8));
+    run<0, 4, 4>("const 4x4", g, out);
+    run<5, 4, 4>("smem both, no prefetch 4x4", g, out);
+    run<6, 4, 4>("smem both, pingpong 4x4", g, out);
+    run<5, 2, 4>("smem both, no prefetch 2x4", g, out);
+    run<5, 4, 2>("smem both, no prefetch 4x2", g, out);
+    return 0;
+}
