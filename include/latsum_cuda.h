@@ -1,5 +1,5 @@
 /* latsum_cuda.h -- C ABI of liblatsum_cuda.so, the B200 (sm_100a) engine behind
- * the drop-in latsum C++ API (include/latsum/*.hpp).
+ * the drop-in latsum C++ API (the headers under include/latsum/).
  *
  * The reference (arXiv 1405.2270, /root/reference/proj) is a header-only C++
  * library with no FFI; its "operator API" is the set of inline functions in
@@ -126,8 +126,30 @@ int ls_functional_batch(const double* A_d, int64_t lda, const double* B_d, int64
                         int64_t ldy, const double* Z_d, int64_t ldz, int F, double scale,
                         double* out_d, void* stream);
 
+/* Streaming compare: for every block b of a launch of nblocks blocks,
+ * part_d[2b] = max(part_d[2b], max|a - b|) and part_d[2b+1] = max(.., max|b|)
+ * over n entries (max_norm_diff_canonical's per-slab reduction,
+ * canonical.hpp:289-293; max is exact, so the order does not matter). */
+int ls_maxdiff_accumulate(const double* a_d, const double* b_d, int64_t n, double* part_d, int nblocks,
+                          void* stream);
+
 /* ---- host-level entry points (drop-in headers, e2e path) ----------------
  * Synchronous; all pointers host memory; results copied back. */
+/* build_newton_master(lens, h, rule) (newton.hpp:57-75) in either generator
+ * mode: f_h[l] is lens[l] x R column-major; equal-length axes share data. */
+int ls_h_newton_master(int mode, const int64_t lens[3], double h, const double* tau_h, int R, double* f0_h,
+                       double* f1_h, double* f2_h);
+/* Batched scale * scalar_product(P, x_f (x) y_f (x) z_f) for F rank-1 tensors
+ * (columns of X/Y/Z, dims[l] rows): potential_matrix's pair projections
+ * (project.hpp:65-97) and the BASELINE energy functionals. */
+int ls_h_functional_batch(const int64_t dims[3], int R, const double* A_h, const double* B_h, const double* C_h,
+                          const double* w_h, int F, const double* X_h, const double* Y_h, const double* Z_h,
+                          double scale, double* out_h);
+/* max_norm_diff_canonical(a, b) (canonical.hpp:282-301): both tensors are
+ * expanded slab-chunk by slab-chunk on the device and compared there. */
+int ls_h_max_norm_diff(const int64_t dims[3], int Ra, const double* A0_h, const double* A1_h, const double* A2_h,
+                       const double* wa_h, int Rb, const double* B0_h, const double* B1_h, const double* B2_h,
+                       const double* wb_h, double* max_diff_h, double* max_abs_b_h);
 /* build_lattice_master (lattice.hpp:109-113) / erf master: f_h[l] is
  * (2*L[l]*n x R), column-major. */
 int ls_h_lattice_master(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h,

@@ -51,6 +51,10 @@ SIGNATURES = {
     "ls_gram_reduce": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _vp, _vp]),
     "ls_functional_batch": (_i, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i, _i64, _i64, _i64, _vp, _i64, _vp, _i64,
                                  _vp, _i64, _i, _d, _vp, _vp]),
+    "ls_maxdiff_accumulate": (_i, [_vp, _vp, _i64, _vp, _i, _vp]),
+    "ls_h_newton_master": (_i, [_i, _vp, _d, _vp, _i, _vp, _vp, _vp]),
+    "ls_h_functional_batch": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _d, _vp]),
+    "ls_h_max_norm_diff": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ls_h_lattice_master": (_i, [_i, _vp, _i64, _d, _vp, _i, _vp, _vp, _vp]),
     "ls_h_gen_column": (_i, [_i, _d, _i64, _d, _vp]),
     "ls_h_assemble_axis": (_i, [_vp, _i64, _i, _i, _vp, _i64, _i64, _i, _vp]),

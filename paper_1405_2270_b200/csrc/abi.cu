@@ -251,6 +251,111 @@ int ls_h_gen_column(int mode, double t, int64_t len, double h, double* out_h) {
     return LS_OK;
 }
 
+int ls_h_newton_master(int mode, const int64_t lens[3], double h, const double* tau_h, int R, double* f0_h,
+                       double* f1_h, double* f2_h) {
+    if (!(h > 0.0) || !std::isfinite(h)) return ls::fail(LS_EVALIDATION, "generator: mesh h must be positive");
+    for (int l = 0; l < 3; ++l)
+        if (lens[l] < 2 || lens[l] % 2 != 0)
+            return ls::fail(LS_EVALIDATION, "generator: axis lengths must be even and >= 2");
+    for (int q = 0; q < R; ++q)
+        if (!(tau_h[q] >= 0.0) || !std::isfinite(tau_h[q]))
+            return ls::fail(LS_EVALIDATION, "generator: exponents must be finite and >= 0");
+    if (R == 0) return LS_OK;
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    DevBuf tau;
+    LS_TRY(ls::upload(tau, tau_h, sizeof(double) * R, st->compute));
+    double* outs[3] = {f0_h, f1_h, f2_h};
+    for (int l = 0; l < 3; ++l) {
+        // Axes of equal length share one factor (newton.hpp:60-69).
+        int same = -1;
+        for (int m = 0; m < l; ++m)
+            if (lens[m] == lens[l]) same = m;
+        if (same >= 0) {
+            LS_CUDA(cudaStreamSynchronize(st->compute));
+            std::memcpy(outs[l], outs[same], sizeof(double) * static_cast<size_t>(lens[l] * R));
+            continue;
+        }
+        DevBuf f;
+        LS_TRY(f.alloc(sizeof(double) * static_cast<size_t>(lens[l] * R), st->compute));
+        LS_TRY(ls_gen_master(mode, tau.d(), R, lens[l], h, f.d(), lens[l], st->compute));
+        LS_CUDA(cudaMemcpyAsync(outs[l], f.p, sizeof(double) * lens[l] * R, cudaMemcpyDeviceToHost, st->compute));
+        LS_CUDA(cudaStreamSynchronize(st->compute));
+    }
+    return LS_OK;
+}
+
+int ls_h_functional_batch(const int64_t dims[3], int R, const double* A_h, const double* B_h, const double* C_h,
+                          const double* w_h, int F, const double* X_h, const double* Y_h, const double* Z_h,
+                          double scale, double* out_h) {
+    if (F == 0) return LS_OK;
+    if (R == 0) {
+        for (int f = 0; f < F; ++f) out_h[f] = 0.0;
+        return LS_OK;
+    }
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    DevBuf A, B, C, w, X, Y, Z, out;
+    LS_TRY(ls::upload(A, A_h, sizeof(double) * dims[0] * R, st->compute));
+    LS_TRY(ls::upload(B, B_h, sizeof(double) * dims[1] * R, st->compute));
+    LS_TRY(ls::upload(C, C_h, sizeof(double) * dims[2] * R, st->compute));
+    LS_TRY(ls::upload(w, w_h, sizeof(double) * R, st->compute));
+    LS_TRY(ls::upload(X, X_h, sizeof(double) * dims[0] * F, st->compute));
+    LS_TRY(ls::upload(Y, Y_h, sizeof(double) * dims[1] * F, st->compute));
+    LS_TRY(ls::upload(Z, Z_h, sizeof(double) * dims[2] * F, st->compute));
+    LS_TRY(out.alloc(sizeof(double) * F, st->compute));
+    LS_TRY(ls_functional_batch(A.d(), dims[0], B.d(), dims[1], C.d(), dims[2], w.d(), R, dims[0], dims[1], dims[2],
+                               X.d(), dims[0], Y.d(), dims[1], Z.d(), dims[2], F, scale, out.d(), st->compute));
+    LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double) * F, cudaMemcpyDeviceToHost, st->compute));
+    LS_CUDA(cudaStreamSynchronize(st->compute));
+    return LS_OK;
+}
+
+int ls_h_max_norm_diff(const int64_t dims[3], int Ra, const double* A0_h, const double* A1_h, const double* A2_h,
+                       const double* wa_h, int Rb, const double* B0_h, const double* B1_h, const double* B2_h,
+                       const double* wb_h, double* max_diff_h, double* max_abs_b_h) {
+    *max_diff_h = 0.0;
+    *max_abs_b_h = 0.0;
+    const int64_t slab = dims[0] * dims[1];
+    if (slab == 0 || dims[2] == 0) return LS_OK;
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    const cudaStream_t s = st->compute;
+    const double* ah[3] = {A0_h, A1_h, A2_h};
+    const double* bh[3] = {B0_h, B1_h, B2_h};
+    DevBuf fa[3], fb[3], wa, wb, ga, gb, part;
+    for (int l = 0; l < 3; ++l) {
+        LS_TRY(ls::upload(fa[l], ah[l], sizeof(double) * dims[l] * Ra, s));
+        LS_TRY(ls::upload(fb[l], bh[l], sizeof(double) * dims[l] * Rb, s));
+    }
+    LS_TRY(ls::upload(wa, wa_h, sizeof(double) * std::max(Ra, 1), s));
+    LS_TRY(ls::upload(wb, wb_h, sizeof(double) * std::max(Rb, 1), s));
+    // Both tensors expanded chunk by chunk on the device; the grids never leave HBM
+    // (max_norm_diff_canonical, canonical.hpp:282-301).
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(dims[2], (256ll << 20) / (slab * 8)));
+    LS_TRY(ga.alloc(sizeof(double) * chunk * slab, s));
+    LS_TRY(gb.alloc(sizeof(double) * chunk * slab, s));
+    const int nblocks = 4 * ls::sm_count();
+    LS_TRY(part.alloc(sizeof(double) * 2 * nblocks, s));
+    LS_CUDA(cudaMemsetAsync(part.p, 0, sizeof(double) * 2 * nblocks, s));
+    for (int64_t k0 = 0; k0 < dims[2]; k0 += chunk) {
+        const int64_t k1 = std::min(dims[2], k0 + chunk);
+        LS_TRY(ls_expand(fa[0].d(), dims[0], fa[1].d(), dims[1], fa[2].d(), dims[2], wa.d(), dims[0], dims[1],
+                         dims[2], Ra, k0, k1, ga.d(), 0, 0, nullptr, nullptr, nullptr, nullptr, s));
+        LS_TRY(ls_expand(fb[0].d(), dims[0], fb[1].d(), dims[1], fb[2].d(), dims[2], wb.d(), dims[0], dims[1],
+                         dims[2], Rb, k0, k1, gb.d(), 0, 0, nullptr, nullptr, nullptr, nullptr, s));
+        LS_TRY(ls_maxdiff_accumulate(ga.d(), gb.d(), (k1 - k0) * slab, part.d(), nblocks, s));
+    }
+    std::vector<double> hp(2 * static_cast<size_t>(nblocks));
+    LS_CUDA(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, s));
+    LS_CUDA(cudaStreamSynchronize(s));
+    for (int b = 0; b < nblocks; ++b) {
+        *max_diff_h = std::max(*max_diff_h, hp[2 * b]);
+        *max_abs_b_h = std::max(*max_abs_b_h, hp[2 * b + 1]);
+    }
+    return LS_OK;
+}
+
 int ls_h_lattice_master(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h,
                         int R, double* f0_h, double* f1_h, double* f2_h) {
     if (n < 2 || n % 2 != 0 || !(b > 0.0) || !std::isfinite(b))

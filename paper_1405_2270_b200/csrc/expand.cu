@@ -69,6 +69,7 @@ struct ExpandArgs {
     int64_t n_ichunks;
     int64_t n_units;
     int debug;        // development knobs (LS_EXPAND_DEBUG): 1 no stores, 2 fill once, 4 no tail
+    int accumulate;   // add into out / partial instead of overwriting (rank-chunked expansions)
 };
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -335,7 +336,10 @@ expand_dmma_kernel(const ExpandArgs p) {
                     const int i = ibase + 8 * n + 2 * t;
                     if (i + 1 < p.N1) {
                         if (STORE) {
-                            if (p.vec_store) {
+                            if (p.accumulate) {
+                                row[i] += acc[m][n][0];
+                                row[i + 1] += acc[m][n][1];
+                            } else if (p.vec_store) {
                                 __stcs(reinterpret_cast<double2*>(row + i), make_double2(acc[m][n][0], acc[m][n][1]));
                             } else {
                                 row[i] = acc[m][n][0];
@@ -346,7 +350,7 @@ expand_dmma_kernel(const ExpandArgs p) {
                             fsum += rn_mul(rn_mul(acc[m][n][0], p.rho1[i]), r2) +
                                     rn_mul(rn_mul(acc[m][n][1], p.rho1[i + 1]), r2);
                     } else if (i < p.N1) {
-                        if (STORE) row[i] = acc[m][n][0];
+                        if (STORE) row[i] = p.accumulate ? row[i] + acc[m][n][0] : acc[m][n][0];
                         if (FUNC) fsum += rn_mul(rn_mul(acc[m][n][0], p.rho1[i]), r2);
                     }
                 }
@@ -368,7 +372,8 @@ expand_dmma_kernel(const ExpandArgs p) {
                 if (threadIdx.x == 0) {
                     double sum = 0.0;
                     for (int wv = 0; wv < WARPS; ++wv) sum += red[wv];
-                    p.partial[unit] = rn_mul(sum, p.rho3[p.k0 + kk]);
+                    const double part = rn_mul(sum, p.rho3[p.k0 + kk]);
+                    p.partial[unit] = p.accumulate ? p.partial[unit] + part : part;
                 }
             }
             within = 0;
@@ -485,9 +490,17 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     return LS_OK;
 }
 
+constexpr int kRankChunk = 256;
+
+bool chunk_plan(Plan& out) {
+    int KD, n_tail;
+    split_rank(kRankChunk, KD, n_tail);
+    return plan_for(KD, n_tail, out);
+}
+
 template <bool STORE, bool FUNC>
 int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
-    a.KC = pl.KC;
+    a.KC = std::min(pl.KC, a.KD);
     if (pl.warps == 8) return launch<8, 4, STORE, FUNC>(a, s);
     if (pl.wi == 2) return launch<4, 2, STORE, FUNC>(a, s);
     return launch<4, 1, STORE, FUNC>(a, s);
@@ -500,7 +513,8 @@ extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_
     int KD, n_tail;
     split_rank(std::max(R, 1), KD, n_tail);
     Plan pl;
-    if (!plan_for(KD, n_tail, pl) || k1 < k0) return -1;
+    if (k1 < k0) return -1;
+    if (!plan_for(KD, n_tail, pl) && !chunk_plan(pl)) return -1;
     const int64_t IC = 8 * kTN * pl.wi;
     return ls::ceil_div(N1, IC) * (k1 - k0);
 }
@@ -542,12 +556,40 @@ extern "C" int ls_expand(const double* A_d, int64_t lda, const double* B_d, int6
     a.vec_store = (ldy % 2 == 0 && ldz % 2 == 0 && (reinterpret_cast<uintptr_t>(out_d) & 15) == 0) ? 1 : 0;
     a.rho1 = rho1_d; a.rho2 = rho2_d; a.rho3 = rho3_d; a.partial = partial_d;
     if (const char* dbg = std::getenv("LS_EXPAND_DEBUG")) a.debug = std::atoi(dbg);
-    Plan pl;
-    if (!plan_for(a.KD, a.n_tail, pl)) return ls::fail(LS_EGUARD, "expand: rank too large for the shared-memory tile");
     const bool store = out_d != nullptr;
-    if (store && func) return launch_plan<true, true>(pl, a, s);
-    if (store) return launch_plan<true, false>(pl, a, s);
-    return launch_plan<false, true>(pl, a, s);
+    Plan pl;
+    if (plan_for(a.KD, a.n_tail, pl)) {
+        if (store && func) return launch_plan<true, true>(pl, a, s);
+        if (store) return launch_plan<true, false>(pl, a, s);
+        return launch_plan<false, true>(pl, a, s);
+    }
+    // Ranks beyond one shared-memory tile (e.g. direct sums, rank M0 * cells * R): expand
+    // kRankChunk ranks at a time with one tile plan (so partial-sum units line up), the first
+    // chunk writing and later chunks accumulating.
+    Plan pc;
+    if (!chunk_plan(pc)) return ls::fail(LS_EGUARD, "expand: no tile plan for rank chunks");
+    for (int r0 = 0; r0 < R; r0 += kRankChunk) {
+        const int rc = std::min(kRankChunk, R - r0);
+        ExpandArgs c = a;
+        c.A = A_d + lda * r0;
+        c.B = B_d + ldb * r0;
+        c.C = C_d + ldc * r0;
+        c.w = w_d + r0;
+        c.R = rc;
+        split_rank(rc, c.KD, c.n_tail);
+        c.accumulate = r0 > 0 ? 1 : 0;
+        c.vec_store = a.vec_store;
+        if (c.KC > c.KD) c.KC = c.KD;
+        int rc_status;
+        if (store && func)
+            rc_status = launch_plan<true, true>(pc, c, s);
+        else if (store)
+            rc_status = launch_plan<true, false>(pc, c, s);
+        else
+            rc_status = launch_plan<false, true>(pc, c, s);
+        if (rc_status != LS_OK) return rc_status;
+    }
+    return LS_OK;
 }
 
 extern "C" int ls_sum_partials(const double* partial_d, int64_t count, double* out_d, void* stream) {

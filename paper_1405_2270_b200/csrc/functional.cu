@@ -101,7 +101,41 @@ __global__ void functional_batch_kernel(const double* __restrict__ A, int64_t ld
     }
 }
 
+// Block-partial max |a - b| and max |b| over n entries (max is order-independent: exact).
+__global__ void maxdiff_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                               double* __restrict__ part) {
+    __shared__ double sd[256], sb[256];
+    double md = 0.0, mb = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        md = fmax(md, fabs(a[e] - b[e]));
+        mb = fmax(mb, fabs(b[e]));
+    }
+    sd[threadIdx.x] = md;
+    sb[threadIdx.x] = mb;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sd[threadIdx.x] = fmax(sd[threadIdx.x], sd[threadIdx.x + w]);
+            sb[threadIdx.x] = fmax(sb[threadIdx.x], sb[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = fmax(part[2 * blockIdx.x], sd[0]);
+        part[2 * blockIdx.x + 1] = fmax(part[2 * blockIdx.x + 1], sb[0]);
+    }
+}
+
 }  // namespace
+
+extern "C" int ls_maxdiff_accumulate(const double* a_d, const double* b_d, int64_t n, double* part_d, int nblocks,
+                                     void* stream) {
+    if (n < 0 || nblocks < 1 || nblocks > 4096) return ls::fail(LS_EVALIDATION, "maxdiff: bad arguments");
+    if (n == 0) return LS_OK;
+    maxdiff_kernel<<<nblocks, 256, 0, ls::as_stream(stream)>>>(a_d, b_d, n, part_d);
+    LS_LAUNCHED("maxdiff_kernel");
+    return LS_OK;
+}
 
 extern "C" int ls_eval_points(const double* A_d, int64_t lda, const double* B_d, int64_t ldb,
                               const double* C_d, int64_t ldc, const double* w_d, int R,
