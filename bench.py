@@ -45,10 +45,8 @@ C0 = 1.0
 
 def lattice_for(world: int) -> tuple[int, int, int]:
     """Weak-scaling lattice: 1024^3 points (L = 16^3) per rank, grown along z, then y, then x."""
-    table = {1: (16, 16, 16), 2: (16, 16, 32), 4: (16, 32, 32), 8: (32, 32, 32)}
-    if world in table:
-        return table[world]
-    return (16, 16, 16 * world)
+    from paper_1405_2270_b200.distributed import weak_scaling_lattice
+    return weak_scaling_lattice(world)
 
 
 def fp64_peak_tflops() -> tuple[float, str]:
@@ -94,10 +92,23 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "20"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+        # nvidia-smi needs a moment to start; wait for its first sample (bounded).
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < 5.0:
+            if self.path.exists() and self.path.stat().st_size > 0:
+                break
+            time.sleep(0.02)
+        self.t_start = time.time()
         return self
+
+    def mark(self):
+        """Restrict the summary to samples taken after this call (the timed region)."""
+        self.skip = 0
+        if self.path.exists():
+            self.skip = len(self.path.read_text().splitlines())
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -110,7 +121,7 @@ class ClockSampler:
     def summary(self) -> dict:
         rows = []
         if self.path.exists():
-            for line in self.path.read_text().splitlines():
+            for line in self.path.read_text().splitlines()[getattr(self, "skip", 0):]:
                 parts = [p.strip() for p in line.split(",")]
                 if len(parts) >= 8:
                     rows.append(parts)
@@ -145,8 +156,8 @@ def make_problem(world: int):
 
 
 def slab_range(N3: int, rank: int, world: int) -> tuple[int, int]:
-    per = N3 // world
-    return rank * per, (rank + 1) * per if rank < world - 1 else N3
+    from paper_1405_2270_b200.distributed import slab_range as sr
+    return sr(N3, rank, world)
 
 
 def workload_config(spec, world, rule) -> dict:
@@ -166,32 +177,33 @@ def workload_config(spec, world, rule) -> dict:
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
+    from paper_1405_2270_b200.distributed import ShardedPotential
     L, spec, rule = make_problem(world)
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    L.load_library().ls_set_device(local_rank)
-    N1, N2, N3 = spec.target_dims()
-    k0, k1 = slab_range(N3, rank, world)
-    pipe = L.DevicePipeline(spec, rule, mode="erf", device=dev)
-    out = torch.empty((k1 - k0, N2, N1), dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream(dev)
     lib = L.load_library()
+    lib.ls_set_device(local_rank)
+    N1, N2, N3 = spec.target_dims()
+    shard = ShardedPotential(spec, rule, mode="erf", device=dev)
+    pipe, k0, k1 = shard.pipe, shard.k0, shard.k1
+    out = shard.allocate()
+    stream = torch.cuda.current_stream(dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    for _ in range(args.warmup):
-        pipe.step(out, k0, k1, stream)
-    torch.cuda.synchronize()
-
-    # Timed region: K steps, events around each expansion launch for the roofline.
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = lib.ls_launch_count()
     with ClockSampler(local_rank) as clk:
+        for _ in range(args.warmup):
+            shard.step(out, stream)
+        torch.cuda.synchronize()
+        # Timed region: K steps, events around each expansion launch for the roofline.
+        launches0 = lib.ls_launch_count()
         barrier()
         torch.cuda.synchronize()
+        clk.mark()
         t_start.record(stream)
         for s in range(args.steps):
             pipe.generate(stream)
@@ -202,15 +214,14 @@ def run_ours(args, rank, world, local_rank):
         t_end.record(stream)
         torch.cuda.synchronize()
         barrier()
-    launches = lib.ls_launch_count() - launches0
+        launches = lib.ls_launch_count() - launches0
     ms_total = t_start.elapsed_time(t_end)
     exp_ms = [a.elapsed_time(b) for a, b in ev]
+    exp_mean = statistics.mean(exp_ms)
     if world > 1:
-        tt = torch.tensor([ms_total, statistics.mean(exp_ms)], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms_total, exp_mean], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total, exp_mean = float(tt[0]), float(tt[1])
-    else:
-        exp_mean = statistics.mean(exp_ms)
     ms_step = ms_total / args.steps
     pts_total = float(N1) * N2 * N3
     value = pts_total / (ms_step * 1e-3) / 1e9
@@ -241,6 +252,10 @@ def run_ours(args, rank, world, local_rank):
                     "peak_source": hbm_src},
         "share_of_step": round(exp_mean / ms_step, 4),
     }
+
+    # Energy functional <V, rho> (BASELINE cfg2): fused expansion-reduction over this rank's slabs
+    # + one scalar all_reduce, checked against the 1D rank-term form.
+    energy = run_energy(L, shard, spec, world, dev)
     del out
     torch.cuda.empty_cache()
 
@@ -258,10 +273,33 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs; "
             "unit charge at each cell centre; quadrature rule computed on the host)",
             "config": workload_config(spec, world, rule), "roofline": roofline, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": cpu,
+            "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": cpu, "energy": energy,
             "assembly_note": "generator + assembly are inside every step (replicated per rank)",
         }
         print(json.dumps(line), flush=True)
+
+
+def run_energy(L, shard, spec, world, dev):
+    import torch
+    N = spec.target_dims()
+    h = spec.unit.h
+    rho_np = []
+    for l in range(3):
+        x = (np.arange(N[l]) + 0.5 - N[l] / 2.0) * h
+        rho_np.append(np.exp(-x * x / 2.0))  # rank-1 Gaussian density, centre = box centre, sigma = 1 bohr
+    rho = [torch.as_tensor(r, device=dev) for r in rho_np]
+    shard.energy(rho)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e = shard.energy(rho)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    pipe = shard.pipe
+    X = [torch.as_tensor(r.reshape(-1, 1), device=dev) for r in rho_np]
+    e1d = float(L.DevicePipeline.functional_batch_device([pipe.factor(l).T for l in range(3)], pipe.w, X)[0])
+    return {"value": e, "one_d_value": e1d, "rel_diff_vs_1d": abs(e - e1d) / abs(e1d), "ms": round(ms, 3),
+            "density": "rho(x)=exp(-|x|^2/2) separable, centre = box centre",
+            "path": "fused expansion-reduction over own z-slabs + scalar all_reduce (NCCL)"}
 
 
 def run_e2e(L, spec, rule, k0, k1, args, world, dev):
@@ -383,7 +421,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=3)

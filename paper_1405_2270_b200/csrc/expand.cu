@@ -39,8 +39,6 @@
 
 namespace {
 
-constexpr int kTM = 4;  // j tiles (of 8) per warp
-constexpr int kTN = 4;  // i tiles (of 8) per warp
 constexpr int kNS = 3;  // stages in the A2 ring
 
 struct ExpandArgs {
@@ -142,18 +140,28 @@ __global__ void pack_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t
     }
 }
 
-template <int WARPS, int WI>
+// CTA tile: WARPS warps as WI (along i) x WJ (along j); each warp owns TM x TN 8x8
+// accumulator tiles; MINB CTAs per SM (register budget 64K / (MINB * 32 * WARPS)).
+template <int WARPS_, int WI_, int TM_, int TN_, int MINB_>
 struct Tile {
+    static constexpr int WARPS = WARPS_;
+    static constexpr int WI = WI_;
+    static constexpr int TM = TM_;            // j tiles (of 8) per warp
+    static constexpr int TN = TN_;            // i tiles (of 8) per warp
+    static constexpr int MINB = MINB_;
     static constexpr int WJ = WARPS / WI;
-    static constexpr int IC = 8 * kTN * WI;  // i rows per unit
-    static constexpr int JT = kTM * WJ;      // j tiles (of 8) per stage
+    static constexpr int IC = 8 * TN * WI;    // i rows per unit
+    static constexpr int JT = TM * WJ;        // j tiles (of 8) per stage
     static constexpr int JC = 8 * JT;        // j columns per stage
 };
 
-template <int WARPS, int WI, bool STORE, bool FUNC>
-__global__ void __launch_bounds__(WARPS * 32, 2)
+template <class T, bool STORE, bool FUNC>
+__global__ void __launch_bounds__(T::WARPS * 32, T::MINB)
 expand_dmma_kernel(const ExpandArgs p) {
-    using T = Tile<WARPS, WI>;
+    constexpr int WARPS = T::WARPS;
+    constexpr int WI = T::WI;
+    constexpr int kTM = T::TM;
+    constexpr int kTN = T::TN;
     constexpr int kThreads = WARPS * 32;
     constexpr int IC = T::IC;
     constexpr int JT = T::JT;
@@ -419,42 +427,58 @@ void split_rank(int R, int& KD, int& n_tail) {
 // Shared-memory budget per SM (B200: 228 KB, 227 KB per CTA opt-in, 1 KB reserved per CTA).
 constexpr size_t kSmemPerSM = 228 * 1024;
 
-template <int WARPS, int WI>
+template <class T>
 size_t smem_bytes(int KD, int KC, int n_tail) {
-    using T = Tile<WARPS, WI>;
     const size_t stage = static_cast<size_t>(T::JT) * KC * 32 + static_cast<size_t>(T::JT) * 8 * n_tail;
     return sizeof(double) * (16 + kNS * stage + static_cast<size_t>(T::IC) * KD * 4 +
                              static_cast<size_t>(T::IC) * n_tail + 2 * (4 * static_cast<size_t>(KD) + n_tail));
 }
 
-// Tile plans, best first: (8 warps, 128-row i-chunk, whole rank per stage, 2 CTAs/SM) for the
-// BASELINE ranks; narrower i-chunks and short K-chunks as the rank grows.
+// Tile plans, best first.
+using TileWide = Tile<8, 4, 4, 4, 2>;    // 128-row i-chunk, 32x32 warp tiles, 2 CTAs/SM
+using TileWide3 = Tile<8, 4, 2, 4, 3>;   // same i-chunk, 16x32 warp tiles, 3 CTAs/SM (24 warps/SM)
+using TileMid = Tile<4, 2, 4, 4, 2>;     // 64-row i-chunk (larger ranks)
+using TileNarrow = Tile<4, 1, 4, 4, 2>;  // 32-row i-chunk (largest ranks)
+
 struct Plan {
-    int warps, wi, KC;
+    int id;  // 0 wide, 1 wide3, 2 mid, 3 narrow
+    int KC;
+    int ic;
 };
 
+template <class T>
+bool fits(int KD, int KC, int n_tail) {
+    return static_cast<size_t>(T::MINB) * (smem_bytes<T>(KD, KC, n_tail) + 1024) <= kSmemPerSM;
+}
+
 bool plan_for(int KD, int n_tail, Plan& out) {
-    const Plan cands[] = {{8, 4, 0}, {8, 4, 8}, {4, 2, 4}, {4, 1, 4}, {4, 1, 2}};
-    for (const Plan& c : cands) {
+    int force = -1;
+    if (const char* e = std::getenv("LS_EXPAND_PLAN")) force = std::atoi(e);  // development A/B knob
+    struct Cand {
+        int id, KC;
+    };
+    const Cand cands[] = {{0, 0}, {1, 0}, {0, 8}, {2, 4}, {3, 4}, {3, 2}};
+    for (const Cand& c : cands) {
+        if (force >= 0 && c.id != force) continue;
         const int KC = c.KC == 0 ? KD : std::min(KD, c.KC);
-        size_t bytes;
-        if (c.warps == 8)
-            bytes = smem_bytes<8, 4>(KD, KC, n_tail);
-        else if (c.wi == 2)
-            bytes = smem_bytes<4, 2>(KD, KC, n_tail);
-        else
-            bytes = smem_bytes<4, 1>(KD, KC, n_tail);
-        if (2 * (bytes + 1024) <= kSmemPerSM) {
-            out = {c.warps, c.wi, KC};
+        bool ok = false;
+        int ic = 0;
+        switch (c.id) {
+            case 0: ok = fits<TileWide>(KD, KC, n_tail); ic = TileWide::IC; break;
+            case 1: ok = fits<TileWide3>(KD, KC, n_tail); ic = TileWide3::IC; break;
+            case 2: ok = fits<TileMid>(KD, KC, n_tail); ic = TileMid::IC; break;
+            default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
+        }
+        if (ok) {
+            out = {c.id, KC, ic};
             return true;
         }
     }
     return false;
 }
 
-template <int WARPS, int WI, bool STORE, bool FUNC>
+template <class T, bool STORE, bool FUNC>
 int launch(ExpandArgs& a, cudaStream_t s) {
-    using T = Tile<WARPS, WI>;
     a.n_ichunks = ls::ceil_div(a.N1, T::IC);
     a.n_units = a.n_ichunks * (a.k1 - a.k0);
     a.n_jc = ls::ceil_div(a.N2, T::JC);
@@ -475,15 +499,15 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     if (a.n_units * a.n_jc * a.n_kc >= (int64_t(1) << 31) || a.N1 + T::IC >= (int64_t(1) << 31) ||
         a.N2 + T::JC >= (int64_t(1) << 31))
         return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
-    const size_t smem = smem_bytes<WARPS, WI>(a.KD, a.KC, a.n_tail);
-    auto kern = expand_dmma_kernel<WARPS, WI, STORE, FUNC>;
+    const size_t smem = smem_bytes<T>(a.KD, a.KC, a.n_tail);
+    auto kern = expand_dmma_kernel<T, STORE, FUNC>;
     LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
+    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T::WARPS * 32, smem));
     if (per_sm < 1) return ls::fail(LS_EGUARD, "expand: tile does not fit on an SM");
     const int64_t grid = std::min<int64_t>(a.n_units, (int64_t)ls::sm_count() * per_sm);
     if (grid > 0) {
-        kern<<<(unsigned)grid, WARPS * 32, smem, s>>>(a);
+        kern<<<(unsigned)grid, T::WARPS * 32, smem, s>>>(a);
         LS_LAUNCHED("expand_dmma_kernel");
     }
     LS_CUDA(cudaFreeAsync(bp, s));
@@ -501,9 +525,12 @@ bool chunk_plan(Plan& out) {
 template <bool STORE, bool FUNC>
 int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
     a.KC = std::min(pl.KC, a.KD);
-    if (pl.warps == 8) return launch<8, 4, STORE, FUNC>(a, s);
-    if (pl.wi == 2) return launch<4, 2, STORE, FUNC>(a, s);
-    return launch<4, 1, STORE, FUNC>(a, s);
+    switch (pl.id) {
+        case 0: return launch<TileWide, STORE, FUNC>(a, s);
+        case 1: return launch<TileWide3, STORE, FUNC>(a, s);
+        case 2: return launch<TileMid, STORE, FUNC>(a, s);
+        default: return launch<TileNarrow, STORE, FUNC>(a, s);
+    }
 }
 
 }  // namespace
@@ -515,7 +542,7 @@ extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_
     Plan pl;
     if (k1 < k0) return -1;
     if (!plan_for(KD, n_tail, pl) && !chunk_plan(pl)) return -1;
-    const int64_t IC = 8 * kTN * pl.wi;
+    const int64_t IC = pl.ic;
     return ls::ceil_div(N1, IC) * (k1 - k0);
 }
 
