@@ -66,7 +66,8 @@ struct ExpandArgs {
     double* partial;
     int64_t n_ichunks;
     int64_t n_units;
-    int debug;        // development knobs (LS_EXPAND_DEBUG): 1 no stores, 2 fill once, 4 no tail
+    int debug;        // development knobs (LS_EXPAND_DEBUG): 1 no stores (sink), 2 fill once, 4 no tail,
+                      // 8 scale once, 16 no epilogue at all
     int accumulate;   // add into out / partial instead of overwriting (rank-chunked expansions)
 };
 
@@ -259,7 +260,7 @@ expand_dmma_kernel(const ExpandArgs p) {
             if (FUNC) fsum = 0.0;
             __syncthreads();
         }
-        if (within == per_unit - 1 && unit + static_cast<int>(gridDim.x) < n_units)
+        if (within == per_unit - 1 && unit + static_cast<int>(gridDim.x) < n_units && !(p.debug & 8))
             compute_scale(unit + gridDim.x, scale + (parity ^ 1) * rpad);  // read after the unit barrier
 
         const int slot = st % kNS;
@@ -329,6 +330,7 @@ expand_dmma_kernel(const ExpandArgs p) {
             for (int m = 0; m < kTM; ++m) {
                 const int j = jb + 8 * m + g;
                 if (j >= p.N2) continue;
+                if (p.debug & 16) continue;
                 if (p.debug & 1) {
                     double sx = 0.0;
 #pragma unroll

@@ -14,6 +14,51 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // 4: both, ping-pong unrolled by 2 (no moves)
 template <int MODE, int TM, int TN>
 __global__ void __launch_bounds__(256, 2) loop_kernel(const double* __restrict__ g, double* out, int KD, int NJ) {
+    if (MODE == 7 || MODE == 8) {
+        // smem operands + an epilogue every KD k-steps (MODE 7: streaming stores like the
+        // expansion, MODE 8: drain into a register sink only)
+        __shared__ double sm2[4 * 11 * 32 * 4 + 64];
+        for (int e = threadIdx.x; e < 4 * 11 * 32 * 4; e += 256) sm2[e] = 1.0 + e * 1e-9;
+        __syncthreads();
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+        const double* asw = sm2 + lane;
+        double sink = 0.0;
+        for (int jb = 0; jb < NJ; ++jb) {
+            double acc[TM][TN][2];
+#pragma unroll
+            for (int m = 0; m < TM; ++m)
+#pragma unroll
+                for (int n = 0; n < TN; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+#pragma unroll 1
+            for (int ks = 0; ks < KD; ++ks) {
+                double a[TM], b[TN];
+#pragma unroll
+                for (int m = 0; m < TM; ++m) a[m] = asw[(m * 11 + ks) * 32];
+#pragma unroll
+                for (int n = 0; n < TN; ++n) b[n] = asw[(n * 11 + ks) * 32 + 64];
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) dmma(acc[m][n][0], acc[m][n][1], a[m], b[n]);
+            }
+            if (MODE == 7) {
+                const long base = ((long)(blockIdx.x * 8 + warp) * NJ + jb) * (TM * 8) * 1024;
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n)
+                        __stcs(reinterpret_cast<double2*>(out + 8 + base + (8 * m + g) * 1024 + 8 * n + 2 * t),
+                               make_double2(acc[m][n][0], acc[m][n][1]));
+            } else {
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) sink += acc[m][n][0] + acc[m][n][1];
+            }
+        }
+        if (sink == 1.2345) out[0] = sink;
+        return;
+    }
     __shared__ double sm[4 * 11 * 32 * 4 + 64];
     for (int e = threadIdx.x; e < 4 * 11 * 32 * 4; e += 256) sm[e] = 1.0 + e * 1e-9;
     __syncthreads();
@@ -147,10 +192,10 @@ void run(const char* name, const double* g, double* out, int per_sm = 2) {
 }
 
 int main() {
-    double *g, *out; CK(cudaMalloc(&g, 8 * 8 * 11 * 32 * 8)); CK(cudaMalloc(&out, 8));
+    double *g, *out; CK(cudaMalloc(&g, 8 * 8 * 11 * 32 * 8)); CK(cudaMalloc(&out, (size_t)148 * 2 * 8 * 200 * 32 * 1024 * 8 + 64));
     CK(cudaMemset(g, 0, 8 * 8 * 11 * 32 * 8));
-    run<5, 4, 4>("smem both 4x4", g, out, 2);
-    run<5, 4, 4>("smem both 4x4", g, out, 1);
-    run<0, 4, 4>("const 4x4", g, out, 1);
+    run<5, 4, 4>("smem both 4x4, no epilogue", g, out, 2);
+    run<8, 4, 4>("smem both 4x4, drain to sink every 10 k-steps", g, out, 2);
+    run<7, 4, 4>("smem both 4x4, streaming stores every 10 k-steps", g, out, 2);
     return 0;
 }
