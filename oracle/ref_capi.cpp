@@ -14,6 +14,7 @@
 #include <exception>
 #include <string>
 
+#include "latsum/bundle.hpp"
 #include "latsum/canonical.hpp"
 #include "latsum/errors.hpp"
 #include "latsum/grid.hpp"
@@ -288,6 +289,19 @@ int ref_potential_matrix(double b, int64_t n, int nb, const double* centers, con
         Rank1Basis basis = sample_gaussian_basis(GridSpec(b, n), specs);
         const int64_t d[3] = {n, n, n};
         from_matrix(potential_matrix(basis, make_tensor(d, R, P0, P1, P2, wp), volume_element != 0), V);
+    });
+}
+
+// save_bundle (bundle.hpp:33-54) of a tensor; used to produce the reference-written fixture.
+int ref_save_bundle(const char* path, int64_t n1, int64_t n2, int64_t n3, int R, const double* A, const double* B,
+                    const double* C, const double* w, double h, double ox, double oy, double oz) {
+    return guarded([&] {
+        const int64_t d[3] = {n1, n2, n3};
+        TensorBundle b;
+        b.tensor = make_tensor(d, R, A, B, C, w);
+        b.h = h;
+        b.origin = {ox, oy, oz};
+        save_bundle(path, b);
     });
 }
 

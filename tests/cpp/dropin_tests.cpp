@@ -3,8 +3,13 @@
 // cites the reference test it mirrors (proj/tests/*.cpp). Build:
 //   g++ -std=c++20 -O2 -Iinclude -Iinclude/eigen_compat tests/cpp/dropin_tests.cpp
 //       -Lpaper_1405_2270_b200 -llatsum_cuda -Wl,-rpath,<repo>/paper_1405_2270_b200
+#include <unistd.h>
+
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <iterator>
 #include <functional>
 #include <limits>
 #include <random>
@@ -622,6 +627,107 @@ TEST(Acceptance, Fig5AssembledMatchesDirect) {  // acceptance.cpp:112-115 -> rep
                 static_cast<long>(ds.rank), d.max_diff / d.max_abs_b, secs);
     EXPECT_LE(d.max_diff / d.max_abs_b, 1e-12);
     EXPECT_LT(secs, 60.0);
+}
+
+// ------------------------------------------------------------------ bundle / CSV formats
+std::string golden_dir() {
+    const char* d = std::getenv("LATSUM_GOLDEN_DIR");
+    return d ? d : "tests/golden";
+}
+
+std::string tmp_path(const std::string& name) {
+    return "/tmp/latsum_dropin_" + std::to_string(static_cast<long>(::getpid())) + "_" + name;
+}
+
+TEST(Bundle, RoundTripIsExact) {  // test_bundle.cpp:33-58
+    std::mt19937 gen(71);
+    TensorBundle b;
+    b.tensor = random_tensor(gen, {5, 4, 3}, 3);
+    b.h = 0.125;
+    b.origin = {-1.0, 0.5, 2.0};
+    const std::string path = tmp_path("rt.bin");
+    save_bundle(path, b);
+    TensorBundle r = load_bundle(path);
+    EXPECT_EQ(r.h, b.h);
+    EXPECT_TRUE(r.origin == b.origin);
+    EXPECT_EQ(r.tensor.rank(), 3);
+    for (int l = 0; l < 3; ++l) EXPECT_TRUE((r.tensor.factor(l).array() == b.tensor.factor(l).array()).all());
+    EXPECT_TRUE((r.tensor.weights().array() == b.tensor.weights().array()).all());
+    std::remove(path.c_str());
+}
+
+TEST(Bundle, ReadsAndRewritesReferenceFileBitForBit) {  // bundle.hpp:18-94 (reference-written fixture)
+    const std::string ref = golden_dir() + "/ref_bundle_mc_box.bin";
+    TensorBundle b = load_bundle(ref);
+    EXPECT_TRUE((b.tensor.dims() == Dims3{24, 16, 16}));
+    EXPECT_EQ(b.tensor.rank(), 63);
+    EXPECT_EQ(b.h, 0.25);
+    const std::string path = tmp_path("rewrite.bin");
+    save_bundle(path, b);
+    std::ifstream x(ref, std::ios::binary), y(path, std::ios::binary);
+    std::string bx((std::istreambuf_iterator<char>(x)), std::istreambuf_iterator<char>());
+    std::string by((std::istreambuf_iterator<char>(y)), std::istreambuf_iterator<char>());
+    EXPECT_TRUE(bx == by);
+    // the loaded tensor expands on the GPU like any other
+    DenseTensor3 d = densify(b.tensor);
+    EXPECT_LT(rel_diff(d, scalar_oracle(b.tensor)), 1e-13);
+    std::remove(path.c_str());
+}
+
+TEST(Bundle, RejectsBadFiles) {  // test_bundle.cpp:60-86
+    const std::string path = tmp_path("bad.bin");
+    {
+        std::ofstream o(path, std::ios::binary);
+        o << "NOTABUNDLE";
+    }
+    EXPECT_THROW(load_bundle(path), validation_error);
+    {
+        std::ofstream o(path, std::ios::binary);
+        o.write(bundle_magic, 8);
+        const std::int64_t hdr[4] = {2, 2, 2, 1};
+        o.write(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+    }
+    EXPECT_THROW(load_bundle(path), validation_error);  // truncated
+    EXPECT_THROW(load_bundle(tmp_path("missing.bin")), validation_error);
+    std::remove(path.c_str());
+}
+
+TEST(Csv, ReadsChargesAndBasis) {  // test_bundle.cpp:88-140
+    const std::string c = tmp_path("charges.csv"), bpath = tmp_path("basis.csv"), bad = tmp_path("bad.csv");
+    {
+        std::ofstream o(c);
+        o << "x,y,z,Z\n0,0,0,1\n\n0.25, -0.5, 0.75, 2.5\n";
+    }
+    std::vector<Charge> ch = read_charges_csv(c);
+    ASSERT_EQ(ch.size(), 2u);
+    EXPECT_EQ(ch[1].pos[1], -0.5);
+    EXPECT_EQ(ch[1].Z, 2.5);
+    {
+        std::ofstream o(bpath);
+        o << "0,0,0,0.5\n0.1,0.2,0.3,0.7\n-0.5,0,0,0.9\n";
+    }
+    std::vector<GaussianBasisSpec> bs = read_basis_csv(bpath);
+    ASSERT_EQ(bs.size(), 3u);
+    EXPECT_EQ(bs[2].sigma, 0.9);
+    EXPECT_EQ(bs[2].center[0], -0.5);
+    {
+        std::ofstream o(bad);
+        o << "1,2,3\n";
+    }
+    EXPECT_THROW(read_charges_csv(bad), validation_error);
+    {
+        std::ofstream o(bad);
+        o << "1,2,3,4\nfoo,1,2,3\n";
+    }
+    EXPECT_THROW(read_charges_csv(bad), validation_error);
+    {
+        std::ofstream o(bad);
+        o << "x,y,z,Z\n";
+    }
+    EXPECT_THROW(read_charges_csv(bad), validation_error);
+    EXPECT_THROW(read_charges_csv(tmp_path("nope.csv")), validation_error);
+    EXPECT_EQ(format_double(0.1), std::string("0.10000000000000001"));
+    for (const auto& f : {c, bpath, bad}) std::remove(f.c_str());
 }
 
 int main(int argc, char** argv) { return minitest::run_all(argc, argv); }

@@ -90,6 +90,13 @@ def main():
     # erf moment KAT columns (newton.hpp:21-37): b=3, n=6, t=0.7, both lengths
     g["moment_b3_n6_t07"] = r.gaussian_moment_vector(3.0, 6, 0.7, False)
     g["moment_b3_n6_t07_doubled"] = r.gaussian_moment_vector(3.0, 6, 0.7, True)
+    # a bundle file written by the reference's own save_bundle (bundle.hpp:33-54)
+    r.lib.ref_save_bundle.restype = C.c_int
+    r.lib.ref_save_bundle.argtypes = [C.c_char_p] + [C.c_int64] * 3 + [C.c_int] + [C.POINTER(C.c_double)] * 4 + \
+        [C.c_double] * 4
+    bpath = ROOT / "tests" / "golden" / "ref_bundle_mc_box.bin"
+    r._check(r.lib.ref_save_bundle(str(bpath).encode(), 24, 16, 16, len(wout), dp(f[0]), dp(f[1]), dp(f[2]),
+                                   dp(wout), 0.25, -2.875, -1.875, -1.875), "save_bundle")
     out = ROOT / "tests" / "golden" / "golden_r01.npz"
     np.savez_compressed(out, **g)
     print(out, out.stat().st_size, "bytes,", len(g), "arrays")

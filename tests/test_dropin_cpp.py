@@ -47,7 +47,7 @@ def test_headers_are_self_contained(tmp_path):
 
 @pytest.mark.gpu
 def test_dropin_cases_pass_on_gpu(binary):
-    r = subprocess.run([str(binary)], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([str(binary)], capture_output=True, text=True, timeout=600, cwd=str(ROOT))
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 failed" in r.stdout
