@@ -181,6 +181,7 @@ expand_dmma_kernel(const ExpandArgs p) {
     double* as = ring + kNS * stage_elems;                         // [IC/8][KD][32]
     double* tail = as + IC * KD * 4;                               // [n_tail][IC]
     double* scale = tail + IC * n_tail;                            // [2][rpad] (unit parity)
+    double* r1s = scale + 2 * rpad;                                // [IC] rho1 of the unit (FUNC)
     __shared__ double red[WARPS];
 
     const int warp = threadIdx.x >> 5;
@@ -257,7 +258,10 @@ expand_dmma_kernel(const ExpandArgs p) {
                 const int i = ib + e % IC;
                 tail[e] = i < p.N1 ? rn_mul(__ldg(p.A + i + p.lda * q), sc[q]) : 0.0;
             }
-            if (FUNC) fsum = 0.0;
+            if (FUNC) {
+                fsum = 0.0;
+                for (int e = threadIdx.x; e < IC; e += kThreads) r1s[e] = ib + e < p.N1 ? p.rho1[ib + e] : 0.0;
+            }
             __syncthreads();
         }
         if (within == per_unit - 1 && unit + static_cast<int>(gridDim.x) < n_units && !(p.debug & 8))
@@ -338,30 +342,34 @@ expand_dmma_kernel(const ExpandArgs p) {
                     if (sx == 1.2345) p.out[0] = sx;
                     continue;
                 }
-                double* row = STORE ? p.out + kk * p.ldz + static_cast<int64_t>(j) * p.ldy : nullptr;
-                double r2 = 0.0;
-                if (FUNC) r2 = p.rho2[j];
+                if (FUNC) {
+                    // rho-weighted partial: rows of the tile against rho1 (shared), then rho2(j).
+                    double sm = 0.0;
+#pragma unroll
+                    for (int n = 0; n < kTN; ++n) {
+                        const double2 r = *reinterpret_cast<const double2*>(r1s + wi * (8 * kTN) + 8 * n + 2 * t);
+                        sm = fma(acc[m][n][0], r.x, sm);
+                        sm = fma(acc[m][n][1], r.y, sm);
+                    }
+                    fsum = fma(sm, p.rho2[j], fsum);
+                }
+                if (!STORE) continue;
+                double* row = p.out + kk * p.ldz + static_cast<int64_t>(j) * p.ldy;
 #pragma unroll
                 for (int n = 0; n < kTN; ++n) {
                     const int i = ibase + 8 * n + 2 * t;
                     if (i + 1 < p.N1) {
-                        if (STORE) {
-                            if (p.accumulate) {
-                                row[i] += acc[m][n][0];
-                                row[i + 1] += acc[m][n][1];
-                            } else if (p.vec_store) {
-                                __stcs(reinterpret_cast<double2*>(row + i), make_double2(acc[m][n][0], acc[m][n][1]));
-                            } else {
-                                row[i] = acc[m][n][0];
-                                row[i + 1] = acc[m][n][1];
-                            }
+                        if (p.accumulate) {
+                            row[i] += acc[m][n][0];
+                            row[i + 1] += acc[m][n][1];
+                        } else if (p.vec_store) {
+                            __stcs(reinterpret_cast<double2*>(row + i), make_double2(acc[m][n][0], acc[m][n][1]));
+                        } else {
+                            row[i] = acc[m][n][0];
+                            row[i + 1] = acc[m][n][1];
                         }
-                        if (FUNC)
-                            fsum += rn_mul(rn_mul(acc[m][n][0], p.rho1[i]), r2) +
-                                    rn_mul(rn_mul(acc[m][n][1], p.rho1[i + 1]), r2);
                     } else if (i < p.N1) {
-                        if (STORE) row[i] = p.accumulate ? row[i] + acc[m][n][0] : acc[m][n][0];
-                        if (FUNC) fsum += rn_mul(rn_mul(acc[m][n][0], p.rho1[i]), r2);
+                        row[i] = p.accumulate ? row[i] + acc[m][n][0] : acc[m][n][0];
                     }
                 }
             }
@@ -433,7 +441,8 @@ template <class T>
 size_t smem_bytes(int KD, int KC, int n_tail) {
     const size_t stage = static_cast<size_t>(T::JT) * KC * 32 + static_cast<size_t>(T::JT) * 8 * n_tail;
     return sizeof(double) * (16 + kNS * stage + static_cast<size_t>(T::IC) * KD * 4 +
-                             static_cast<size_t>(T::IC) * n_tail + 2 * (4 * static_cast<size_t>(KD) + n_tail));
+                             static_cast<size_t>(T::IC) * n_tail + 2 * (4 * static_cast<size_t>(KD) + n_tail) +
+                             static_cast<size_t>(T::IC));
 }
 
 // Tile plans, best first.

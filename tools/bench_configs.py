@@ -208,7 +208,7 @@ def main():
     fh = open(a.out, "w") if a.out else None
 
     def emit(d):
-        s = json.dumps({k: (round(v, 6) if isinstance(v, float) else v) for k, v in d.items()})
+        s = json.dumps({k: (float(f"{v:.7g}") if isinstance(v, float) else v) for k, v in d.items()})
         print(s, flush=True)
         if fh:
             fh.write(s + "\n")
