@@ -39,7 +39,6 @@
 
 namespace {
 
-constexpr int kNS = 3;  // stages in the A2 ring
 
 struct ExpandArgs {
     const double* A;
@@ -143,8 +142,9 @@ __global__ void pack_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t
 
 // CTA tile: WARPS warps as WI (along i) x WJ (along j); each warp owns TM x TN 8x8
 // accumulator tiles; MINB CTAs per SM (register budget 64K / (MINB * 32 * WARPS)).
-template <int WARPS_, int WI_, int TM_, int TN_, int MINB_>
+template <int WARPS_, int WI_, int TM_, int TN_, int MINB_, int NS_ = 3>
 struct Tile {
+    static constexpr int NS = NS_;            // stages in the A2 ring
     static constexpr int WARPS = WARPS_;
     static constexpr int WI = WI_;
     static constexpr int TM = TM_;            // j tiles (of 8) per warp
@@ -166,6 +166,7 @@ expand_dmma_kernel(const ExpandArgs p) {
     constexpr int kThreads = WARPS * 32;
     constexpr int IC = T::IC;
     constexpr int JT = T::JT;
+    constexpr int kNS = T::NS;
     // All counters are 32-bit (launch() checks the ranges); only addresses are 64-bit.
     const int KD = p.KD, KC = p.KC, n_tail = p.n_tail, n_kc = p.n_kc;
     const int frag_elems = JT * KC * 32;
@@ -440,7 +441,7 @@ constexpr size_t kSmemPerSM = 228 * 1024;
 template <class T>
 size_t smem_bytes(int KD, int KC, int n_tail) {
     const size_t stage = static_cast<size_t>(T::JT) * KC * 32 + static_cast<size_t>(T::JT) * 8 * n_tail;
-    return sizeof(double) * (16 + kNS * stage + static_cast<size_t>(T::IC) * KD * 4 +
+    return sizeof(double) * (16 + T::NS * stage + static_cast<size_t>(T::IC) * KD * 4 +
                              static_cast<size_t>(T::IC) * n_tail + 2 * (4 * static_cast<size_t>(KD) + n_tail) +
                              static_cast<size_t>(T::IC));
 }
@@ -450,6 +451,9 @@ using TileWide = Tile<8, 4, 4, 4, 2>;    // 128-row i-chunk, 32x32 warp tiles, 2
 using TileWide3 = Tile<8, 4, 2, 4, 3>;   // same i-chunk, 16x32 warp tiles, 3 CTAs/SM (24 warps/SM)
 using TileMid = Tile<4, 2, 4, 4, 2>;     // 64-row i-chunk (larger ranks)
 using TileNarrow = Tile<4, 1, 4, 4, 2>;  // 32-row i-chunk (largest ranks)
+using TileLR1 = Tile<8, 1, 4, 4, 1>;     // large ranks: 32-row i-chunk, 256-column stages, 1 CTA/SM
+using TileLR2 = Tile<8, 2, 4, 4, 1>;     // large ranks: 64-row i-chunk, 128-column stages, 1 CTA/SM
+using TileLR1b = Tile<8, 1, 4, 4, 1, 2>; // as TileLR1 with a 2-deep ring of longer stages
 
 struct Plan {
     int id;  // 0 wide, 1 wide3, 2 mid, 3 narrow
@@ -468,7 +472,9 @@ bool plan_for(int KD, int n_tail, Plan& out) {
     struct Cand {
         int id, KC;
     };
-    const Cand cands[] = {{0, 0}, {1, 0}, {0, 8}, {2, 4}, {3, 4}, {3, 2}};
+    // Measured on B200 (tools/profile_expand.py, tools/profile_rank.py): plan 0 for the BASELINE
+    // rank 41 (29.2 TF/s); plan 8 for rank 328 (28.7 TF/s vs 20.3 for the 4-warp plan 3).
+    const Cand cands[] = {{0, 0}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
     for (const Cand& c : cands) {
         if (force >= 0 && c.id != force) continue;
         const int KC = c.KC == 0 ? KD : std::min(KD, c.KC);
@@ -478,10 +484,14 @@ bool plan_for(int KD, int n_tail, Plan& out) {
             case 0: ok = fits<TileWide>(KD, KC, n_tail); ic = TileWide::IC; break;
             case 1: ok = fits<TileWide3>(KD, KC, n_tail); ic = TileWide3::IC; break;
             case 2: ok = fits<TileMid>(KD, KC, n_tail); ic = TileMid::IC; break;
+            case 6: ok = fits<TileLR1>(KD, KC, n_tail); ic = TileLR1::IC; break;
+            case 7: ok = fits<TileLR2>(KD, KC, n_tail); ic = TileLR2::IC; break;
+            case 8: ok = fits<TileLR1b>(KD, KC, n_tail); ic = TileLR1b::IC; break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
         }
         if (ok) {
             out = {c.id, KC, ic};
+            if (const char* e = std::getenv("LS_EXPAND_KC")) out.KC = std::max(1, std::min(KD, std::atoi(e)));
             return true;
         }
     }
@@ -540,6 +550,9 @@ int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
         case 0: return launch<TileWide, STORE, FUNC>(a, s);
         case 1: return launch<TileWide3, STORE, FUNC>(a, s);
         case 2: return launch<TileMid, STORE, FUNC>(a, s);
+        case 6: return launch<TileLR1, STORE, FUNC>(a, s);
+        case 7: return launch<TileLR2, STORE, FUNC>(a, s);
+        case 8: return launch<TileLR1b, STORE, FUNC>(a, s);
         default: return launch<TileNarrow, STORE, FUNC>(a, s);
     }
 }
