@@ -266,6 +266,10 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(spec, rule, budget_s=args.cpu_seconds)
 
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = run_other_configs(L, dev)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -274,9 +278,85 @@ def run_ours(args, rank, world, local_rank):
             "unit charge at each cell centre; quadrature rule computed on the host)",
             "config": workload_config(spec, world, rule), "roofline": roofline, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": cpu, "energy": energy,
+            "other_configs": configs,
             "assembly_note": "generator + assembly are inside every step (replicated per rank)",
         }
         print(json.dumps(line), flush=True)
+
+
+def _ev_ms(fn, reps=3):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = float("inf")
+    for _ in range(reps):
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return best
+
+
+def run_other_configs(L, dev):
+    """The other BASELINE configs, measured live on this GPU (device time, inputs in HBM):
+    cfg0 full step; cfg3 (8 atoms, rank 328) assembly and one 8-GPU z-shard of the expansion;
+    cfg4 (periodic n=256, L=256) assembly, 256^3 expansion and the batch of 1024 functionals.
+    cfg2 (2048^3) is the N=8 point of the scaling run; its 1-GPU numbers are in profiles/."""
+    import torch
+    out = {}
+    # cfg0
+    spec = L.LatticeSpec((4, 4, 4), L.GridSpec(B, n_CELL), [L.Charge((0.0, 0.0, 0.0), 1.0)])
+    rule = L.sinc_quadrature(EPS, spec.unit.h, math.sqrt(3.0) * 4 * B, M_QUAD, C0)
+    pipe = L.DevicePipeline(spec, rule, mode="erf", device=dev)
+    grid = torch.empty(tuple(reversed(pipe.dims)), dtype=torch.float64, device=dev)
+    t = _ev_ms(lambda: pipe.step(grid))
+    out["cfg0"] = {"grid": list(pipe.dims), "rank": pipe.Rt, "step_ms": round(t, 4),
+                   "gpts": round(float(np.prod(pipe.dims)) / (t * 1e-3) / 1e9, 2)}
+    del grid
+    # cfg3: 8 atoms at seeded vertices in [0.1b, 0.9b]^3, Z in 1..8, L = 32
+    rng = np.random.default_rng(20241019)
+    h = B / n_CELL
+    ia = rng.integers(7, 58, size=(8, 3))
+    Z = rng.integers(1, 9, size=8).astype(float)
+    spec = L.LatticeSpec((32, 32, 32), L.GridSpec(B, n_CELL), [L.Charge(tuple(ia[c] * h - B / 2), Z[c]) for c in range(8)])
+    rule = L.sinc_quadrature(EPS, h, math.sqrt(3.0) * 32 * B, M_QUAD, C0)
+    pipe = L.DevicePipeline(spec, rule, mode="erf", device=dev)
+    N = pipe.dims
+    k1 = N[2] // 8
+    shard = torch.empty((k1, N[1], N[0]), dtype=torch.float64, device=dev)
+    t_asm = _ev_ms(lambda: (pipe.generate(), pipe.assemble()))
+    t_exp = _ev_ms(lambda: pipe.expand(shard, 0, k1))
+    out["cfg3"] = {"grid": list(N), "rank": pipe.Rt, "generator_plus_assembly_ms": round(t_asm, 4),
+                   "shard8_expand_ms": round(t_exp, 3),
+                   "shard8_tflops": round(2 * pipe.Rt * N[0] * N[1] * k1 / (t_exp * 1e-3) / 1e12, 2),
+                   "full_grid_at_8_gpus_gpts": round(8 * N[0] * N[1] * k1 / (t_exp * 1e-3) / 1e9, 1)}
+    del shard
+    torch.cuda.empty_cache()
+    # cfg4: periodic, L = 256, n = 256 (master 131072 per axis), 1024 Gaussian test functions
+    spec = L.LatticeSpec((256, 256, 256), L.GridSpec(B, 256), [L.Charge((0.0, 0.0, 0.0), 1.0)])
+    rule = L.sinc_quadrature(EPS, spec.unit.h, math.sqrt(3.0) * 256 * B, M_QUAD, C0)
+    pipe = L.DevicePipeline(spec, rule, mode="erf", periodic=True, device=dev)
+    grid = torch.empty(tuple(reversed(pipe.dims)), dtype=torch.float64, device=dev)
+    t_asm = _ev_ms(lambda: (pipe.generate(), pipe.assemble()))
+    t_exp = _ev_ms(lambda: pipe.expand(grid))
+    rng = np.random.default_rng(4)
+    F = 1024
+    alpha = 10 ** rng.uniform(-1, 1, F)
+    sigma = 1 / np.sqrt(2 * alpha)
+    centres = rng.uniform(-B / 2, B / 2, (F, 3))
+    mids = (np.arange(256) + 0.5 - 128) * spec.unit.h
+    G = [torch.as_tensor(np.exp(-(mids[:, None] - centres[None, :, l]) ** 2 / (2 * sigma ** 2)), device=dev)
+         for l in range(3)]
+    t_f = _ev_ms(lambda: L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w, G))
+    out["cfg4_L256"] = {"grid": list(pipe.dims), "rank": pipe.Rt, "master_len": 2 * 256 * 256,
+                        "generator_plus_assembly_ms": round(t_asm, 4), "expand_ms": round(t_exp, 4),
+                        "expand_gpts": round(float(np.prod(pipe.dims)) / (t_exp * 1e-3) / 1e9, 1),
+                        "functionals_1024_ms": round(t_f, 4)}
+    del grid
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_energy(L, shard, spec, world, dev):
@@ -427,6 +507,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg0/cfg3/cfg4 side measurements")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
