@@ -133,6 +133,36 @@ int ls_functional_batch(const double* A_d, int64_t lda, const double* B_d, int64
 int ls_maxdiff_accumulate(const double* a_d, const double* b_d, int64_t n, double* part_d, int nblocks,
                           void* stream);
 
+/* ---- device-resident pipeline (native runtime object) -------------------
+ * generator -> assembled sum -> expansion -> functional with every stage in
+ * HBM on the current device; the handle owns the master, assembled factors
+ * and weights (Z_nu * w_q). charges_h holds M0 rows (x, y, z, Z) in
+ * unit-cell coordinates [-b/2, b/2] (validated and snapped like
+ * LatticeSpec, lattice.hpp:28-69). dims = n^3 (periodic) or (L*n)^3-shaped. */
+typedef struct ls_pipeline ls_pipeline;
+int ls_pipeline_create(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h, const double* w_h,
+                       int R, const double* charges_h, int M0, int periodic, ls_pipeline** out);
+int ls_pipeline_destroy(ls_pipeline* p);
+/* dims, total rank M0*R and the device factors / weights (any output may be NULL). */
+int ls_pipeline_info(const ls_pipeline* p, int64_t dims[3], int* rank_total, const double** A_d,
+                     const double** B_d, const double** C_d, const double** w_d);
+int ls_pipeline_generate(ls_pipeline* p, void* stream);
+int ls_pipeline_assemble(ls_pipeline* p, void* stream);
+/* slabs [k0, k1) into out_d (dense, i-fastest, (k1-k0)*N1*N2 doubles). */
+int ls_pipeline_expand(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void* stream);
+int ls_pipeline_step(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void* stream);
+/* out_d[0] = sum over slabs [k0,k1) of V * rho1(i) rho2(j) rho3(k) (fused, V never stored). */
+int ls_pipeline_energy(ls_pipeline* p, const double* r1_d, const double* r2_d, const double* r3_d, int64_t k0,
+                       int64_t k1, double* out_d, void* stream);
+
+/* Small runtime helpers for callers without the CUDA headers: device memory
+ * on the current device, a synchronous copy in any direction (cudaMemcpyDefault
+ * on `stream`), and a stream wait. */
+int ls_device_malloc(size_t bytes, void** out_d);
+int ls_device_free(void* p_d);
+int ls_memcpy(void* dst, const void* src, size_t bytes, void* stream);
+int ls_synchronize(void* stream);
+
 /* ---- host-level entry points (drop-in headers, e2e path) ----------------
  * Synchronous; all pointers host memory; results copied back. */
 /* build_newton_master(lens, h, rule) (newton.hpp:57-75) in either generator

@@ -55,6 +55,18 @@ SIGNATURES = {
     "ls_h_newton_master": (_i, [_i, _vp, _d, _vp, _i, _vp, _vp, _vp]),
     "ls_h_functional_batch": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _d, _vp]),
     "ls_h_max_norm_diff": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "ls_pipeline_create": (_i, [_i, _vp, _i64, _d, _vp, _vp, _i, _vp, _i, _i, C.POINTER(_vp)]),
+    "ls_pipeline_destroy": (_i, [_vp]),
+    "ls_pipeline_info": (_i, [_vp, _vp, C.POINTER(_i), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
+    "ls_pipeline_generate": (_i, [_vp, _vp]),
+    "ls_pipeline_assemble": (_i, [_vp, _vp]),
+    "ls_pipeline_expand": (_i, [_vp, _i64, _i64, _vp, _vp]),
+    "ls_pipeline_step": (_i, [_vp, _i64, _i64, _vp, _vp]),
+    "ls_pipeline_energy": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp]),
+    "ls_device_malloc": (_i, [C.c_size_t, C.POINTER(_vp)]),
+    "ls_device_free": (_i, [_vp]),
+    "ls_memcpy": (_i, [_vp, _vp, C.c_size_t, _vp]),
+    "ls_synchronize": (_i, [_vp]),
     "ls_h_lattice_master": (_i, [_i, _vp, _i64, _d, _vp, _i, _vp, _vp, _vp]),
     "ls_h_gen_column": (_i, [_i, _d, _i64, _d, _vp]),
     "ls_h_assemble_axis": (_i, [_vp, _i64, _i, _i, _vp, _i64, _i64, _i, _vp]),

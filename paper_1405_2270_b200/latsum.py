@@ -421,12 +421,22 @@ def functional_batch(P: CanonicalTensor3, rho: Sequence[np.ndarray], scale: floa
 
 
 # ---------------------------------------------------------- device pipeline
-class DevicePipeline:
-    """Generator -> assembly -> expansion with every stage resident in HBM.
+class _DeviceView:
+    """Zero-copy torch view of device memory owned by the native pipeline (CUDA array interface)."""
 
-    Device memory and streams come from torch (plumbing only); all compute is
-    liblatsum_cuda.so. Factors are kept as (R, len) row-major tensors, i.e.
-    column-major (len x R) matrices with leading dimension len.
+    def __init__(self, ptr: int, shape: tuple[int, ...]):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f8", "data": (ptr, False), "version": 2,
+                                         "strides": None}
+
+
+class DevicePipeline:
+    """Generator -> assembly -> expansion -> functional, every stage resident in HBM.
+
+    A thin handle on the native pipeline object of liblatsum_cuda.so
+    (``ls_pipeline_*``, csrc/pipeline.cu), which owns the master, the assembled
+    factors and the weights. torch provides output buffers and streams only;
+    factors are exposed as zero-copy (R, N_l) views, i.e. column-major
+    (N_l x R) matrices with leading dimension N_l.
     """
 
     def __init__(self, spec: LatticeSpec, rule: QuadratureRule, mode: str = "erf", periodic: bool = False,
@@ -436,93 +446,73 @@ class DevicePipeline:
         self.torch = torch
         self.spec, self.rule, self.mode, self.periodic = spec, rule, mode, periodic
         self.dev = torch.device("cuda") if device is None else torch.device(device)
-        n = spec.unit.n
-        self.h = spec.unit.h
+        self._lib = _abi.load()
+        L = np.array(spec.L, dtype=np.int64)
+        ch = np.array([[*c.pos, c.Z] for c in spec.charges], dtype=np.float64)
+        tau = _f64(rule.exponents).ravel()
+        w = _f64(rule.weights).ravel()
+        handle = C.c_void_p()
+        with torch.cuda.device(self.dev):
+            call("ls_pipeline_create", MODES[mode], _p(L), spec.unit.n, spec.unit.b, _p(tau), _p(w),
+                 rule.node_count(), _p(ch), len(ch), int(periodic), C.byref(handle))
+        self._h = handle
+        dims = np.zeros(3, dtype=np.int64)
+        rt = C.c_int(0)
+        ptrs = [C.c_void_p() for _ in range(4)]
+        call("ls_pipeline_info", self._h, _p(dims), C.byref(rt), *(C.byref(q) for q in ptrs))
+        self.dims = tuple(int(d) for d in dims)
+        self.Rt = rt.value
         self.R = rule.node_count()
         self.M0 = spec.charge_count()
-        self.Rt = self.M0 * self.R
-        self.dims = (n, n, n) if periodic else spec.target_dims()
-        t = lambda a, dt=torch.float64: torch.as_tensor(np.asarray(a), dtype=dt, device=self.dev)  # noqa: E731
-        self.tau = t(rule.exponents)
-        self.w = t([c.Z * wq for c in spec.charges for wq in rule.weights])
-        self.ia = [t([spec.charge_grid_index(l, nu) for nu in range(self.M0)], torch.int64) for l in range(3)]
-        # Distinct axes (equal L and equal charge indices give bit-identical factors).
-        self.axis_src = []
-        for l in range(3):
-            src = l
-            for m in range(l):
-                if spec.L[m] == spec.L[l] and torch.equal(self.ia[m], self.ia[l]):
-                    src = m
-                    break
-            self.axis_src.append(src)
-        self.master = [torch.empty((self.R, 2 * spec.L[l] * n), dtype=torch.float64, device=self.dev)
-                       if self.axis_src[l] == l else None for l in range(3)]
-        self.fac = [torch.empty((self.Rt, self.dims[l]), dtype=torch.float64, device=self.dev)
-                    if self.axis_src[l] == l else None for l in range(3)]
-        self.launches = 0
+        self._fac = [torch.as_tensor(_DeviceView(ptrs[l].value, (self.Rt, self.dims[l])), device=self.dev)
+                     for l in range(3)]
+        self.w = torch.as_tensor(_DeviceView(ptrs[3].value, (self.Rt,)), device=self.dev)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.ls_pipeline_destroy(h)
+            self._h = None
 
     @staticmethod
     def _ptr(x):
         return C.c_void_p(x.data_ptr()) if x is not None else None
 
     def factor(self, l):
-        return self.fac[self.axis_src[l]]
+        return self._fac[l]
 
     def _stream(self, stream):
         s = stream if stream is not None else self.torch.cuda.current_stream(self.dev)
         return C.c_void_p(s.cuda_stream)
 
     def generate(self, stream=None):
-        s = self._stream(stream)
-        for l in range(3):
-            if self.master[l] is not None:
-                length = self.master[l].shape[1]
-                call("ls_gen_master", MODES[self.mode], self._ptr(self.tau), self.R, length, self.h,
-                     self._ptr(self.master[l]), length, s)
-                self.launches += 1
+        call("ls_pipeline_generate", self._h, self._stream(stream))
 
     def assemble(self, stream=None):
-        s = self._stream(stream)
-        n = self.spec.unit.n
-        for l in range(3):
-            if self.fac[l] is not None:
-                call("ls_assemble_axis", self._ptr(self.master[l]), self.master[l].shape[1], self.R, self.M0,
-                     self._ptr(self.ia[l]), n, self.spec.L[l], int(self.periodic), self._ptr(self.fac[l]),
-                     self.dims[l], s)
-                self.launches += 1
+        call("ls_pipeline_assemble", self._h, self._stream(stream))
 
-    def expand(self, out, k0=0, k1=None, stream=None, rho=None, partial=None):
-        """Writes slabs [k0, k1) into `out` (a (k1-k0, N2, N1) float64 tensor) or, with rho, only
-        the per-unit functional partials."""
+    def expand(self, out, k0=0, k1=None, stream=None):
+        """Writes slabs [k0, k1) into `out` (a contiguous (k1-k0, N2, N1) float64 tensor)."""
         k1 = self.dims[2] if k1 is None else k1
-        N1, N2, N3 = self.dims
-        A, B, Cf = (self.factor(l) for l in range(3))
-        r = rho if rho is not None else (None, None, None)
-        call("ls_expand", self._ptr(A), N1, self._ptr(B), N2, self._ptr(Cf), N3, self._ptr(self.w), N1, N2, N3,
-             self.Rt, k0, k1, self._ptr(out), 0, 0, self._ptr(r[0]), self._ptr(r[1]), self._ptr(r[2]),
-             self._ptr(partial), self._stream(stream))
-        self.launches += 1
+        call("ls_pipeline_expand", self._h, k0, k1, self._ptr(out), self._stream(stream))
 
     def step(self, out, k0=0, k1=None, stream=None):
         """One pass of the hot path: generate, assemble, expand into `out`."""
-        self.generate(stream)
-        self.assemble(stream)
-        self.expand(out, k0, k1, stream)
+        k1 = self.dims[2] if k1 is None else k1
+        call("ls_pipeline_step", self._h, k0, k1, self._ptr(out), self._stream(stream))
 
     def partial_count(self, k0=0, k1=None):
         k1 = self.dims[2] if k1 is None else k1
-        return int(_abi.load().ls_expand_partial_count(self.dims[0], self.dims[1], self.Rt, k0, k1))
+        return int(self._lib.ls_expand_partial_count(self.dims[0], self.dims[1], self.Rt, k0, k1))
 
     def grid_functional(self, rho, k0=0, k1=None, stream=None):
         """sum V*rho over slabs [k0, k1) fused into the expansion (V not stored); returns a
         1-element device tensor."""
-        torch = self.torch
-        npart = self.partial_count(k0, k1)
-        partial = torch.zeros(max(npart, 1), dtype=torch.float64, device=self.dev)
-        out = torch.zeros(1, dtype=torch.float64, device=self.dev)
-        self.expand(None, k0, k1, stream, rho=rho, partial=partial)
-        call("ls_sum_partials", self._ptr(partial), npart, self._ptr(out), self._stream(stream))
-        self.launches += 1
+        k1 = self.dims[2] if k1 is None else k1
+        out = self.torch.zeros(1, dtype=self.torch.float64, device=self.dev)
+        r = [x.contiguous() for x in rho]
+        call("ls_pipeline_energy", self._h, self._ptr(r[0]), self._ptr(r[1]), self._ptr(r[2]), k0, k1,
+             self._ptr(out), self._stream(stream))
         return out
 
     @staticmethod

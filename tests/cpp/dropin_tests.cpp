@@ -629,6 +629,48 @@ TEST(Acceptance, Fig5AssembledMatchesDirect) {  // acceptance.cpp:112-115 -> rep
     EXPECT_LT(secs, 60.0);
 }
 
+// ------------------------------------------------------------------ device-resident API
+TEST(DevicePotential, MatchesHostPipelineAndEnergy) {  // additive API over ls_pipeline_*
+    LatticeSpec spec = make_spec({3, 2, 2}, 8, 2.0, {Charge{{0.0, 0.0, 0.0}, 1.0}, Charge{{0.5, -0.25, 0.25}, 2.0}});
+    QuadratureRule rule = sinc_quadrature(1e-4, spec.unit.h(), std::sqrt(3.0) * 6.0, 10, 1.0);
+    DevicePotential dev(spec, rule, Generator::midpoint);
+    const Dims3 d = dev.dims();
+    EXPECT_TRUE((d == Dims3{24, 16, 16}));
+    EXPECT_EQ(dev.rank(), 2 * rule.node_count());
+    DeviceBuffer grid(static_cast<std::size_t>(d[0] * d[1] * d[2]));
+    dev.step(0, d[2], grid.data());
+    std::vector<double> got(grid.size());
+    grid.download(got.data(), got.size());
+    // the same lattice through the drop-in host path
+    SumResult s = assembled_box_sum(spec, build_lattice_master(spec, rule));
+    DenseTensor3 want = densify(s.tensor);
+    double md = 0.0;
+    for (std::size_t e = 0; e < got.size(); ++e) md = std::max(md, std::abs(got[e] - want.data()[static_cast<Index>(e)]));
+    EXPECT_LT(md / max_abs(want), 1e-14);
+    CanonicalTensor3 t = dev.tensor();
+    for (int l = 0; l < 3; ++l) EXPECT_TRUE((t.factor(l).array() == s.tensor.factor(l).array()).all());
+    // energy against the 1D form (scalar_product with a rank-1 density)
+    std::array<Vector, 3> r;
+    for (int l = 0; l < 3; ++l) {
+        r[l].resize(d[l]);
+        for (Index i = 0; i < d[l]; ++i) r[l][i] = 1.0 / (1.0 + static_cast<double>(i));
+    }
+    DeviceBuffer r1(d[0]), r2(d[1]), r3(d[2]), e(1);
+    r1.upload(r[0].data(), d[0]);
+    r2.upload(r[1].data(), d[1]);
+    r3.upload(r[2].data(), d[2]);
+    dev.energy(r1.data(), r2.data(), r3.data(), 0, d[2], e.data());
+    double energy = 0.0;
+    e.download(&energy, 1);
+    std::array<Matrix, 3> rf{Matrix(r[0]), Matrix(r[1]), Matrix(r[2])};
+    const double want_e = scalar_product(s.tensor, CanonicalTensor3(std::move(rf), Vector::Ones(1)));
+    EXPECT_NEAR(energy, want_e, 1e-12 * std::abs(want_e));
+    // z-slab shards cover the grid exactly once
+    Index covered = 0;
+    for (int rk = 0; rk < 3; ++rk) covered += slab_range(d[2], rk, 3).second - slab_range(d[2], rk, 3).first;
+    EXPECT_EQ(covered, d[2]);
+}
+
 // ------------------------------------------------------------------ bundle / CSV formats
 std::string golden_dir() {
     const char* d = std::getenv("LATSUM_GOLDEN_DIR");
