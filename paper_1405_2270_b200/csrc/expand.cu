@@ -33,6 +33,7 @@
 // One __syncthreads per stage guards ring-slot reuse; units are spread over
 // a persistent grid (CTAs per SM x SM count).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -68,6 +69,7 @@ struct ExpandArgs {
     int debug;        // development knobs (LS_EXPAND_DEBUG): 1 no stores (sink), 2 fill once, 4 no tail,
                       // 8 scale once, 16 no epilogue at all
     int accumulate;   // add into out / partial instead of overwriting (rank-chunked expansions)
+    const double* S;  // per-slab scales S(k, q) = w_q * A3(k, q), [k][q] (TMEM variant)
 };
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -85,6 +87,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     asm volatile(
@@ -405,6 +410,17 @@ expand_dmma_kernel(const ExpandArgs p) {
     }
 }
 
+__global__ void scale_table_kernel(const double* __restrict__ w, const double* __restrict__ C, int64_t ldc, int R,
+                                   int64_t k1, double* __restrict__ S) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k1 * R; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e / R;
+        const int q = static_cast<int>(e % R);
+        S[e] = rn_mul(w[q], C[k + ldc * q]);  // canonical.hpp:244
+    }
+}
+
+#include "expand_tmem.cuh"
+
 __global__ void sum_partials_kernel(const double* __restrict__ part, int64_t count,
                                     double* __restrict__ out) {
     // One block, fixed order: thread-strided partial sums, then a fixed tree.
@@ -456,10 +472,34 @@ using TileLR2 = Tile<8, 2, 4, 4, 1>;     // large ranks: 64-row i-chunk, 128-col
 using TileLR1b = Tile<8, 1, 4, 4, 1, 2>; // as TileLR1 with a 2-deep ring of longer stages
 
 struct Plan {
-    int id;  // 0 wide, 1 wide3, 2 mid, 3 narrow
+    int id;  // see plan_for; 20 = TileWide geometry with A1k in TMEM
     int KC;
     int ic;
 };
+
+constexpr int kPlanTmem = 20;
+// TMEM variant shape (ring depth, j-chunks per stage); LS_EXPAND_TMEM=<ns><jps> overrides.
+struct TmemShape {
+    int ns, jps;
+};
+inline TmemShape tmem_shape() {
+    TmemShape sh{4, 1};
+    if (const char* e = std::getenv("LS_EXPAND_TMEM")) {
+        const int v = std::atoi(e);
+        sh = {v / 10, v % 10};
+    }
+    return sh;
+}
+
+// The TMEM variant: TileWide geometry, whole rank per stage, A1k double-buffered in 256 TMEM
+// columns (KD <= 14, at most one tail rank); shared memory holds only the A2 ring.
+bool fits_tmem(int KD, int n_tail) {
+    if (KD > 14 || n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > kTmemCols) return false;
+    const TmemShape sh = tmem_shape();
+    const size_t jt = static_cast<size_t>(TileWide::JT) * sh.jps;
+    const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
+    return 2 * (sizeof(double) * (32 + sh.ns * stage) + 1024) <= kSmemPerSM;
+}
 
 template <class T>
 bool fits(int KD, int KC, int n_tail) {
@@ -474,7 +514,7 @@ bool plan_for(int KD, int n_tail, Plan& out) {
     };
     // Measured on B200 (tools/profile_expand.py, tools/profile_rank.py): plan 0 for the BASELINE
     // rank 41 (29.2 TF/s); plan 8 for rank 328 (28.7 TF/s vs 20.3 for the 4-warp plan 3).
-    const Cand cands[] = {{0, 0}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
+    const Cand cands[] = {{kPlanTmem, 0}, {0, 0}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
     for (const Cand& c : cands) {
         if (force >= 0 && c.id != force) continue;
         const int KC = c.KC == 0 ? KD : std::min(KD, c.KC);
@@ -487,6 +527,7 @@ bool plan_for(int KD, int n_tail, Plan& out) {
             case 6: ok = fits<TileLR1>(KD, KC, n_tail); ic = TileLR1::IC; break;
             case 7: ok = fits<TileLR2>(KD, KC, n_tail); ic = TileLR2::IC; break;
             case 8: ok = fits<TileLR1b>(KD, KC, n_tail); ic = TileLR1b::IC; break;
+            case kPlanTmem: ok = fits_tmem(KD, n_tail); ic = TileWide::IC; break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
         }
         if (ok) {
@@ -498,35 +539,62 @@ bool plan_for(int KD, int n_tail, Plan& out) {
     return false;
 }
 
-template <class T, bool STORE, bool FUNC>
+template <class T, bool STORE, bool FUNC, bool TMEM = false>
 int launch(ExpandArgs& a, cudaStream_t s) {
+    const TmemShape sh = TMEM ? tmem_shape() : TmemShape{T::NS, 1};
+    const int JT = T::JT * sh.jps, JC = T::JC * sh.jps;
+    if (TMEM) a.KC = a.KD;
     a.n_ichunks = ls::ceil_div(a.N1, T::IC);
     a.n_units = a.n_ichunks * (a.k1 - a.k0);
-    a.n_jc = ls::ceil_div(a.N2, T::JC);
-    a.n_jt = a.n_jc * T::JT;
+    a.n_jc = ls::ceil_div(a.N2, JC);
+    a.n_jt = a.n_jc * JT;
     a.n_kc = static_cast<int>(ls::ceil_div(a.KD, a.KC));
     // Pack A2 once per call (stream-ordered scratch from the pool).
     double* bp = nullptr;
-    const size_t stage_elems = static_cast<size_t>(T::JT) * a.KC * 32 + static_cast<size_t>(T::JT) * 8 * a.n_tail;
+    const size_t stage_elems = static_cast<size_t>(JT) * a.KC * 32 + static_cast<size_t>(JT) * 8 * a.n_tail;
     const size_t bp_elems = static_cast<size_t>(a.n_kc) * a.n_jc * stage_elems;
+    const size_t s_elems = TMEM ? static_cast<size_t>(a.k1) * a.R : 0;
     ls::ensure_pool();
-    LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bp), bp_elems * sizeof(double), s));
+    LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bp), (bp_elems + s_elems) * sizeof(double), s));
+    if (TMEM) {
+        double* S = bp + bp_elems;
+        const int64_t ns = a.k1 * a.R;
+        scale_table_kernel<<<(unsigned)std::min<int64_t>(ls::ceil_div(ns, 256), 4096), 256, 0, s>>>(a.w, a.C, a.ldc,
+                                                                                                      a.R, a.k1, S);
+        LS_LAUNCHED("scale_table_kernel");
+        a.S = S;
+    }
     const int64_t pb = std::min<int64_t>(ls::ceil_div(static_cast<int64_t>(bp_elems), 256), 4096);
-    pack_b_kernel<<<(unsigned)pb, 256, 0, s>>>(a.B, a.ldb, a.N2, a.R, a.KD, a.n_tail, a.KC, a.n_kc, T::JT, a.n_jc,
-                                               bp);
+    pack_b_kernel<<<(unsigned)pb, 256, 0, s>>>(a.B, a.ldb, a.N2, a.R, a.KD, a.n_tail, a.KC, a.n_kc, JT, a.n_jc, bp);
     LS_LAUNCHED("pack_b_kernel");
     a.Bp = bp;
     // 32-bit counters inside the kernel
     if (a.n_units * a.n_jc * a.n_kc >= (int64_t(1) << 31) || a.N1 + T::IC >= (int64_t(1) << 31) ||
-        a.N2 + T::JC >= (int64_t(1) << 31))
+        a.N2 + JC >= (int64_t(1) << 31))
         return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
-    const size_t smem = smem_bytes<T>(a.KD, a.KC, a.n_tail);
-    auto kern = expand_dmma_kernel<T, STORE, FUNC>;
+    const size_t smem = TMEM ? sizeof(double) * (32 + sh.ns * stage_elems) : smem_bytes<T>(a.KD, a.KC, a.n_tail);
+    void (*kern)(ExpandArgs) = expand_dmma_kernel<T, STORE, FUNC>;
+    if constexpr (TMEM) {
+        const int code = 10 * sh.ns + sh.jps;
+        if (code == 31) kern = expand_tmem_kernel<STORE, FUNC, 3, 1>;
+        else if (code == 41) kern = expand_tmem_kernel<STORE, FUNC, 4, 1>;
+        else if (code == 51) kern = expand_tmem_kernel<STORE, FUNC, 5, 1>;
+        else if (code == 22) kern = expand_tmem_kernel<STORE, FUNC, 2, 2>;
+        else return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
+    }
     LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     int per_sm = 0;
     LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T::WARPS * 32, smem));
     if (per_sm < 1) return ls::fail(LS_EGUARD, "expand: tile does not fit on an SM");
+    // The occupancy query under-reports the tcgen05 kernel (1 instead of 2 CTAs/SM although
+    // registers, shared memory and the 2 x 256 TMEM columns all fit two); use the launch bound.
+    if (TMEM) per_sm = T::MINB;
     const int64_t grid = std::min<int64_t>(a.n_units, (int64_t)ls::sm_count() * per_sm);
+    if (std::getenv("LS_EXPAND_VERBOSE"))
+        std::fprintf(stderr, "ls_expand: tile %dx%d warps, IC %d, KC %d/%d, smem %zu B, %d CTA/SM, grid %lld, %s\n",
+                     T::WARPS, T::WI, T::IC, a.KC, a.KD, smem, per_sm, static_cast<long long>(grid),
+                     TMEM ? "A1k in TMEM" : "A1k in smem");
     if (grid > 0) {
         kern<<<(unsigned)grid, T::WARPS * 32, smem, s>>>(a);
         LS_LAUNCHED("expand_dmma_kernel");
@@ -547,6 +615,7 @@ template <bool STORE, bool FUNC>
 int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
     a.KC = std::min(pl.KC, a.KD);
     switch (pl.id) {
+        case kPlanTmem: return launch<TileWide, STORE, FUNC, true>(a, s);
         case 0: return launch<TileWide, STORE, FUNC>(a, s);
         case 1: return launch<TileWide3, STORE, FUNC>(a, s);
         case 2: return launch<TileMid, STORE, FUNC>(a, s);
@@ -567,7 +636,8 @@ extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_
     if (k1 < k0) return -1;
     if (!plan_for(KD, n_tail, pl) && !chunk_plan(pl)) return -1;
     const int64_t IC = pl.ic;
-    return ls::ceil_div(N1, IC) * (k1 - k0);
+    // the TMEM variant writes one partial per warp (no CTA barrier per unit)
+    return ls::ceil_div(N1, IC) * (k1 - k0) * (pl.id == kPlanTmem ? 8 : 1);
 }
 
 extern "C" int ls_expand(const double* A_d, int64_t lda, const double* B_d, int64_t ldb,

@@ -1,0 +1,364 @@
+// expand_tmem.cuh -- K3 variant with the scaled left factor A1k resident in tensor
+// memory (TMEM), double-buffered across work units. Included by expand.cu.
+//
+// The shared-memory variant (expand_dmma_kernel) must stop every warp of the CTA at each
+// unit boundary: one barrier before A1k of the next slab overwrites the current one, one
+// after the fill. Here A1k lives in TMEM (256 of 512 columns per CTA, otherwise unused by
+// an FP64 kernel): two buffers, so the warps fill unit u+1's A1k piece by piece while they
+// multiply unit u, and units hand over through mbarriers (as_full / as_empty) instead of
+// CTA barriers. Shared memory then holds only the TMA ring of A2 stages.
+//
+// TMEM layout (per CTA, lanes = warp quarter wi = warp & 3, i.e. the warps sharing i-tiles):
+//   buffer b, column b*CB + ks*8 + it*2 + {0,1}: A1k(8*(4*wi + it) + g, 4*ks + t) (lo, hi words)
+//   buffer b, column b*CB + 8*KD + qt*16 + n*4 + {0..3}: the two tail-rank values lane (g, t)
+//   needs for i-tile n: A1k(32*wi + 8n + 2t + {0,1}, 4*KD + qt)
+// CB = 8*KD + 16*n_tail columns, so KD <= 14 fits two buffers in 256 columns.
+#pragma once
+
+namespace tmem {
+
+// Issue a 32-lane x 8-column load (4 doubles per thread); the registers are valid after wait_ld().
+// No memory clobbers: ordinary shared-memory loads may be scheduled around these, while the
+// volatile asm statements (ld, wait, DMMA) keep their program order.
+__device__ __forceinline__ void ld_x8_issue(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void wait_ld(uint32_t (&r)[8]) {
+    // The register operands tie the wait to the loaded values, so no use is hoisted above it.
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]));
+}
+__device__ __forceinline__ void unpack(const uint32_t (&r)[8], double (&v)[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = __hiloint2double(static_cast<int>(r[2 * c + 1]), static_cast<int>(r[2 * c]));
+}
+__device__ __forceinline__ void ld_x8(uint32_t taddr, double (&v)[4]) {
+    uint32_t r[8];
+    ld_x8_issue(taddr, r);
+    wait_ld(r);
+    unpack(r, v);
+}
+
+__device__ __forceinline__ void st_x8(uint32_t taddr, const double (&v)[4]) {
+    uint32_t r[8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        r[2 * c] = static_cast<uint32_t>(__double2loint(v[c]));
+        r[2 * c + 1] = static_cast<uint32_t>(__double2hiint(v[c]));
+    }
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+}  // namespace tmem
+
+constexpr int kTmemCols = 256;  // per CTA; two CTAs per SM use all 512 columns
+
+// Requires: Tile geometry TileWide (8 warps, WI = 4, TM = TN = 4), whole rank in one stage
+// (n_kc == 1), KD <= 14, n_tail <= 1.
+// NS: ring depth; JPS: 64-column j-chunks per ring stage (each warp computes JPS tiles per stage).
+template <bool STORE, bool FUNC, int NS, int JPS>
+__global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p) {
+    constexpr int WARPS = 8, WI = 4, kTM = 4, kTN = 4, IC = 128, JT = 8 * JPS, JC = 64, kNS = NS;
+    constexpr int kThreads = WARPS * 32;
+    const int KD = p.KD, n_tail = p.n_tail;
+    const int CB = 8 * KD + 16 * n_tail;
+    const int frag_elems = JT * KD * 32;
+    const int stage_elems = frag_elems + JT * 8 * n_tail;
+    const int n_ichunks = static_cast<int>(p.n_ichunks);
+    const int n_units = static_cast<int>(p.n_units);
+    const int per_unit = static_cast<int>(p.n_jc);
+    const unsigned stage_bytes = static_cast<unsigned>(stage_elems * sizeof(double));
+
+    // Shared-memory header (256 bytes): 16 mbarrier slots, then the slot counters and the TMEM
+    // base address; the A2 ring follows.
+    static_assert(kNS + 4 <= 16 && kNS <= 12, "header holds up to 12 ring slots");
+    extern __shared__ __align__(128) double smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // [kNS] A2 stage landed
+    uint64_t* as_full = full + kNS;                            // [2] A1k buffer written by every warp
+    uint64_t* as_empty = as_full + 2;                          // [2] A1k buffer released by every warp
+    int* released = reinterpret_cast<int*>(smem + 16);         // [kNS] warps done with a ring slot
+    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 24);
+    double* ring = smem + 32;                                   // [kNS][stage_elems]
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2;
+    const int t = lane & 3;
+    const int wi = warp & 3;  // i-tiles, and the TMEM lane quarter this warp may access
+    const int wj = warp >> 2;
+
+    const int my_units = n_units > static_cast<int>(blockIdx.x)
+                             ? (n_units - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                             : 0;
+    const int n_stages = my_units * per_unit;
+
+    auto issue = [&](int st) {
+        const int c = st % per_unit;
+        const double* src = p.Bp + static_cast<int64_t>(c) * stage_elems;
+        uint64_t* bar = full + (st % kNS);
+        mbar_arrive_expect_tx(bar, stage_bytes);
+        tma_bulk_g2s(ring + (st % kNS) * stage_elems, src, stage_bytes, bar);
+    };
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_s)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kNS; ++b) {
+            mbar_init(full + b, 1);
+            released[b] = 0;
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(as_full + b, WARPS);
+            mbar_init(as_empty + b, WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const uint32_t tq = *tmem_base_s + (static_cast<uint32_t>(32 * wi) << 16);  // this warp's lane quarter
+
+    // Fill tasks of one unit for this warp: fragment k-steps ks = wj, wj+2, ... (4 values each),
+    // then (warp wj == 0 only) the tail ranks (8 values each).
+    const int n_frag_tasks = (KD - wj + 1) / 2;
+    const int n_tasks = n_frag_tasks + (wj == 0 ? n_tail : 0);
+    auto task_loads = [&](int u, int task, double (&av)[8], double& sv) {
+        const int ib = (u % n_ichunks) * IC;
+        const int64_t k = p.k0 + u / n_ichunks;
+        if (task < n_frag_tasks) {
+            const int ks = wj + 2 * task;
+            const int q = 4 * ks + t;
+            sv = q < p.R ? __ldg(p.S + k * p.R + q) : 0.0;
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+                const int i = ib + 8 * (4 * wi + it) + g;
+                av[it] = (i < p.N1 && q < p.R) ? __ldg(p.A + i + p.lda * q) : 0.0;
+            }
+        } else {
+            const int q = 4 * KD + (task - n_frag_tasks);
+            sv = __ldg(p.S + k * p.R + q);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int i = ib + 32 * wi + 8 * (e >> 1) + 2 * t + (e & 1);
+                av[e] = i < p.N1 ? __ldg(p.A + i + p.lda * q) : 0.0;
+            }
+        }
+    };
+    auto task_store = [&](int buf, int task, const double (&av)[8], double sv) {
+        const uint32_t col = static_cast<uint32_t>(buf * CB);
+        if (task < n_frag_tasks) {
+            const int ks = wj + 2 * task;
+            double v[4];
+#pragma unroll
+            for (int it = 0; it < 4; ++it) v[it] = rn_mul(av[it], sv);  // Eigen's A1 * scale.asDiagonal()
+            tmem::st_x8(tq + col + 8 * ks, v);
+        } else {
+            const int qt = task - n_frag_tasks;
+            double v0[4], v1[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                v0[e] = rn_mul(av[e], sv);
+                v1[e] = rn_mul(av[4 + e], sv);
+            }
+            tmem::st_x8(tq + col + 8 * KD + 16 * qt, v0);
+            tmem::st_x8(tq + col + 8 * KD + 16 * qt + 8, v1);
+        }
+    };
+    auto publish = [&](int buf) {
+        tmem::wait_st();
+        tmem::fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(as_full + buf);
+    };
+
+    // Prologue: the first unit's A1k (buffer 0), all tasks now.
+    if (my_units > 0) {
+        for (int task = 0; task < n_tasks; ++task) {
+            double av[8], sv;
+            task_loads(blockIdx.x, task, av, sv);
+            task_store(0, task, av, sv);
+        }
+        publish(0);
+    }
+    if (threadIdx.x == 0)
+        for (int st = 0; st < kNS && st < n_stages; ++st) issue(st);
+
+    double acc[kTM][kTN][2];
+    double fsum = 0.0;
+    int st = 0;
+    // fill schedule for the next unit: tasks spread over stages [first_fill, per_unit)
+    const int first_fill = per_unit > 2 ? 2 : 0;
+    for (int n = 0; n < my_units; ++n) {
+        const int unit = blockIdx.x + n * gridDim.x;
+        const int buf = n & 1;
+        const bool has_next = n + 1 < my_units;
+        const int ib = (unit % n_ichunks) * IC;
+        const int64_t kk = unit / n_ichunks;
+        mbar_wait(as_full + buf, static_cast<unsigned>((n >> 1) & 1));
+        tmem::fence_after();
+        const uint32_t tb = tq + static_cast<uint32_t>(buf * CB);
+        if (FUNC) fsum = 0.0;
+        int next_task = 0;
+
+        for (int jc = 0; jc < per_unit; ++jc, ++st) {
+            // Fill task(s) for the next unit: loads now, product + TMEM store after the DMMAs.
+            const int span = per_unit - first_fill;
+            int target = 0;
+            if (has_next && jc >= first_fill) target = min(n_tasks, ((jc - first_fill + 1) * n_tasks + span - 1) / span);
+            const bool fill_now = target > next_task;
+            if (fill_now && next_task == 0 && n >= 1)  // buffer buf^1 was read by unit n-1
+                mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1));
+
+            const int slot = st % kNS;
+            mbar_wait(full + slot, static_cast<unsigned>((st / kNS) & 1));
+            const double* stage = ring + slot * stage_elems;
+#pragma unroll 1
+            for (int h = 0; h < JPS; ++h) {
+                const int jt0 = h * 8 + wj * kTM;  // first j-tile of this warp's tile in the stage
+#pragma unroll
+                for (int m = 0; m < kTM; ++m)
+#pragma unroll
+                    for (int nn = 0; nn < kTN; ++nn) acc[m][nn][0] = acc[m][nn][1] = 0.0;
+                if (n_tail) {
+                    // Rank remainder (R mod 4 = 1) on DFMA before the DMMAs. (Placing it after the
+                    // DMMA loop, where it would overlap the accumulator drain, measured 12% slower:
+                    // it then lengthens the exposed drain before the epilogue.)
+                    const double* tbp = stage + frag_elems + jt0 * 8 + g;
+                    double bt[kTM];
+#pragma unroll
+                    for (int m = 0; m < kTM; ++m) bt[m] = tbp[m * 8];
+                    double at0[4], at1[4];
+                    tmem::ld_x8(tb + 8 * KD, at0);
+                    tmem::ld_x8(tb + 8 * KD + 8, at1);
+                    const double atx[8] = {at0[0], at0[1], at0[2], at0[3], at1[0], at1[1], at1[2], at1[3]};
+#pragma unroll
+                    for (int nn = 0; nn < kTN; ++nn)
+#pragma unroll
+                        for (int m = 0; m < kTM; ++m) {
+                            acc[m][nn][0] = fma(atx[2 * nn], bt[m], acc[m][nn][0]);
+                            acc[m][nn][1] = fma(atx[2 * nn + 1], bt[m], acc[m][nn][1]);
+                        }
+                }
+                {
+                    const double* bsw = stage + jt0 * (KD * 32) + lane;
+#pragma unroll 1
+                    for (int ks = 0; ks < KD; ++ks) {
+                        double a[kTM], b[kTN];
+                        uint32_t rb[8];
+                        tmem::ld_x8_issue(tb + 8 * ks, rb);
+#pragma unroll
+                        for (int m = 0; m < kTM; ++m) a[m] = bsw[m * (KD * 32) + ks * 32];
+                        tmem::wait_ld(rb);
+                        tmem::unpack(rb, b);
+#pragma unroll
+                        for (int m = 0; m < kTM; ++m)
+#pragma unroll
+                            for (int nn = 0; nn < kTN; ++nn) dmma_884(acc[m][nn][0], acc[m][nn][1], a[m], b[nn]);
+                    }
+                }
+                if (h == JPS - 1) {
+                    // Release the ring slot; the last warp refills it with stage st + kNS.
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence_block();
+                        if (atomicAdd(released + slot, 1) == WARPS - 1) {
+                            released[slot] = 0;
+                            __threadfence_block();
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            if (st + kNS < n_stages) issue(st + kNS);
+                        }
+                    }
+                    // This stage's fill task(s) for the next unit, after the DMMAs were issued (no fill
+                    // state stays live across the DMMA loop, which keeps its operand registers free).
+                    if (fill_now) {
+                        for (; next_task < target; ++next_task) {
+                            double fav[8], fsv;
+                            task_loads(unit + gridDim.x, next_task, fav, fsv);
+                            task_store(buf ^ 1, next_task, fav, fsv);
+                        }
+                        if (next_task == n_tasks) publish(buf ^ 1);
+                    }
+                }
+
+                // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
+                const int jb = (jc * JPS + h) * JC + wj * (8 * kTM);
+                const int ibase = ib + wi * (8 * kTN);
+#pragma unroll
+                for (int m = 0; m < kTM; ++m) {
+                    const int j = jb + 8 * m + g;
+                    if (j >= p.N2) continue;
+                    if (FUNC) {
+                        double sm = 0.0;
+#pragma unroll
+                        for (int nn = 0; nn < kTN; ++nn) {
+                            const int i = ibase + 8 * nn + 2 * t;
+                            if (i < p.N1) sm = fma(acc[m][nn][0], __ldg(p.rho1 + i), sm);
+                            if (i + 1 < p.N1) sm = fma(acc[m][nn][1], __ldg(p.rho1 + i + 1), sm);
+                        }
+                        fsum = fma(sm, __ldg(p.rho2 + j), fsum);
+                    }
+                    if (!STORE) continue;
+                    double* row = p.out + kk * p.ldz + static_cast<int64_t>(j) * p.ldy;
+#pragma unroll
+                    for (int nn = 0; nn < kTN; ++nn) {
+                        const int i = ibase + 8 * nn + 2 * t;
+                        if (i + 1 < p.N1) {
+                            if (p.accumulate) {
+                                row[i] += acc[m][nn][0];
+                                row[i + 1] += acc[m][nn][1];
+                            } else if (p.vec_store) {
+                                __stcs(reinterpret_cast<double2*>(row + i), make_double2(acc[m][nn][0], acc[m][nn][1]));
+                            } else {
+                                row[i] = acc[m][nn][0];
+                                row[i + 1] = acc[m][nn][1];
+                            }
+                        } else if (i < p.N1) {
+                            row[i] = p.accumulate ? row[i] + acc[m][nn][0] : acc[m][nn][0];
+                        }
+                    }
+                }
+            }
+        }
+        // This warp is done reading A1k buffer buf.
+        tmem::fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(as_empty + buf);
+        if (has_next && next_task < n_tasks) {  // tiny units: finish the fill now
+            if (next_task == 0 && n >= 1)
+                mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1));
+            for (; next_task < n_tasks; ++next_task) {
+                double av[8], sv;
+                task_loads(unit + gridDim.x, next_task, av, sv);
+                task_store(buf ^ 1, next_task, av, sv);
+            }
+            publish(buf ^ 1);
+        }
+        if (FUNC) {
+            // Per-warp partials (no CTA barrier): partial[unit * WARPS + warp], fixed-order xor tree.
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, off);
+            if (lane == 0) {
+                const double part = rn_mul(fsum, p.rho3[p.k0 + kk]);
+                double& slot = p.partial[static_cast<int64_t>(unit) * WARPS + warp];
+                slot = p.accumulate ? slot + part : part;
+            }
+        }
+    }
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_s), "r"(kTmemCols)
+                     : "memory");
+}
