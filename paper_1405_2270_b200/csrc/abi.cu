@@ -134,7 +134,8 @@ int expand_to_host(const double* A, const double* B, const double* C, const doub
     const int64_t slab = d[0] * d[1];
     if (k1 <= k0 || slab == 0) return LS_OK;
     const int64_t slab_bytes = slab * static_cast<int64_t>(sizeof(double));
-    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, (256ll << 20) / slab_bytes));
+    // ~1 GiB chunks: enough work units per launch to fill the GPU; two buffers in flight.
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, (1ll << 30) / slab_bytes));
     DevBuf buf[2];
     cudaEvent_t done_compute[2], done_copy[2];
     for (int b = 0; b < 2; ++b) {
