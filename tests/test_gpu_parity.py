@@ -387,3 +387,98 @@ def test_off_grid_charge_rejected(L):
     spec, rule = cfg(L, 2, n=8, b=2.0, charges=((0.1, 0, 0, 1.0),), M=8)
     with pytest.raises(L.ValidationError):
         L.lattice_potential(spec, rule)
+
+
+# ------------------------------------------------- size-independent properties at BASELINE sizes
+def _grid(L, spec, rule, mode="erf", k0=0, k1=None):
+    import torch
+    pipe = L.DevicePipeline(spec, rule, mode=mode)
+    N = pipe.dims
+    k1 = N[2] if k1 is None else k1
+    out = torch.empty((k1 - k0, N[1], N[0]), dtype=torch.float64, device="cuda")
+    pipe.step(out, k0, k1)
+    torch.cuda.synchronize()
+    return pipe, out
+
+
+def test_cfg1_charge_scaling_is_exact(L):
+    """Z enters only through the weights Z*w_q (lattice.hpp:284-287): doubling Z doubles every grid
+    value bit for bit over the full 1024^3 grid."""
+    import torch
+    spec1, rule = cfg(L, 16)
+    spec2, _ = cfg(L, 16, charges=((0.0, 0.0, 0.0, 2.0),))
+    _, v1 = _grid(L, spec1, rule)
+    _, v2 = _grid(L, spec2, rule)
+    assert torch.equal(v2, 2.0 * v1)
+
+
+def test_cfg1_superposition_of_charges(L):
+    """Linearity in the charges (test_lattice.cpp:157-172 at full size): the two-charge potential
+    equals the sum of the single-charge potentials to rounding."""
+    import torch
+    a = (0.0, 0.0, 0.0, 1.0)
+    b = (1.25, -2.5, 3.75, 3.0)
+    spec_ab, rule = cfg(L, 16, charges=(a, b))
+    spec_a, _ = cfg(L, 16, charges=(a,))
+    spec_b, _ = cfg(L, 16, charges=(b,))
+    _, vab = _grid(L, spec_ab, rule)
+    _, va = _grid(L, spec_a, rule)
+    va.add_(_grid(L, spec_b, rule)[1])
+    scale = float(vab.abs().max())
+    assert float((vab - va).abs().max()) <= 1e-13 * scale
+
+
+def test_cfg1_shards_and_determinism(L):
+    """z-slab shards reproduce the single-GPU grid bit for bit, and repeated runs are identical."""
+    import torch
+    spec, rule = cfg(L, 16)
+    pipe, full = _grid(L, spec, rule)
+    again = torch.empty_like(full)
+    pipe.step(again)
+    torch.cuda.synchronize()
+    assert torch.equal(full, again)
+    from paper_1405_2270_b200.distributed import slab_range
+    N3 = pipe.dims[2]
+    for world in (2, 3, 8):
+        for r in range(world):
+            k0, k1 = slab_range(N3, r, world)
+            part = torch.empty((k1 - k0, pipe.dims[1], pipe.dims[0]), dtype=torch.float64, device="cuda")
+            pipe.expand(part, k0, k1)
+            torch.cuda.synchronize()
+            assert torch.equal(part, full[k0:k1])
+    del again
+
+
+def test_cfg2_sharded_energy_matches_whole(L):
+    """The per-shard fused energies summed (what the NCCL all_reduce does) equal the single-pass
+    2048^3 energy to rounding, and both match the 1D rank-term form."""
+    import torch
+    spec, rule = cfg(L, 32)
+    pipe = L.DevicePipeline(spec, rule, mode="erf")
+    pipe.generate()
+    pipe.assemble()
+    N = pipe.dims
+    x = (np.arange(N[0]) + 0.5 - N[0] / 2) * spec.unit.h
+    r1 = torch.as_tensor(np.exp(-x * x / 8.0), device="cuda")  # sigma = 2 bohr
+    rho = [r1, r1, r1]
+    whole = float(pipe.grid_functional(rho)[0])
+    from paper_1405_2270_b200.distributed import slab_range
+    parts = [float(pipe.grid_functional(rho, *slab_range(N[2], r, 8))[0]) for r in range(8)]
+    assert abs(sum(parts) - whole) <= 1e-13 * abs(whole)
+    X = [r1.reshape(-1, 1)] * 3
+    one_d = float(L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w, X)[0])
+    assert abs(whole - one_d) <= 1e-12 * abs(one_d)
+
+
+def test_cfg4_periodic_translation_symmetry(L):
+    """A unit charge at the cell centre on a periodic lattice: the potential on the reference cell
+    is symmetric under i -> n-1-i on every axis (to rounding of the ascending-k sums)."""
+    import torch
+    spec, rule = cfg(L, 64, n=256)
+    pipe = L.DevicePipeline(spec, rule, mode="erf", periodic=True)
+    out = torch.empty((256, 256, 256), dtype=torch.float64, device="cuda")
+    pipe.step(out)
+    torch.cuda.synchronize()
+    scale = float(out.abs().max())
+    for d in range(3):
+        assert float((out - torch.flip(out, dims=[d])).abs().max()) <= 1e-13 * scale
