@@ -470,11 +470,13 @@ def test_cfg2_sharded_energy_matches_whole(L):
     assert abs(whole - one_d) <= 1e-12 * abs(one_d)
 
 
-def test_cfg4_periodic_translation_symmetry(L):
-    """A unit charge at the cell centre on a periodic lattice: the potential on the reference cell
-    is symmetric under i -> n-1-i on every axis (to rounding of the ascending-k sums)."""
+def test_cfg4_periodic_mirror_symmetry(L):
+    """A unit charge at the cell centre of a periodic block with odd L (reference cell (L-1)/2, so
+    the images sit symmetrically, lattice.hpp:100-106): the unit-cell potential at the cfg4 grid
+    (n = 256) is symmetric under i -> n-1-i on every axis, to rounding of the ascending-k sums.
+    (For the even-L BASELINE blocks the image set is one cell longer on one side.)"""
     import torch
-    spec, rule = cfg(L, 64, n=256)
+    spec, rule = cfg(L, 63, n=256)
     pipe = L.DevicePipeline(spec, rule, mode="erf", periodic=True)
     out = torch.empty((256, 256, 256), dtype=torch.float64, device="cuda")
     pipe.step(out)
