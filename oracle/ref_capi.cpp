@@ -305,4 +305,31 @@ int ref_save_bundle(const char* path, int64_t n1, int64_t n2, int64_t n3, int R,
     });
 }
 
+// calibrate_quadrature (newton.hpp:161-189) on GridSpec(b, n) with KernelTolerance(eps, a_min, a_max):
+// returns M (or -1 on failure) and the winning C0; the rule itself follows from sinc_quadrature.
+int ref_calibrate_quadrature(double b, int64_t n, double eps, double a_min, double a_max, int m_cap, double* C0,
+                             int* trace_len) {
+    int M = -1;
+    int rc = guarded([&] {
+        CalibrationTrace trace;
+        QuadratureRule r = calibrate_quadrature(GridSpec(b, n), KernelTolerance(eps, a_min, a_max), &trace, m_cap);
+        M = r.M;
+        *C0 = r.C0;
+        *trace_len = static_cast<int>(trace.entries.size());
+    });
+    return rc ? -rc : M;
+}
+
+// calibrate_for_lattice (lattice.hpp:118-126) for one unit charge at the cell centre.
+int ref_calibrate_for_lattice(const int64_t L[3], int64_t n, double b, double eps, double* C0) {
+    int M = -1;
+    int rc = guarded([&] {
+        const double ch[4] = {0.0, 0.0, 0.0, 1.0};
+        QuadratureRule r = calibrate_for_lattice(make_spec(L, n, b, ch, 1), eps);
+        M = r.M;
+        *C0 = r.C0;
+    });
+    return rc ? -rc : M;
+}
+
 }  // extern "C"

@@ -225,6 +225,82 @@ def build_newton_master(lens: Sequence[int], h: float, rule: QuadratureRule,
     return CanonicalTensor3(factors, rule.weights.copy())
 
 
+# ------------------------------------------------------- probes and calibration (newton.hpp)
+@dataclass(frozen=True)
+class KernelTolerance:
+    """grid.hpp:41-60."""
+    eps: float
+    a_min: float
+    a_max: float
+
+    def __post_init__(self):
+        if not (0.0 < self.eps < 1.0):
+            raise ValidationError(f"tolerance: eps must lie in (0, 1), got {self.eps}")
+        if not (0.0 < self.a_min < self.a_max):
+            raise ValidationError(f"tolerance: need 0 < a_min < a_max, got a_min = {self.a_min}, "
+                                  f"a_max = {self.a_max}")
+
+
+def default_tolerance(grid: GridSpec, eps: float) -> KernelTolerance:
+    """grid.hpp:62-64."""
+    return KernelTolerance(eps, grid.h, math.sqrt(3.0) * grid.b)
+
+
+def kernel_probe_set(grid: GridSpec, tol: KernelTolerance) -> np.ndarray:
+    """newton.hpp:97-132: (P, 4) array of (i, j, k, r) probes in ascending (i, j, k) order."""
+    n = grid.n
+    c, sh = n // 2, min(8, n // 2)
+    keys = set()
+    rng = range(c - sh, c + sh)
+    for i in rng:
+        for j in rng:
+            for k in rng:
+                keys.add((i * n + j) * n + k)
+    for i in range(n):
+        keys.update({(i * n + c) * n + c, (i * n + i) * n + c, (i * n + i) * n + i})
+    stride = max(1, n // 16)
+    for i in range(0, n, stride):
+        for j in range(0, n, stride):
+            for k in range(0, n, stride):
+                keys.add((i * n + j) * n + k)
+    key = np.array(sorted(keys), dtype=np.int64)
+    i, j, k = key // (n * n), (key // n) % n, key % n
+    mid = lambda a: (a.astype(np.float64) + 0.5 - n / 2.0) * grid.h  # noqa: E731
+    x, y, z = mid(i), mid(j), mid(k)
+    r = np.sqrt(x * x + y * y + z * z)
+    keep = (r >= tol.a_min) & (r <= tol.a_max)
+    return np.stack([i[keep], j[keep], k[keep], r[keep]], axis=1)
+
+
+def measure_probe_error(kernel: CanonicalTensor3, probes: np.ndarray) -> float:
+    """newton.hpp:136-144: max |T(p) r - 1| over the probes, all evaluated in one GPU batch."""
+    v = eval_points(kernel, probes[:, :3].astype(np.int64))
+    return float(np.max(np.abs(v * probes[:, 3] - 1.0))) if len(v) else 0.0
+
+
+def calibrate_quadrature(grid: GridSpec, tol: KernelTolerance, trace: list | None = None,
+                         m_cap: int = 128) -> QuadratureRule:
+    """newton.hpp:161-189: smallest M (best C0 in {1,2,3,4} at that M) meeting eps on the probes."""
+    probes = kernel_probe_set(grid, tol)
+    if len(probes) == 0:
+        raise ValidationError("calibrate_quadrature: no grid midpoints in [a_min, a_max]")
+    best_seen = math.inf
+    for M in range(2, m_cap + 1):
+        pick, pick_err = None, math.inf
+        for c0 in (1.0, 2.0, 3.0, 4.0):
+            rule = sinc_quadrature(tol.eps, tol.a_min, tol.a_max, M, c0)
+            err = measure_probe_error(build_newton_master([grid.n] * 3, grid.h, rule), probes)
+            if trace is not None:
+                trace.append((M, c0, err))
+            if err < pick_err:
+                pick, pick_err = rule, err
+        best_seen = min(best_seen, pick_err)
+        if pick_err <= tol.eps:
+            return pick
+    raise ResourceGuardError(f"calibrate_quadrature: no rule with M <= {m_cap} meets eps = {tol.eps}; "
+                             f"best achieved error {best_seen}")
+
+
 # ----------------------------------------------------------------- lattice.hpp
 @dataclass
 class Charge:
@@ -273,6 +349,14 @@ class LatticeSpec:
             raise ValidationError(f"lattice: charge {nu} coordinate {p} on axis {axis} does not lie on a grid "
                                   "point of the unit cell")
         return int(r)
+
+
+def calibrate_for_lattice(spec: "LatticeSpec", eps: float, trace: list | None = None) -> QuadratureRule:
+    """lattice.hpp:118-126: probes drawn from the doubled target extent."""
+    spec.validate()
+    Lm = max(spec.L)
+    grid = GridSpec(2.0 * Lm * spec.unit.b, 2 * Lm * spec.unit.n)
+    return calibrate_quadrature(grid, KernelTolerance(eps, spec.unit.h, math.sqrt(3.0) * Lm * spec.unit.b), trace)
 
 
 def window_start_box(N: int, n: int, i_a: int, k: int) -> int:

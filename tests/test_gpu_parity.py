@@ -484,3 +484,32 @@ def test_cfg4_periodic_mirror_symmetry(L):
     scale = float(out.abs().max())
     for d in range(3):
         assert float((out - torch.flip(out, dims=[d])).abs().max()) <= 1e-13 * scale
+
+
+def test_calibration_matches_reference(L, ref):
+    """calibrate_quadrature / calibrate_for_lattice (newton.hpp:161-189, lattice.hpp:118-126) with
+    every candidate's probes evaluated on the GPU pick the same (M, C0) as the reference."""
+    import ctypes as C
+    ref.lib.ref_calibrate_quadrature.restype = C.c_int
+    ref.lib.ref_calibrate_quadrature.argtypes = [C.c_double, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int,
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_int)]
+    for b, n, eps in ((2.0, 16, 1e-4), (2.0, 16, 1e-6), (2.0, 32, 1e-5)):
+        grid = L.GridSpec(b, n)
+        tol = L.default_tolerance(grid, eps)
+        trace = []
+        rule = L.calibrate_quadrature(grid, tol, trace)
+        c0 = C.c_double(0)
+        tl = C.c_int(0)
+        M = ref.lib.ref_calibrate_quadrature(b, n, eps, tol.a_min, tol.a_max, 128, C.byref(c0), C.byref(tl))
+        assert (rule.M, rule.C0) == (M, c0.value)
+        assert len(trace) == tl.value
+        assert L.measure_probe_error(L.build_newton_master([n] * 3, grid.h, rule), L.kernel_probe_set(grid, tol)) <= eps
+    ref.lib.ref_calibrate_for_lattice.restype = C.c_int
+    ref.lib.ref_calibrate_for_lattice.argtypes = [C.POINTER(C.c_int64), C.c_int64, C.c_double, C.c_double,
+                                                  C.POINTER(C.c_double)]
+    spec = L.LatticeSpec((4, 2, 1), L.GridSpec(2.0, 8), [L.Charge((0.0, 0.0, 0.0), 1.0)])
+    rule = L.calibrate_for_lattice(spec, 1e-4)
+    Lx = np.array(spec.L, dtype=np.int64)
+    c0 = C.c_double(0)
+    M = ref.lib.ref_calibrate_for_lattice(Lx.ctypes.data_as(C.POINTER(C.c_int64)), 8, 2.0, 1e-4, C.byref(c0))
+    assert (rule.M, rule.C0) == (M, c0.value)
