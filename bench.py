@@ -314,6 +314,14 @@ def run_other_configs(L, dev):
     t = _ev_ms(lambda: pipe.step(grid))
     out["cfg0"] = {"grid": list(pipe.dims), "rank": pipe.Rt, "step_ms": round(t, 4),
                    "gpts": round(float(np.prod(pipe.dims)) / (t * 1e-3) / 1e9, 2)}
+    # calibration of the cfg1 lattice (the reference CLI's dominant cost): GPU-evaluated probes
+    spec1 = L.LatticeSpec((16, 16, 16), L.GridSpec(B, n_CELL), [L.Charge((0.0, 0.0, 0.0), 1.0)])
+    L.calibrate_for_lattice(spec1, EPS)
+    t0 = time.perf_counter()
+    cal = L.calibrate_for_lattice(spec1, EPS)
+    out["calibration_cfg1"] = {"eps": EPS, "M": cal.M, "C0": cal.C0,
+                               "ms": round((time.perf_counter() - t0) * 1e3, 3),
+                               "note": "calibrate_for_lattice, host-timed; picks the BASELINE M=20"}
     del grid
     # cfg3: 8 atoms at seeded vertices in [0.1b, 0.9b]^3, Z in 1..8, L = 32
     rng = np.random.default_rng(20241019)

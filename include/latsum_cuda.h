@@ -126,6 +126,14 @@ int ls_functional_batch(const double* A_d, int64_t lda, const double* B_d, int64
                         int64_t ldy, const double* Z_d, int64_t ldz, int F, double scale,
                         double* out_d, void* stream);
 
+/* Probe error of the rank-R Newton-kernel tensor on a length-len midpoint
+ * grid (build_newton_tensor, newton.hpp:79-84) straight from the rule:
+ * out_d[0] = max_p |T(i_p, j_p, k_p) r_p - 1| (measure_probe_error,
+ * newton.hpp:136-144) without materializing the factors; bit-identical to
+ * eval_point on the generated master. idx_d holds P (i, j, k) triples. */
+int ls_probe_error(const double* tau_d, const double* w_d, int R, int64_t len, double h, const int64_t* idx_d,
+                   const double* r_d, int64_t P, double* out_d, void* stream);
+
 /* Streaming compare: for every block b of a launch of nblocks blocks,
  * part_d[2b] = max(part_d[2b], max|a - b|) and part_d[2b+1] = max(.., max|b|)
  * over n entries (max_norm_diff_canonical's per-slab reduction,
@@ -165,6 +173,15 @@ int ls_synchronize(void* stream);
 
 /* ---- host-level entry points (drop-in headers, e2e path) ----------------
  * Synchronous; all pointers host memory; results copied back. */
+/* calibrate_quadrature(GridSpec(b, n), KernelTolerance(eps, a_min, a_max),
+ * trace, m_cap) (newton.hpp:161-189): smallest M, best C0 in {1,2,3,4}, whose
+ * kernel meets eps on the probe set (newton.hpp:97-132); all probes of a
+ * candidate evaluated by ls_probe_error. The trace arrays (capacity
+ * trace_cap; may be NULL with trace_len NULL) receive every candidate.
+ * No rule within m_cap -> LS_EGUARD (resource_guard_error). */
+int ls_h_calibrate_quadrature(double b, int64_t n, double eps, double a_min, double a_max, int m_cap, int* M_out,
+                              double* C0_out, int* trace_len, int* trace_M, double* trace_C0, double* trace_err,
+                              int trace_cap);
 /* build_newton_master(lens, h, rule) (newton.hpp:57-75) in either generator
  * mode: f_h[l] is lens[l] x R column-major; equal-length axes share data. */
 int ls_h_newton_master(int mode, const int64_t lens[3], double h, const double* tau_h, int R, double* f0_h,

@@ -238,6 +238,101 @@ int ls_sinc_quadrature(double eps, double a_min, double a_max, int M, double C0,
     return LS_OK;
 }
 
+// calibrate_quadrature (newton.hpp:161-189) with every candidate's probes evaluated on the GPU
+// by the fused probe_error kernel: the probe set (newton.hpp:97-132) is built once on the host
+// and uploaded once; per candidate only tau/w go up and one double comes back.
+int ls_h_calibrate_quadrature(double b, int64_t n, double eps, double a_min, double a_max, int m_cap, int* M_out,
+                              double* C0_out, int* trace_len, int* trace_M, double* trace_C0, double* trace_err,
+                              int trace_cap) {
+    if (!(b > 0.0) || !std::isfinite(b) || n < 2 || n % 2 != 0)
+        return ls::fail(LS_EVALIDATION, "grid: need b > 0 and even n >= 2");
+    if (!(eps > 0.0 && eps < 1.0)) return ls::fail(LS_EVALIDATION, "tolerance: eps must lie in (0, 1)");
+    if (!(a_min > 0.0 && a_min < a_max)) return ls::fail(LS_EVALIDATION, "tolerance: need 0 < a_min < a_max");
+    const double h = b / static_cast<double>(n);
+    // probe set: shell around the centre, three rays, strided lattice; sorted unique, in band
+    std::vector<int64_t> keys;
+    auto add = [&](int64_t i, int64_t j, int64_t k) {
+        if (i >= 0 && i < n && j >= 0 && j < n && k >= 0 && k < n) keys.push_back((i * n + j) * n + k);
+    };
+    const int64_t c = n / 2, sh = std::min<int64_t>(8, n / 2);
+    for (int64_t i = c - sh; i < c + sh; ++i)
+        for (int64_t j = c - sh; j < c + sh; ++j)
+            for (int64_t k = c - sh; k < c + sh; ++k) add(i, j, k);
+    for (int64_t i = 0; i < n; ++i) {
+        add(i, c, c);
+        add(i, i, c);
+        add(i, i, i);
+    }
+    const int64_t stride = std::max<int64_t>(1, n / 16);
+    for (int64_t i = 0; i < n; i += stride)
+        for (int64_t j = 0; j < n; j += stride)
+            for (int64_t k = 0; k < n; k += stride) add(i, j, k);
+    std::sort(keys.begin(), keys.end());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    std::vector<int64_t> idx;
+    std::vector<double> rad;
+    for (int64_t key : keys) {
+        const int64_t i = key / (n * n), j = (key / n) % n, k = key % n;
+        auto mid = [&](int64_t a) { return (static_cast<double>(a) + 0.5 - static_cast<double>(n) / 2.0) * h; };
+        const double x = mid(i), y = mid(j), z = mid(k);
+        const double r = std::sqrt(x * x + y * y + z * z);
+        if (r >= a_min && r <= a_max) {
+            idx.insert(idx.end(), {i, j, k});
+            rad.push_back(r);
+        }
+    }
+    if (rad.empty()) return ls::fail(LS_EVALIDATION, "calibrate_quadrature: no grid midpoints in [a_min, a_max]");
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    const cudaStream_t s = st->compute;
+    const int64_t P = static_cast<int64_t>(rad.size());
+    const int maxR = 2 * m_cap + 1;
+    DevBuf didx, drad, dtau, dw, derr;
+    LS_TRY(ls::upload(didx, idx.data(), sizeof(int64_t) * idx.size(), s));
+    LS_TRY(ls::upload(drad, rad.data(), sizeof(double) * rad.size(), s));
+    LS_TRY(dtau.alloc(sizeof(double) * maxR, s));
+    LS_TRY(dw.alloc(sizeof(double) * maxR, s));
+    LS_TRY(derr.alloc(sizeof(double) * 4, s));
+    std::vector<double> tau(maxR), w(maxR), nodes(maxR);
+    const double depths[4] = {1.0, 2.0, 3.0, 4.0};
+    int n_trace = 0;
+    double best_seen = INFINITY;
+    for (int M = 2; M <= m_cap; ++M) {
+        const int R = 2 * M + 1;
+        double errs[4];
+        for (int d = 0; d < 4; ++d) {
+            double step = 0.0;
+            LS_TRY(ls_sinc_quadrature(eps, a_min, a_max, M, depths[d], nodes.data(), tau.data(), w.data(), &step));
+            LS_CUDA(cudaMemcpyAsync(dtau.p, tau.data(), sizeof(double) * R, cudaMemcpyHostToDevice, s));
+            LS_CUDA(cudaMemcpyAsync(dw.p, w.data(), sizeof(double) * R, cudaMemcpyHostToDevice, s));
+            LS_TRY(ls_probe_error(dtau.d(), dw.d(), R, n, h, didx.i(), drad.d(), P, derr.d() + d, s));
+        }
+        LS_CUDA(cudaMemcpyAsync(errs, derr.p, sizeof(errs), cudaMemcpyDeviceToHost, s));
+        LS_CUDA(cudaStreamSynchronize(s));
+        int pick = 0;
+        for (int d = 0; d < 4; ++d) {
+            if (trace_len && n_trace < trace_cap) {
+                trace_M[n_trace] = M;
+                trace_C0[n_trace] = depths[d];
+                trace_err[n_trace] = errs[d];
+            }
+            ++n_trace;
+            if (errs[d] < errs[pick]) pick = d;
+        }
+        best_seen = std::min(best_seen, errs[pick]);
+        if (errs[pick] <= eps) {
+            *M_out = M;
+            *C0_out = depths[pick];
+            if (trace_len) *trace_len = n_trace;
+            return LS_OK;
+        }
+    }
+    if (trace_len) *trace_len = n_trace;
+    return ls::fail(LS_EGUARD, "calibrate_quadrature: no rule with M <= " + std::to_string(m_cap) +
+                                   " meets eps = " + std::to_string(eps) + "; best achieved error " +
+                                   std::to_string(best_seen));
+}
+
 int ls_h_gen_column(int mode, double t, int64_t len, double h, double* out_h) {
     if (!(t >= 0.0) || !std::isfinite(t))
         return ls::fail(LS_EVALIDATION, "generator: t must be finite and >= 0");

@@ -126,7 +126,50 @@ __global__ void maxdiff_kernel(const double* __restrict__ a, const double* __res
     }
 }
 
+// Probe error of the rank-R Newton-kernel tensor straight from the rule (newton.hpp:136-144 on
+// build_newton_tensor, newton.hpp:79-84): each probe's three factor entries are generated with
+// the midpoint formula of gen_midpoint_kernel (bit-identical to the materialized master) and
+// combined in eval_point's rank order; max |v r - 1| via an atomic max on the bit pattern
+// (non-negative doubles order like their bits, and max is exact).
+__global__ void probe_error_kernel(const double* __restrict__ tau, const double* __restrict__ w, int R,
+                                   int64_t len, double h, const int64_t* __restrict__ idx,
+                                   const double* __restrict__ r, int64_t P,
+                                   unsigned long long* __restrict__ out_bits) {
+    const double half_len = static_cast<double>(len) / 2.0;
+    double worst = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+        const double mi = rn_mul(rn_sub(rn_add(static_cast<double>(idx[3 * p]), 0.5), half_len), h);
+        const double mj = rn_mul(rn_sub(rn_add(static_cast<double>(idx[3 * p + 1]), 0.5), half_len), h);
+        const double mk = rn_mul(rn_sub(rn_add(static_cast<double>(idx[3 * p + 2]), 0.5), half_len), h);
+        double sum = 0.0;
+        for (int q = 0; q < R; ++q) {
+            const double t = tau[q];
+            const double xi = rn_mul(t, mi), xj = rn_mul(t, mj), xk = rn_mul(t, mk);
+            const double fi = exp(-rn_mul(xi, xi)), fj = exp(-rn_mul(xj, xj)), fk = exp(-rn_mul(xk, xk));
+            sum = rn_add(sum, rn_mul(rn_mul(rn_mul(w[q], fi), fj), fk));
+        }
+        worst = fmax(worst, fabs(rn_sub(rn_mul(sum, r[p]), 1.0)));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out_bits, static_cast<unsigned long long>(__double_as_longlong(worst)));
+}
+
 }  // namespace
+
+extern "C" int ls_probe_error(const double* tau_d, const double* w_d, int R, int64_t len, double h,
+                              const int64_t* idx_d, const double* r_d, int64_t P, double* out_d, void* stream) {
+    if (R < 0 || P < 0 || len < 2 || len % 2 != 0 || !(h > 0.0))
+        return ls::fail(LS_EVALIDATION, "probe_error: bad arguments");
+    const cudaStream_t s = ls::as_stream(stream);
+    LS_CUDA(cudaMemsetAsync(out_d, 0, sizeof(double), s));
+    if (P == 0) return LS_OK;
+    const int64_t blocks = std::min<int64_t>(ls::ceil_div(P, 256), 4 * ls::sm_count());
+    probe_error_kernel<<<(unsigned)blocks, 256, 0, s>>>(tau_d, w_d, R, len, h, idx_d, r_d, P,
+                                                         reinterpret_cast<unsigned long long*>(out_d));
+    LS_LAUNCHED("probe_error_kernel");
+    return LS_OK;
+}
 
 extern "C" int ls_maxdiff_accumulate(const double* a_d, const double* b_d, int64_t n, double* part_d, int nblocks,
                                      void* stream) {

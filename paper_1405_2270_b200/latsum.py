@@ -280,25 +280,20 @@ def measure_probe_error(kernel: CanonicalTensor3, probes: np.ndarray) -> float:
 
 def calibrate_quadrature(grid: GridSpec, tol: KernelTolerance, trace: list | None = None,
                          m_cap: int = 128) -> QuadratureRule:
-    """newton.hpp:161-189: smallest M (best C0 in {1,2,3,4} at that M) meeting eps on the probes."""
-    probes = kernel_probe_set(grid, tol)
-    if len(probes) == 0:
-        raise ValidationError("calibrate_quadrature: no grid midpoints in [a_min, a_max]")
-    best_seen = math.inf
-    for M in range(2, m_cap + 1):
-        pick, pick_err = None, math.inf
-        for c0 in (1.0, 2.0, 3.0, 4.0):
-            rule = sinc_quadrature(tol.eps, tol.a_min, tol.a_max, M, c0)
-            err = measure_probe_error(build_newton_master([grid.n] * 3, grid.h, rule), probes)
-            if trace is not None:
-                trace.append((M, c0, err))
-            if err < pick_err:
-                pick, pick_err = rule, err
-        best_seen = min(best_seen, pick_err)
-        if pick_err <= tol.eps:
-            return pick
-    raise ResourceGuardError(f"calibrate_quadrature: no rule with M <= {m_cap} meets eps = {tol.eps}; "
-                             f"best achieved error {best_seen}")
+    """newton.hpp:161-189: smallest M (best C0 in {1,2,3,4} at that M) meeting eps on the probes;
+    the whole scan runs natively (ls_h_calibrate_quadrature) with every candidate's probes
+    evaluated by one fused GPU kernel."""
+    cap = 4 * max(m_cap, 2)
+    tM = np.zeros(cap, dtype=np.int32)
+    tC = np.zeros(cap)
+    tE = np.zeros(cap)
+    M, C0, n_tr = C.c_int(0), C.c_double(0.0), C.c_int(0)
+    rc = _abi.load().ls_h_calibrate_quadrature(grid.b, grid.n, tol.eps, tol.a_min, tol.a_max, m_cap, C.byref(M),
+                                               C.byref(C0), C.byref(n_tr), _p(tM), _p(tC), _p(tE), cap)
+    if trace is not None:
+        trace.extend((int(tM[e]), float(tC[e]), float(tE[e])) for e in range(min(n_tr.value, cap)))
+    _abi.check(rc, "calibrate_quadrature")
+    return sinc_quadrature(tol.eps, tol.a_min, tol.a_max, M.value, C0.value)
 
 
 # ----------------------------------------------------------------- lattice.hpp
