@@ -498,7 +498,7 @@ bool fits_tmem(int KD, int n_tail) {
     const TmemShape sh = tmem_shape();
     const size_t jt = static_cast<size_t>(TileWide::JT) * sh.jps;
     const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
-    return 2 * (sizeof(double) * (32 + sh.ns * stage) + 1024) <= kSmemPerSM;
+    return 2 * (sizeof(double) * (32 + kTmemStgElems + sh.ns * stage) + 1024) <= kSmemPerSM;
 }
 
 template <class T>
@@ -572,7 +572,8 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     if (a.n_units * a.n_jc * a.n_kc >= (int64_t(1) << 31) || a.N1 + T::IC >= (int64_t(1) << 31) ||
         a.N2 + JC >= (int64_t(1) << 31))
         return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
-    const size_t smem = TMEM ? sizeof(double) * (32 + sh.ns * stage_elems) : smem_bytes<T>(a.KD, a.KC, a.n_tail);
+    const size_t smem =
+        TMEM ? sizeof(double) * (32 + kTmemStgElems + sh.ns * stage_elems) : smem_bytes<T>(a.KD, a.KC, a.n_tail);
     void (*kern)(ExpandArgs) = expand_dmma_kernel<T, STORE, FUNC>;
     if constexpr (TMEM) {
         const int code = 10 * sh.ns + sh.jps;

@@ -6,7 +6,8 @@
 // after the fill. Here A1k lives in TMEM (256 of 512 columns per CTA, otherwise unused by
 // an FP64 kernel): two buffers, so the warps fill unit u+1's A1k piece by piece while they
 // multiply unit u, and units hand over through mbarriers (as_full / as_empty) instead of
-// CTA barriers. Shared memory then holds only the TMA ring of A2 stages.
+// CTA barriers. Shared memory then holds the TMA ring of A2 stages and a small per-warp
+// staging area through which the next fill task's A1/S operands arrive by cp.async.
 //
 // TMEM layout (per CTA, lanes = warp quarter wi = warp & 3, i.e. the warps sharing i-tiles):
 //   buffer b, column b*CB + ks*8 + it*2 + {0,1}: A1k(8*(4*wi + it) + g, 4*ks + t) (lo, hi words)
@@ -60,6 +61,16 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 }  // namespace tmem
 
 constexpr int kTmemCols = 256;  // per CTA; two CTAs per SM use all 512 columns
+constexpr int kFillSlots = 9;   // per lane: up to 8 A1 values + the slab scale of one fill task
+constexpr int kTmemStgElems = 8 * kFillSlots * 32;  // per CTA (8 warps)
+
+// 8-byte global->shared copy (LDGSTS); src_size 0 writes zeros without reading.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Requires: Tile geometry TileWide (8 warps, WI = 4, TM = TN = 4), whole rank in one stage
 // (n_kc == 1), KD <= 14, n_tail <= 1.
@@ -86,7 +97,7 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
     uint64_t* as_empty = as_full + 2;                          // [2] A1k buffer released by every warp
     int* released = reinterpret_cast<int*>(smem + 16);         // [kNS] warps done with a ring slot
     uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 24);
-    double* ring = smem + 32;                                   // [kNS][stage_elems]
+    double* ring = smem + 32 + kTmemStgElems;                   // [kNS][stage_elems]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -129,52 +140,66 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
     __syncthreads();
     tmem::fence_after();
     const uint32_t tq = *tmem_base_s + (static_cast<uint32_t>(32 * wi) << 16);  // this warp's lane quarter
+    double* stg = smem + 32 + warp * (kFillSlots * 32) + lane;  // this lane's fill staging slots (stride 32)
 
     // Fill tasks of one unit for this warp: fragment k-steps ks = wj, wj+2, ... (4 values each),
     // then (warp wj == 0 only) the tail ranks (8 values each).
     const int n_frag_tasks = (KD - wj + 1) / 2;
     const int n_tasks = n_frag_tasks + (wj == 0 ? n_tail : 0);
-    auto task_loads = [&](int u, int task, double (&av)[8], double& sv) {
+    // A fill task's operands are copied global->shared asynchronously one task ahead (the copy
+    // for the following task is issued right after a task is consumed), so the L2 latency of the
+    // A1/S reads is off the warp's critical path.
+    auto task_issue = [&](int u, int task) {
         const int ib = (u % n_ichunks) * IC;
         const int64_t k = p.k0 + u / n_ichunks;
         if (task < n_frag_tasks) {
             const int ks = wj + 2 * task;
             const int q = 4 * ks + t;
-            sv = q < p.R ? __ldg(p.S + k * p.R + q) : 0.0;
+            cp_async8(stg + 8 * 32, p.S + k * p.R + (q < p.R ? q : 0), q < p.R);
 #pragma unroll
             for (int it = 0; it < 4; ++it) {
                 const int i = ib + 8 * (4 * wi + it) + g;
-                av[it] = (i < p.N1 && q < p.R) ? __ldg(p.A + i + p.lda * q) : 0.0;
+                const bool ok = i < p.N1 && q < p.R;
+                cp_async8(stg + it * 32, ok ? p.A + i + p.lda * q : p.A, ok);
             }
         } else {
             const int q = 4 * KD + (task - n_frag_tasks);
-            sv = __ldg(p.S + k * p.R + q);
+            cp_async8(stg + 8 * 32, p.S + k * p.R + q, true);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const int i = ib + 32 * wi + 8 * (e >> 1) + 2 * t + (e & 1);
-                av[e] = i < p.N1 ? __ldg(p.A + i + p.lda * q) : 0.0;
+                cp_async8(stg + e * 32, i < p.N1 ? p.A + i + p.lda * q : p.A, i < p.N1);
             }
         }
+        cp_async_commit();
     };
-    auto task_store = [&](int buf, int task, const double (&av)[8], double sv) {
+    auto task_consume = [&](int buf, int task) {
+        cp_async_wait_all();
+        const double sv = stg[8 * 32];
         const uint32_t col = static_cast<uint32_t>(buf * CB);
         if (task < n_frag_tasks) {
             const int ks = wj + 2 * task;
             double v[4];
 #pragma unroll
-            for (int it = 0; it < 4; ++it) v[it] = rn_mul(av[it], sv);  // Eigen's A1 * scale.asDiagonal()
+            for (int it = 0; it < 4; ++it) v[it] = rn_mul(stg[it * 32], sv);  // Eigen's A1 * scale.asDiagonal()
             tmem::st_x8(tq + col + 8 * ks, v);
         } else {
             const int qt = task - n_frag_tasks;
             double v0[4], v1[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                v0[e] = rn_mul(av[e], sv);
-                v1[e] = rn_mul(av[4 + e], sv);
+                v0[e] = rn_mul(stg[e * 32], sv);
+                v1[e] = rn_mul(stg[(4 + e) * 32], sv);
             }
             tmem::st_x8(tq + col + 8 * KD + 16 * qt, v0);
             tmem::st_x8(tq + col + 8 * KD + 16 * qt + 8, v1);
         }
+    };
+    // Consume task `task` of unit u into buffer buf, then start the copy for the task after it.
+    auto run_task = [&](int u, int task, int buf) {
+        task_consume(buf, task);
+        if (task + 1 < n_tasks) task_issue(u, task + 1);
+        else if (u + static_cast<int>(gridDim.x) < n_units) task_issue(u + gridDim.x, 0);
     };
     auto publish = [&](int buf) {
         tmem::wait_st();
@@ -185,11 +210,8 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
 
     // Prologue: the first unit's A1k (buffer 0), all tasks now.
     if (my_units > 0) {
-        for (int task = 0; task < n_tasks; ++task) {
-            double av[8], sv;
-            task_loads(blockIdx.x, task, av, sv);
-            task_store(0, task, av, sv);
-        }
+        task_issue(blockIdx.x, 0);
+        for (int task = 0; task < n_tasks; ++task) run_task(blockIdx.x, task, 0);
         publish(0);
     }
     if (threadIdx.x == 0)
@@ -198,8 +220,12 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
     double acc[kTM][kTN][2];
     double fsum = 0.0;
     int st = 0;
-    // fill schedule for the next unit: tasks spread over stages [first_fill, per_unit)
+    // Fill schedule for the next unit: tasks spread evenly over stages [first_fill, per_unit),
+    // offset by warp so the warps of an SM sub-partition do not fill in the same stage.
+    // (Finishing the fill earlier in the unit measured no faster.)
     const int first_fill = per_unit > 2 ? 2 : 0;
+    const int fill_w = per_unit - first_fill;
+    auto fill_stage = [&](int task) { return first_fill + ((task * WARPS + warp) * fill_w) / (WARPS * n_tasks); };
     for (int n = 0; n < my_units; ++n) {
         const int unit = blockIdx.x + n * gridDim.x;
         const int buf = n & 1;
@@ -214,9 +240,9 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
 
         for (int jc = 0; jc < per_unit; ++jc, ++st) {
             // Fill task(s) for the next unit: loads now, product + TMEM store after the DMMAs.
-            const int span = per_unit - first_fill;
-            int target = 0;
-            if (has_next && jc >= first_fill) target = min(n_tasks, ((jc - first_fill + 1) * n_tasks + span - 1) / span);
+            int target = next_task;
+            if (has_next)
+                while (target < n_tasks && fill_stage(target) <= jc) ++target;
             const bool fill_now = target > next_task;
             if (fill_now && next_task == 0 && n >= 1)  // buffer buf^1 was read by unit n-1
                 mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1));
@@ -283,11 +309,7 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
                     // This stage's fill task(s) for the next unit, after the DMMAs were issued (no fill
                     // state stays live across the DMMA loop, which keeps its operand registers free).
                     if (fill_now) {
-                        for (; next_task < target; ++next_task) {
-                            double fav[8], fsv;
-                            task_loads(unit + gridDim.x, next_task, fav, fsv);
-                            task_store(buf ^ 1, next_task, fav, fsv);
-                        }
+                        for (; next_task < target; ++next_task) run_task(unit + gridDim.x, next_task, buf ^ 1);
                         if (next_task == n_tasks) publish(buf ^ 1);
                     }
                 }
@@ -338,11 +360,7 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
         if (has_next && next_task < n_tasks) {  // tiny units: finish the fill now
             if (next_task == 0 && n >= 1)
                 mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1));
-            for (; next_task < n_tasks; ++next_task) {
-                double av[8], sv;
-                task_loads(unit + gridDim.x, next_task, av, sv);
-                task_store(buf ^ 1, next_task, av, sv);
-            }
+            for (; next_task < n_tasks; ++next_task) run_task(unit + gridDim.x, next_task, buf ^ 1);
             publish(buf ^ 1);
         }
         if (FUNC) {
