@@ -255,19 +255,22 @@ def run_ours(args, rank, world, local_rank):
 
     # Energy functional <V, rho> (BASELINE cfg2): fused expansion-reduction over this rank's slabs
     # + one scalar all_reduce, checked against the 1D rank-term form.
-    energy = run_energy(L, shard, spec, world, dev)
+    energy = e2e = None
+    if not args.step_only:
+        energy = run_energy(L, shard, spec, world, dev)
     del out
     torch.cuda.empty_cache()
 
     # e2e through the host-level C-ABI call: host rule/charges in, pinned host grid out.
-    e2e = run_e2e(L, spec, rule, k0, k1, args, world, dev)
+    if not args.step_only:
+        e2e = run_e2e(L, spec, rule, k0, k1, args, world, dev)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.step_only):
         cpu = cpu_baseline(spec, rule, budget_s=args.cpu_seconds)
 
     configs = None
-    if rank == 0 and world == 1 and not args.no_configs:
+    if rank == 0 and world == 1 and not (args.no_configs or args.step_only):
         configs = run_other_configs(L, dev)
 
     if rank == 0:
@@ -516,6 +519,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the cfg0/cfg3/cfg4 side measurements")
+    ap.add_argument("--step-only", action="store_true",
+                    help="only the timed step (for ncu launch lists): no energy, e2e, CPU baseline or configs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
