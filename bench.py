@@ -361,10 +361,15 @@ def run_other_configs(L, dev):
     G = [torch.as_tensor(np.exp(-(mids[:, None] - centres[None, :, l]) ** 2 / (2 * sigma ** 2)), device=dev)
          for l in range(3)]
     t_f = _ev_ms(lambda: L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w, G))
+    # full-grid form: expansion + fused DMMA GEMM (2 * 256^3 * 1024 FLOP) + fixed-order reduction
+    t_fg = _ev_ms(lambda: pipe.grid_functional_batch(G))
+    fg_flop = 2.0 * float(np.prod(pipe.dims)) * F
     out["cfg4_L256"] = {"grid": list(pipe.dims), "rank": pipe.Rt, "master_len": 2 * 256 * 256,
                         "generator_plus_assembly_ms": round(t_asm, 4), "expand_ms": round(t_exp, 4),
                         "expand_gpts": round(float(np.prod(pipe.dims)) / (t_exp * 1e-3) / 1e9, 1),
-                        "functionals_1024_ms": round(t_f, 4)}
+                        "functionals_1024_ms": round(t_f, 4),
+                        "functionals_1024_full_grid_ms": round(t_fg, 4),
+                        "functionals_1024_full_grid_tflops": round(fg_flop / (t_fg * 1e-3) / 1e12, 2)}
     del grid
     torch.cuda.empty_cache()
     return out

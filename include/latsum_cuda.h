@@ -126,6 +126,20 @@ int ls_functional_batch(const double* A_d, int64_t lda, const double* B_d, int64
                         int64_t ldy, const double* Z_d, int64_t ldz, int F, double scale,
                         double* out_d, void* stream);
 
+/* Full-grid form of a functional batch: for F
+ * separable densities rho_f = X(:,f) (x) Y(:,f) (x) Z(:,f) and a dense device
+ * grid V (i fastest; element (i,j,k) at V_d[i + ldy*j + ldz*k]),
+ *     out_d[f] (+)= scale * sum_{i,j,k} V(i,j,k) X(i,f) Y(j,f) Z(k,f).
+ * X, Y, Z are column-major (N1/N2/N3 x F). One fused FP64-DMMA GEMM over
+ * rows (j,k) with the Y*Z weighting and the row reduction in its epilogue, then
+ * a fixed-order sum over row tiles: bitwise reproducible. accumulate != 0 adds
+ * into out_d (slab-chunked grids: pass Z_d offset to the chunk's first slab).
+ * The reference has only the 1D form (scalar_product, canonical.hpp:126-136),
+ * which it matches to rounding. */
+int ls_grid_functional_batch(const double* V_d, int64_t N1, int64_t N2, int64_t N3, int64_t ldy, int64_t ldz,
+                             const double* X_d, int64_t ldx, const double* Y_d, int64_t ldyy, const double* Z_d,
+                             int64_t ldzz, int F, double scale, int accumulate, double* out_d, void* stream);
+
 /* Probe error of the rank-R Newton-kernel tensor on a length-len midpoint
  * grid (build_newton_tensor, newton.hpp:79-84) straight from the rule:
  * out_d[0] = max_p |T(i_p, j_p, k_p) r_p - 1| (measure_probe_error,

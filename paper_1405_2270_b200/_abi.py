@@ -52,6 +52,8 @@ SIGNATURES = {
     "ls_functional_batch": (_i, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i, _i64, _i64, _i64, _vp, _i64, _vp, _i64,
                                  _vp, _i64, _i, _d, _vp, _vp]),
     "ls_maxdiff_accumulate": (_i, [_vp, _vp, _i64, _vp, _i, _vp]),
+    "ls_grid_functional_batch": (_i, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i, _d,
+                                      _i, _vp, _vp]),
     "ls_probe_error": (_i, [_vp, _vp, _i, _i64, _d, _vp, _vp, _i64, _vp, _vp]),
     "ls_h_calibrate_quadrature": (_i, [_d, _i64, _d, _d, _d, _i, C.POINTER(_i), C.POINTER(_d), C.POINTER(_i), _vp, _vp,
                                        _vp, _i]),

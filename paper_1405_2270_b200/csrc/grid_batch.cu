@@ -1,0 +1,215 @@
+// grid_batch.cu -- K4b: a batch of F separable functionals of a dense device grid,
+//
+//   out[f] (+)= scale * sum_{i,j,k} V(i,j,k) * X(i,f) * Y(j,f) * Z(k,f),
+//
+// the full-grid form of SURVEY a18 for cfg4's batch of 1024 test functions (the 1D rank-term
+// form is ls_functional_batch; the reference has only that form, scalar_product at
+// canonical.hpp:126-136, which is the parity oracle for this kernel).
+//
+// It is a GEMM with a fused reduction epilogue. Rows m = j + N2*k of V^T (K = N1 along i)
+// times X (K x F):
+//   C[m, f] = sum_i V(i, m) X(i, f)            FP64 DMMA m8n8k4, 128 x 64 CTA tiles, K by 16
+//   part[m_tile, f] = sum_{m in tile} C[m, f] * (Y(j,f) * Z(k,f))    fixed-order epilogue
+// then out[f] = scale * sum over m-tiles in ascending order (grid_batch_reduce_kernel), so the
+// result is bitwise reproducible. Operands stream global -> shared with cp.async (3 stages);
+// the f-tiles of one m-tile are adjacent in the launch order, so V is read from HBM once and
+// re-read from L2. 2 * N1 * N2 * N3 * F FLOP; at cfg4 (256^3, F = 1024) 3.4e10.
+#include "common.cuh"
+
+namespace {
+
+constexpr int BM = 128, BN = 64, BK = 16, PITCH = BK + 4, NSTAGE = 3;  // pitch 20: conflict-free LDS.64
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+template <int BYTES>
+__device__ __forceinline__ void cp_async(double* dst, const double* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(su32(dst)), "l"(src), "n"(BYTES),
+                 "r"(valid ? BYTES : 0)
+                 : "memory");
+}
+
+struct GridBatchArgs {
+    const double* V;
+    int64_t N1, N2, N3, ldy, ldz;
+    const double* X;
+    int64_t ldx;
+    const double* Y;
+    int64_t ldyy;
+    const double* Z;
+    int64_t ldzz;
+    int F;
+    int64_t M;  // N2 * N3
+    double* part;  // [n_mtiles][F]
+};
+
+// VEC: 16-byte copies (V, X 16-byte aligned, even strides); otherwise 8-byte copies.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads, 2) grid_batch_kernel(const GridBatchArgs p) {
+    extern __shared__ __align__(16) double sm[];
+    double* As = sm;                           // [NSTAGE][BM][PITCH]
+    double* Bs = sm + NSTAGE * BM * PITCH;     // [NSTAGE][BN][PITCH]
+    __shared__ double red[4][BN];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
+    const int f0 = blockIdx.x * BN;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
+    const int n_kc = static_cast<int>((p.N1 + BK - 1) / BK);
+
+    // Each thread copies fixed rows at a fixed column offset kk of every K chunk, so the row
+    // addresses (a 64-bit div/mod for V's (j, k)) are computed once.
+    constexpr int E = VEC ? 2 : 1;  // doubles per copy
+    constexpr int PER_ROW = BK / E, STEP = kThreads / PER_ROW;
+    constexpr int ARPT = BM / STEP, BRPT = BN / STEP;
+    const int kk = (tid % PER_ROW) * E, r0 = tid / PER_ROW;
+    int64_t abase[ARPT], bbase[BRPT];
+#pragma unroll
+    for (int n = 0; n < ARPT; ++n) {
+        const int64_t m = m0 + r0 + n * STEP;
+        abase[n] = m < p.M ? p.ldy * (m % p.N2) + p.ldz * (m / p.N2) : -1;
+    }
+#pragma unroll
+    for (int n = 0; n < BRPT; ++n) {
+        const int f = f0 + r0 + n * STEP;
+        bbase[n] = f < p.F ? p.ldx * f : -1;
+    }
+    auto load = [&](int kc, int stage) {
+        const int64_t i = static_cast<int64_t>(kc) * BK + kk;  // N1 is even when VEC: pairs never straddle
+        double* as = As + stage * BM * PITCH + r0 * PITCH + kk;
+        double* bs = Bs + stage * BN * PITCH + r0 * PITCH + kk;
+#pragma unroll
+        for (int n = 0; n < ARPT; ++n) {
+            const bool ok = abase[n] >= 0 && i < p.N1;
+            cp_async<8 * E>(as + n * STEP * PITCH, ok ? p.V + abase[n] + i : p.V, ok);
+        }
+#pragma unroll
+        for (int n = 0; n < BRPT; ++n) {
+            const bool ok = bbase[n] >= 0 && i < p.N1;
+            cp_async<8 * E>(bs + n * STEP * PITCH, ok ? p.X + bbase[n] + i : p.X, ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < NSTAGE - 1; ++s) {
+        if (s < n_kc) load(s, s);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int kc = 0; kc < n_kc; ++kc) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(NSTAGE - 2) : "memory");
+        __syncthreads();
+        const int nxt = kc + NSTAGE - 1;
+        if (nxt < n_kc) load(nxt, nxt % NSTAGE);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        const double* as = As + (kc % NSTAGE) * BM * PITCH + (wm * 32 + g) * PITCH + t;
+        const double* bs = Bs + (kc % NSTAGE) * BN * PITCH + (wn * 32 + g) * PITCH + t;
+#pragma unroll
+        for (int ks = 0; ks < BK / 4; ++ks) {
+            double a[4], b[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = as[mi * 8 * PITCH + 4 * ks];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) b[ni] = bs[ni * 8 * PITCH + 4 * ks];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+
+    // Epilogue: weight by Y(j,f) * Z(k,f), sum this lane's rows (mi ascending), then the 8 lanes
+    // sharing a column (xor tree over g), then the 4 warps along m (ascending wm).
+    double s[4][2];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) s[ni][0] = s[ni][1] = 0.0;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const int64_t m = m0 + wm * 32 + 8 * mi + g;
+        if (m >= p.M) continue;
+        const int64_t j = m % p.N2, k = m / p.N2;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int f = f0 + wn * 32 + 8 * ni + 2 * t + e;
+                if (f < p.F) {
+                    const double w = rn_mul(__ldg(p.Y + j + p.ldyy * f), __ldg(p.Z + k + p.ldzz * f));
+                    s[ni][e] = fma(acc[mi][ni][e], w, s[ni][e]);
+                }
+            }
+    }
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double v = s[ni][e];
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            if (g == 0) red[wm][wn * 32 + 8 * ni + 2 * t + e] = v;
+        }
+    __syncthreads();
+    if (tid < BN && f0 + tid < p.F) {
+        const double v = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
+        p.part[static_cast<int64_t>(blockIdx.y) * p.F + f0 + tid] = v;
+    }
+}
+
+__global__ void grid_batch_reduce_kernel(const double* __restrict__ part, int64_t n_mtiles, int F, double scale,
+                                         int accumulate, double* __restrict__ out) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= F) return;
+    double s = 0.0;
+    for (int64_t m = 0; m < n_mtiles; ++m) s += part[m * F + f];
+    s = rn_mul(s, scale);
+    out[f] = accumulate ? out[f] + s : s;
+}
+
+}  // namespace
+
+extern "C" int ls_grid_functional_batch(const double* V_d, int64_t N1, int64_t N2, int64_t N3, int64_t ldy,
+                                        int64_t ldz, const double* X_d, int64_t ldx, const double* Y_d,
+                                        int64_t ldyy, const double* Z_d, int64_t ldzz, int F, double scale,
+                                        int accumulate, double* out_d, void* stream) {
+    if (N1 < 0 || N2 < 0 || N3 < 0 || F < 0 || ldy < N1 || ldz < ldy * N2 || ldx < N1 || ldyy < N2 || ldzz < N3)
+        return ls::fail(LS_EVALIDATION, "grid_functional_batch: bad shape");
+    if (F == 0) return LS_OK;
+    const cudaStream_t s = ls::as_stream(stream);
+    const int64_t M = N2 * N3;
+    if (M == 0 || N1 == 0) {
+        if (!accumulate) LS_CUDA(cudaMemsetAsync(out_d, 0, sizeof(double) * F, s));
+        return LS_OK;
+    }
+    const int64_t n_mtiles = ls::ceil_div(M, BM);
+    if (n_mtiles > 65535) return ls::fail(LS_EGUARD, "grid_functional_batch: more than 65535*128 rows (split k)");
+    ls::ensure_pool();
+    double* part = nullptr;
+    LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * n_mtiles * F, s));
+    GridBatchArgs a{V_d, N1, N2, N3, ldy, ldz, X_d, ldx, Y_d, ldyy, Z_d, ldzz, F, M, part};
+    const bool vec = (reinterpret_cast<uintptr_t>(V_d) % 16 == 0) && (reinterpret_cast<uintptr_t>(X_d) % 16 == 0) &&
+                     N1 % 2 == 0 && ldy % 2 == 0 && ldz % 2 == 0 && ldx % 2 == 0;
+    const size_t smem = sizeof(double) * NSTAGE * (BM + BN) * PITCH;
+    void (*kern)(GridBatchArgs) = vec ? grid_batch_kernel<true> : grid_batch_kernel<false>;
+    LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const dim3 grid(static_cast<unsigned>(ls::ceil_div(F, BN)), static_cast<unsigned>(n_mtiles));
+    kern<<<grid, kThreads, smem, s>>>(a);
+    LS_LAUNCHED("grid_batch_kernel");
+    grid_batch_reduce_kernel<<<static_cast<unsigned>(ls::ceil_div(F, 128)), 128, 0, s>>>(part, n_mtiles, F, scale,
+                                                                                        accumulate, out_d);
+    LS_LAUNCHED("grid_batch_reduce_kernel");
+    LS_CUDA(cudaFreeAsync(part, s));
+    return LS_OK;
+}

@@ -499,6 +499,36 @@ def functional_batch(P: CanonicalTensor3, rho: Sequence[np.ndarray], scale: floa
     return out.cpu().numpy()[:F]
 
 
+def grid_functional_batch(P: CanonicalTensor3, rho: Sequence[np.ndarray], scale: float = 1.0,
+                          max_chunk_points: int = 1 << 28) -> np.ndarray:
+    """Full-grid form of functional_batch: P is expanded on the device in
+    z-slab chunks of at most max_chunk_points and every chunk is contracted against the F
+    separable densities by one fused DMMA GEMM (ls_grid_functional_batch). Agrees with the
+    1D rank-term form (scalar_product, canonical.hpp:126-136) to rounding."""
+    import torch
+    dev = torch.device("cuda")
+    fac = [torch.as_tensor(P.factor(l), device=dev).T.contiguous() for l in range(3)]  # (R, n_l)
+    w = torch.as_tensor(P.weights(), device=dev)
+    X, Y, Z = (torch.as_tensor(_f64(r), device=dev) for r in rho)
+    out = DevicePipeline.grid_functional_batch_device(
+        lambda buf, k0, k1: _expand_device(fac, w, P.dims(), k0, k1, buf), P.dims(), [X, Y, Z], scale,
+        max_chunk_points)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _expand_device(fac, w, dims, k0, k1, buf):
+    """ls_expand of slabs [k0, k1) of the device factors fac[l] ((R, n_l) row-major) into buf."""
+    import torch
+    n1, n2, n3 = dims
+    R = w.shape[0]
+    s = torch.cuda.current_stream(buf.device)
+    p = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+    call("ls_expand", p(fac[0]), n1, p(fac[1]), n2, p(fac[2]), n3, p(w), n1, n2, n3, R, k0, k1,
+         C.c_void_p(buf.data_ptr()), buf.stride(1), buf.stride(0), None, None, None, None,
+         C.c_void_p(s.cuda_stream))
+
+
 # ---------------------------------------------------------- device pipeline
 class _DeviceView:
     """Zero-copy torch view of device memory owned by the native pipeline (CUDA array interface)."""
@@ -593,6 +623,35 @@ class DevicePipeline:
         call("ls_pipeline_energy", self._h, self._ptr(r[0]), self._ptr(r[1]), self._ptr(r[2]), k0, k1,
              self._ptr(out), self._stream(stream))
         return out
+
+    @staticmethod
+    def grid_functional_batch_device(expand, dims, rho, scale=1.0, max_chunk_points=1 << 28):
+        """Full-grid functionals sum V * rho_f for F separable rho = (X, Y, Z) (device (n_l, F)
+        tensors): expand(buf, k0, k1) writes slabs [k0, k1) into buf ((k1-k0, n2, n1) float64),
+        which is contracted chunk by chunk (ls_grid_functional_batch, accumulate in slab order)."""
+        import torch
+        n1, n2, n3 = dims
+        X, Y, Z = rho
+        F = X.shape[1]
+        Xt, Yt, Zt = (r.T.contiguous() for r in (X, Y, Z))  # (F, n) rows = column-major (n, F)
+        out = torch.zeros(F, dtype=torch.float64, device=X.device)
+        kc = max(1, min(n3, max_chunk_points // max(1, n1 * n2)))
+        buf = torch.empty((kc, n2, n1), dtype=torch.float64, device=X.device)
+        s = torch.cuda.current_stream(X.device)
+        p = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+        for k0 in range(0, n3, kc):
+            k1 = min(n3, k0 + kc)
+            expand(buf, k0, k1)
+            call("ls_grid_functional_batch", p(buf), n1, n2, k1 - k0, buf.stride(1), buf.stride(0), p(Xt), n1,
+                 p(Yt), n2, C.c_void_p(Zt.data_ptr() + 8 * k0), n3, F, float(scale), int(k0 > 0), p(out),
+                 C.c_void_p(s.cuda_stream))
+        return out
+
+    def grid_functional_batch(self, rho, scale=1.0, max_chunk_points=1 << 28):
+        """Full-grid form of functional_batch on this pipeline's potential (cfg4's 1024 test
+        functions over the whole grid); rho = (X, Y, Z) device (n_l, F) tensors."""
+        return DevicePipeline.grid_functional_batch_device(
+            lambda buf, k0, k1: self.expand(buf, k0, k1), self.dims, rho, scale, max_chunk_points)
 
     @staticmethod
     def functional_batch_device(factors, w, rho, scale=1.0, stream=None):

@@ -334,6 +334,49 @@ def test_cfg4_periodic_and_functional_batch(L, orc, Lc):
     del P
 
 
+@pytest.mark.parametrize("dims,R,F", [((5, 7, 3), 3, 5), ((33, 17, 9), 41, 70), ((130, 66, 4), 6, 129),
+                                      ((64, 64, 64), 41, 64), ((1, 1, 1), 1, 1), ((200, 3, 2), 2, 200)])
+def test_grid_functional_batch_random(L, orc, dims, R, F):
+    """Full-grid functional batch (fused DMMA GEMM) vs the dense grid contracted on the host.
+    Odd N1 takes the 8-byte copy path; F and N2*N3 not multiples of the 64 x 128 tiles."""
+    rng = np.random.default_rng(7 * R + F)
+    f = [np.asfortranarray(rng.uniform(-1, 1, (d, R))) for d in dims]
+    w = rng.uniform(-1, 1, R)
+    t = L.CanonicalTensor3(f, w)
+    V = orc.densify_slabs(f[0], f[1], f[2], w)
+    G = [np.asfortranarray(rng.uniform(-1, 1, (d, F))) for d in dims]
+    got = L.grid_functional_batch(t, G, scale=0.5)
+    want = 0.5 * np.einsum("ijk,if,jf,kf->f", V, *G)
+    mag = 0.5 * np.einsum("ijk,if,jf,kf->f", np.abs(V), *[np.abs(g) for g in G])
+    assert np.all(np.abs(got - want) <= 1e-13 * mag + 1e-300)
+    # slab-chunked evaluation (accumulating launches) agrees to rounding
+    chunked = L.grid_functional_batch(t, G, scale=0.5, max_chunk_points=dims[0] * dims[1])
+    assert np.all(np.abs(chunked - want) <= 1e-13 * mag + 1e-300)
+
+
+def test_cfg4_grid_functional_batch_matches_1d_form(L):
+    """cfg4: 1024 separable Gaussian test functions over the whole 256^3 periodic potential,
+    full-grid form (expansion + fused GEMM) vs the 1D rank-term form (scalar_product)."""
+    import torch
+    spec, rule = cfg(L, 64, n=256)
+    pipe = L.DevicePipeline(spec, rule, mode="erf", periodic=True)
+    pipe.generate()
+    pipe.assemble()
+    rng = np.random.default_rng(11)
+    F = 1024
+    alpha = 10 ** rng.uniform(-1, 1, F)
+    sigma = 1 / np.sqrt(2 * alpha)
+    centres = rng.uniform(-5.0, 5.0, (F, 3))
+    mids = (np.arange(256) + 0.5 - 128) * spec.unit.h
+    G = [torch.as_tensor(np.exp(-(mids[:, None] - centres[None, :, l]) ** 2 / (2 * sigma ** 2)), device="cuda")
+         for l in range(3)]
+    full = pipe.grid_functional_batch(G).cpu().numpy()
+    one_d = L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w, G).cpu().numpy()
+    assert np.max(np.abs(full - one_d) / np.abs(one_d)) <= 1e-12
+    again = pipe.grid_functional_batch(G).cpu().numpy()
+    assert np.array_equal(full, again)  # fixed-order reductions: bitwise run to run
+
+
 def test_eval_points_and_scalar_product(L, orc):  # test_canonical.cpp:88-139
     rng = np.random.default_rng(9)
     f = [np.asfortranarray(rng.uniform(-1, 1, (d, 3))) for d in (4, 5, 6)]
