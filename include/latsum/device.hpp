@@ -73,6 +73,21 @@ public:
         cuda::check(ls_pipeline_energy(h_, r1_d, r2_d, r3_d, k0, k1, out_d, stream), "energy");
     }
 
+    // Full-grid functionals of slabs [k0, k1) for F separable densities
+    // rho_f = X(:,f) (x) Y(:,f) (x) Z(:,f), X/Y/Z column-major N_l x F in device memory:
+    // out_d[f] (+)= sum over the slabs of V * rho_f. The slabs are expanded into scratch_d
+    // ((k1-k0)*N1*N2 doubles), then contracted by one fused FP64-DMMA GEMM. Call it per slab
+    // chunk with accumulate = true after the first to cover grids larger than the scratch.
+    void grid_functionals(const double* X_d, const double* Y_d, const double* Z_d, int F, Index k0, Index k1,
+                          double* scratch_d, double* out_d, bool accumulate = false, void* stream = nullptr) {
+        if (k0 < 0 || k1 < k0 || k1 > dims_[2]) throw validation_error("grid_functionals: bad slab range");
+        expand(k0, k1, scratch_d, stream);
+        cuda::check(ls_grid_functional_batch(scratch_d, dims_[0], dims_[1], k1 - k0, dims_[0], dims_[0] * dims_[1],
+                                             X_d, dims_[0], Y_d, dims_[1], Z_d + k0, dims_[2], F, 1.0,
+                                             accumulate ? 1 : 0, out_d, stream),
+                    "grid_functionals");
+    }
+
     // The assembled canonical tensor, copied to the host (after generate + assemble).
     CanonicalTensor3 tensor(void* stream = nullptr) const {
         const double* f[3];

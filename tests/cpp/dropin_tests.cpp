@@ -671,6 +671,39 @@ TEST(DevicePotential, MatchesHostPipelineAndEnergy) {  // additive API over ls_p
     EXPECT_EQ(covered, d[2]);
 }
 
+TEST(DevicePotential, GridFunctionalsMatchScalarProduct) {  // full-grid batch vs the 1D form
+    LatticeSpec spec = make_spec({2, 3, 2}, 8, 2.0, {Charge{{0.0, 0.0, 0.0}, 1.0}});
+    QuadratureRule rule = sinc_quadrature(1e-4, spec.unit.h(), std::sqrt(3.0) * 6.0, 10, 1.0);
+    DevicePotential dev(spec, rule, Generator::erf, /*periodic=*/true);
+    dev.generate();
+    dev.assemble();
+    const Dims3 d = dev.dims();
+    const int F = 5;
+    std::array<Matrix, 3> rho;
+    for (int l = 0; l < 3; ++l) {
+        rho[l].resize(d[l], F);
+        for (Index i = 0; i < d[l]; ++i)
+            for (int f = 0; f < F; ++f) rho[l](i, f) = std::exp(-0.1 * (f + 1) * static_cast<double>((i - 3) * (i - 3)));
+    }
+    DeviceBuffer X(d[0] * F), Y(d[1] * F), Z(d[2] * F), out(F), scratch(static_cast<std::size_t>(d[0] * d[1] * d[2]));
+    X.upload(rho[0].data(), X.size());
+    Y.upload(rho[1].data(), Y.size());
+    Z.upload(rho[2].data(), Z.size());
+    // two slab chunks, the second accumulating
+    dev.grid_functionals(X.data(), Y.data(), Z.data(), F, 0, 3, scratch.data(), out.data());
+    dev.grid_functionals(X.data(), Y.data(), Z.data(), F, 3, d[2], scratch.data(), out.data(), true);
+    std::vector<double> got(F);
+    out.download(got.data(), F);
+    CanonicalTensor3 t = dev.tensor();
+    for (int f = 0; f < F; ++f) {
+        std::array<Matrix, 3> rf{Matrix(rho[0].col(f)), Matrix(rho[1].col(f)), Matrix(rho[2].col(f))};
+        const double want = scalar_product(t, CanonicalTensor3(std::move(rf), Vector::Ones(1)));
+        EXPECT_NEAR(got[f], want, 1e-12 * std::abs(want));
+    }
+    EXPECT_THROW(dev.grid_functionals(X.data(), Y.data(), Z.data(), F, 2, 1, scratch.data(), out.data()),
+                 validation_error);
+}
+
 // ------------------------------------------------------------------ bundle / CSV formats
 std::string golden_dir() {
     const char* d = std::getenv("LATSUM_GOLDEN_DIR");
