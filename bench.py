@@ -268,6 +268,8 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.step_only):
         cpu = cpu_baseline(spec, rule, budget_s=args.cpu_seconds)
+        one = cpu_baseline(spec, rule, budget_s=min(3.0, args.cpu_seconds), threads=1)  # also 1 thread
+        cpu["single_thread"] = {"value": one["value"], "unit": one["unit"], "cores": 1, "sample": one["sample"]}
 
     configs = None
     if rank == 0 and world == 1 and not (args.no_configs or args.step_only):
