@@ -160,7 +160,12 @@ int ls_maxdiff_accumulate(const double* a_d, const double* b_d, int64_t n, doubl
  * HBM on the current device; the handle owns the master, assembled factors
  * and weights (Z_nu * w_q). charges_h holds M0 rows (x, y, z, Z) in
  * unit-cell coordinates [-b/2, b/2] (validated and snapped like
- * LatticeSpec, lattice.hpp:28-69). dims = n^3 (periodic) or (L*n)^3-shaped. */
+ * LatticeSpec, lattice.hpp:28-69). dims = n^3 (periodic) or (L*n)^3-shaped.
+ * The handle remembers its device: every call runs there and restores the
+ * caller's current device. Calls on one handle are stream-ordered on the
+ * caller's stream; a handle is not meant for concurrent use from several
+ * threads or streams (energy reuses one partial buffer) -- use one handle per
+ * stream, as ShardedPotential does per rank. */
 typedef struct ls_pipeline ls_pipeline;
 int ls_pipeline_create(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h, const double* w_h,
                        int R, const double* charges_h, int M0, int periodic, ls_pipeline** out);

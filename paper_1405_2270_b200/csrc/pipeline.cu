@@ -90,8 +90,10 @@ int ls_pipeline_create(int mode, const int64_t L[3], int64_t n, double b, const 
         }
         for (int q = 0; q < R; ++q) wt[static_cast<size_t>(nu) * R + q] = Z * w_h[q];  // lattice.hpp:284-287
     }
+    int device = 0;
+    LS_CUDA(cudaGetDevice(&device));
     ls_pipeline* p = new ls_pipeline;
-    LS_CUDA(cudaGetDevice(&p->device));
+    p->device = device;
     p->mode = mode;
     p->periodic = periodic ? 1 : 0;
     p->n = n;
@@ -117,9 +119,10 @@ int ls_pipeline_create(int mode, const int64_t L[3], int64_t n, double b, const 
     if ((e = cudaMalloc(&p->tau, sizeof(double) * R)) != cudaSuccess) return fail_cleanup(e, "cudaMalloc tau");
     if ((e = cudaMalloc(&p->w, sizeof(double) * wt.size())) != cudaSuccess) return fail_cleanup(e, "cudaMalloc w");
     if ((e = cudaMalloc(&p->ia, sizeof(int64_t) * ia.size())) != cudaSuccess) return fail_cleanup(e, "cudaMalloc ia");
-    cudaMemcpy(p->tau, tau_h, sizeof(double) * R, cudaMemcpyHostToDevice);
-    cudaMemcpy(p->w, wt.data(), sizeof(double) * wt.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(p->ia, ia.data(), sizeof(int64_t) * ia.size(), cudaMemcpyHostToDevice);
+    if ((e = cudaMemcpy(p->tau, tau_h, sizeof(double) * R, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(p->w, wt.data(), sizeof(double) * wt.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(p->ia, ia.data(), sizeof(int64_t) * ia.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail_cleanup(e, "cudaMemcpy pipeline inputs");
     for (int l = 0; l < 3; ++l) {
         if (p->axis_src[l] != l) {
             p->master[l] = p->master[p->axis_src[l]];
@@ -136,6 +139,8 @@ int ls_pipeline_create(int mode, const int64_t L[3], int64_t n, double b, const 
 }
 
 int ls_pipeline_destroy(ls_pipeline* p) {
+    if (!p) return LS_OK;
+    ls::DeviceGuard dg(p->device);
     release(p);
     return LS_OK;
 }
@@ -153,7 +158,12 @@ int ls_pipeline_info(const ls_pipeline* p, int64_t dims[3], int* rank_total, con
     return LS_OK;
 }
 
+#define LS_PIPELINE_ENTRY(p)                                                 \
+    if (!(p)) return ls::fail(LS_EVALIDATION, "pipeline: null handle");    \
+    ls::DeviceGuard device_guard_((p)->device)
+
 int ls_pipeline_generate(ls_pipeline* p, void* stream) {
+    LS_PIPELINE_ENTRY(p);
     for (int l = 0; l < 3; ++l) {
         if (p->axis_src[l] != l) continue;
         const int64_t len = 2 * p->L[l] * p->n;
@@ -164,6 +174,7 @@ int ls_pipeline_generate(ls_pipeline* p, void* stream) {
 }
 
 int ls_pipeline_assemble(ls_pipeline* p, void* stream) {
+    LS_PIPELINE_ENTRY(p);
     for (int l = 0; l < 3; ++l) {
         if (p->axis_src[l] != l) continue;
         const int rc = ls_assemble_axis(p->master[l], 2 * p->L[l] * p->n, p->R, p->M0, p->ia + l * p->M0, p->n, p->L[l],
@@ -174,11 +185,13 @@ int ls_pipeline_assemble(ls_pipeline* p, void* stream) {
 }
 
 int ls_pipeline_expand(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void* stream) {
+    LS_PIPELINE_ENTRY(p);
     return ls_expand(p->fac[0], p->dims[0], p->fac[1], p->dims[1], p->fac[2], p->dims[2], p->w, p->dims[0], p->dims[1],
                      p->dims[2], p->Rt, k0, k1, out_d, 0, 0, nullptr, nullptr, nullptr, nullptr, stream);
 }
 
 int ls_pipeline_step(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void* stream) {
+    LS_PIPELINE_ENTRY(p);
     int rc = ls_pipeline_generate(p, stream);
     if (!rc) rc = ls_pipeline_assemble(p, stream);
     if (!rc) rc = ls_pipeline_expand(p, k0, k1, out_d, stream);
@@ -187,6 +200,7 @@ int ls_pipeline_step(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void
 
 int ls_pipeline_energy(ls_pipeline* p, const double* r1_d, const double* r2_d, const double* r3_d, int64_t k0,
                        int64_t k1, double* out_d, void* stream) {
+    LS_PIPELINE_ENTRY(p);
     const int64_t np = ls_expand_partial_count(p->dims[0], p->dims[1], p->Rt, k0, k1);
     if (np < 0) return ls::fail(LS_EGUARD, "energy: no tile plan for this rank");
     if (np > p->partial_cap) {

@@ -64,6 +64,12 @@ def test_device_entry_points_validate_before_device_work():
     assert lib.ls_expand(None, 4, None, 4, None, 4, None, 4, 4, 4, 3, 2, 5, None, 0, 0, None, None, None, None,
                          None) == _abi.LS_EVALIDATION
     assert lib.ls_assemble_axis(None, 16, 3, 1, None, 8, 1, 0, None, 4, None) == _abi.LS_EVALIDATION
+    # pipeline entry points reject a null handle; shape errors of the grid batch come first
+    assert lib.ls_pipeline_generate(None, None) == _abi.LS_EVALIDATION
+    assert lib.ls_pipeline_energy(None, None, None, None, 0, 1, None, None) == _abi.LS_EVALIDATION
+    assert b"null handle" in lib.ls_last_error()
+    assert lib.ls_grid_functional_batch(None, 4, 4, 4, 3, 16, None, 4, None, 4, None, 4, 2, 1.0, 0, None,
+                                        None) == _abi.LS_EVALIDATION
 
 
 def test_python_mirror_validation():  # lattice.hpp:57-68, grid.hpp:21-27, canonical.hpp:42-56
