@@ -470,6 +470,7 @@ using TileNarrow = Tile<4, 1, 4, 4, 2>;  // 32-row i-chunk (largest ranks)
 using TileLR1 = Tile<8, 1, 4, 4, 1>;     // large ranks: 32-row i-chunk, 256-column stages, 1 CTA/SM
 using TileLR2 = Tile<8, 2, 4, 4, 1>;     // large ranks: 64-row i-chunk, 128-column stages, 1 CTA/SM
 using TileLR1b = Tile<8, 1, 4, 4, 1, 2>; // as TileLR1 with a 2-deep ring of longer stages
+using TileLR16 = Tile<16, 1, 4, 4, 1, 2>; // large ranks: 16 warps (4 per SM sub-partition), 512-column stages
 
 struct Plan {
     int id;  // see plan_for; 20 = TileWide geometry with A1k in TMEM
@@ -512,9 +513,11 @@ bool plan_for(int KD, int n_tail, Plan& out) {
     struct Cand {
         int id, KC;
     };
-    // Measured on B200 (tools/profile_expand.py, tools/profile_rank.py): plan 0 for the BASELINE
-    // rank 41 (29.2 TF/s); plan 8 for rank 328 (28.7 TF/s vs 20.3 for the 4-warp plan 3).
-    const Cand cands[] = {{kPlanTmem, 0}, {0, 0}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
+    // Measured on B200 (tools/profile_expand.py, tools/profile_rank.py, tools/profile_rank_sweep.py):
+    // the TMEM plan for the BASELINE rank 41 (31.2 TF/s); plan 9 for ranks beyond it (cfg3 rank 328:
+    // 31.3 TF/s, against 28.7 for the 8-warp plan 8 and 20.3 for the 4-warp plan 3; 16-warp tiles
+    // with a 64-row i-chunk (29.0) or 16-row warp tiles (no fit) were slower).
+    const Cand cands[] = {{kPlanTmem, 0}, {0, 0}, {9, 4}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
     for (const Cand& c : cands) {
         if (force >= 0 && c.id != force) continue;
         const int KC = c.KC == 0 ? KD : std::min(KD, c.KC);
@@ -527,6 +530,7 @@ bool plan_for(int KD, int n_tail, Plan& out) {
             case 6: ok = fits<TileLR1>(KD, KC, n_tail); ic = TileLR1::IC; break;
             case 7: ok = fits<TileLR2>(KD, KC, n_tail); ic = TileLR2::IC; break;
             case 8: ok = fits<TileLR1b>(KD, KC, n_tail); ic = TileLR1b::IC; break;
+            case 9: ok = fits<TileLR16>(KD, KC, n_tail); ic = TileLR16::IC; break;
             case kPlanTmem: ok = fits_tmem(KD, n_tail); ic = TileWide::IC; break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
         }
@@ -623,6 +627,7 @@ int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
         case 6: return launch<TileLR1, STORE, FUNC>(a, s);
         case 7: return launch<TileLR2, STORE, FUNC>(a, s);
         case 8: return launch<TileLR1b, STORE, FUNC>(a, s);
+        case 9: return launch<TileLR16, STORE, FUNC>(a, s);
         default: return launch<TileNarrow, STORE, FUNC>(a, s);
     }
 }

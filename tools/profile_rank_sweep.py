@@ -1,0 +1,36 @@
+"""Times ls_expand over a rank sweep on random factors (plan selection study).
+
+  python tools/profile_rank_sweep.py [--n 1024] [--slabs 64] [--ranks 60,82,164,328]
+Set LS_EXPAND_PLAN / LS_EXPAND_KC in the environment to force a plan.
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.environ.get("LS_LAB_ROOT", "/root/repo"))
+import torch  # noqa: E402
+
+from paper_1405_2270_b200.latsum import _expand_device  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=1024)
+ap.add_argument("--slabs", type=int, default=64)
+ap.add_argument("--ranks", default="60,82,123,164,246,328")
+args = ap.parse_args()
+n, ks = args.n, args.slabs
+out = torch.empty((ks, n, n), dtype=torch.float64, device="cuda")
+g = torch.Generator(device="cuda").manual_seed(1)
+for R in map(int, args.ranks.split(",")):
+    fac = [torch.rand((R, n), dtype=torch.float64, device="cuda", generator=g) for _ in range(3)]
+    w = torch.rand(R, dtype=torch.float64, device="cuda", generator=g)
+    _expand_device(fac, w, (n, n, n), 0, ks, out)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(3):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e[0].record()
+        _expand_device(fac, w, (n, n, n), 0, ks, out)
+        e[1].record()
+        torch.cuda.synchronize()
+        best = min(best, e[0].elapsed_time(e[1]))
+    print(f"R={R:4d}: {best:.3f} ms, {2.0 * R * n * n * ks / best / 1e9:.2f} TF/s")
