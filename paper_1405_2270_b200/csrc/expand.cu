@@ -23,18 +23,23 @@
 //    every pipeline stage -- JT j-tiles x KC k-steps -- is one contiguous
 //    block that a single thread moves with cp.async.bulk (TMA) into an
 //    NS-deep ring, completion signalled on an mbarrier (expect_tx);
-//  * warps multiply with register ping-pong fragments (no moves), each
+//  * warps load both fragments straight from shared memory per k-step, each
 //    owning TM x TN independent 8x8 accumulators (M = j, N = i, K = q), and
 //    store straight from the accumulator fragments: lane (g, t) holds
 //    V(i = 8n + 2t + {0,1}, j = 8m + g), a 16-byte aligned pair of the
 //    i-fastest grid, written with streaming stores.
 //  * a rank remainder of 1-2 (R mod 4) runs on DFMA instead of a zero-padded
 //    4-rank DMMA step.
-// One __syncthreads per stage guards ring-slot reuse; units are spread over
-// a persistent grid (CTAs per SM x SM count).
+// No CTA barrier per stage: each warp releases a ring slot after its last
+// DMMA of the stage and the last one refills it. Units are spread over a
+// persistent grid (CTAs per SM x SM count). expand_tmem.cuh holds the default
+// variant for ranks up to 57, with A1k resident in tensor memory.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 
@@ -113,13 +118,25 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
 //   [jt][kk][lane] = A2(8 (jc JT + jt) + g, 4 (kc KC + kk) + t)   (MMA A-fragment order)
 //   then [jt][qt][g] = A2(8 (jc JT + jt) + g, 4 KD + qt)          (DFMA tail ranks)
 // zero padded outside the matrix.
+// With S != nullptr the same launch also writes the TMEM variant's slab-scale table
+// S[k][q] = w_q * C(k, q) for k in [0, k1) (canonical.hpp:244), after the packed stages.
 __global__ void pack_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t N2, int R, int KD, int n_tail,
-                              int KC, int n_kc, int JT, int64_t n_jc, double* __restrict__ Bp) {
+                              int KC, int n_kc, int JT, int64_t n_jc, double* __restrict__ Bp,
+                              const double* __restrict__ w, const double* __restrict__ C, int64_t ldc, int64_t k1,
+                              double* __restrict__ S) {
     const int64_t frag = static_cast<int64_t>(JT) * KC * 32;
     const int64_t stage_elems = frag + static_cast<int64_t>(JT) * 8 * n_tail;
     const int64_t total = static_cast<int64_t>(n_kc) * n_jc * stage_elems;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+    const int64_t n_scale = S ? k1 * R : 0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total + n_scale;
          e += (int64_t)gridDim.x * blockDim.x) {
+        if (e >= total) {
+            const int64_t x = e - total;
+            const int64_t k = x / R;
+            const int q = static_cast<int>(x - k * R);
+            S[x] = rn_mul(w[q], C[k + ldc * q]);
+            continue;
+        }
         const int64_t st = e / stage_elems;
         const int64_t o = e - st * stage_elems;
         const int kc = static_cast<int>(st / n_jc);
@@ -410,15 +427,6 @@ expand_dmma_kernel(const ExpandArgs p) {
     }
 }
 
-__global__ void scale_table_kernel(const double* __restrict__ w, const double* __restrict__ C, int64_t ldc, int R,
-                                   int64_t k1, double* __restrict__ S) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k1 * R; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = e / R;
-        const int q = static_cast<int>(e % R);
-        S[e] = rn_mul(w[q], C[k + ldc * q]);  // canonical.hpp:244
-    }
-}
-
 #include "expand_tmem.cuh"
 
 __global__ void sum_partials_kernel(const double* __restrict__ part, int64_t count,
@@ -543,6 +551,35 @@ bool plan_for(int KD, int n_tail, Plan& out) {
     return false;
 }
 
+// Per-(kernel, device) launch setup, cached: the attribute calls and the occupancy query cost
+// microseconds each, which dominated small expansions (25 us per 128^3 call before). The
+// dynamic shared-memory limit is raised to the device maximum once; occupancy is cached per
+// shared-memory size.
+int kernel_setup(const void* kern, int threads, size_t smem, int& per_sm) {
+    static std::mutex m;
+    static std::map<std::tuple<const void*, int>, bool> configured;
+    static std::map<std::tuple<const void*, int, size_t>, int> occupancy;
+    int dev = 0;
+    LS_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(m);
+    auto ko = occupancy.find({kern, dev, smem});
+    if (ko != occupancy.end()) {
+        per_sm = ko->second;
+        return LS_OK;
+    }
+    if (!configured[{kern, dev}]) {
+        int optin = 0;
+        LS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+        LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
+        configured[{kern, dev}] = true;
+    }
+    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    occupancy[{kern, dev, smem}] = per_sm;
+    return LS_OK;
+}
+
 template <class T, bool STORE, bool FUNC, bool TMEM = false>
 int launch(ExpandArgs& a, cudaStream_t s) {
     const TmemShape sh = TMEM ? tmem_shape() : TmemShape{T::NS, 1};
@@ -560,16 +597,10 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     const size_t s_elems = TMEM ? static_cast<size_t>(a.k1) * a.R : 0;
     ls::ensure_pool();
     LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bp), (bp_elems + s_elems) * sizeof(double), s));
-    if (TMEM) {
-        double* S = bp + bp_elems;
-        const int64_t ns = a.k1 * a.R;
-        scale_table_kernel<<<(unsigned)std::min<int64_t>(ls::ceil_div(ns, 256), 4096), 256, 0, s>>>(a.w, a.C, a.ldc,
-                                                                                                      a.R, a.k1, S);
-        LS_LAUNCHED("scale_table_kernel");
-        a.S = S;
-    }
-    const int64_t pb = std::min<int64_t>(ls::ceil_div(static_cast<int64_t>(bp_elems), 256), 4096);
-    pack_b_kernel<<<(unsigned)pb, 256, 0, s>>>(a.B, a.ldb, a.N2, a.R, a.KD, a.n_tail, a.KC, a.n_kc, JT, a.n_jc, bp);
+    a.S = TMEM ? bp + bp_elems : nullptr;
+    const int64_t pb = std::min<int64_t>(ls::ceil_div(static_cast<int64_t>(bp_elems + s_elems), 256), 4096);
+    pack_b_kernel<<<(unsigned)pb, 256, 0, s>>>(a.B, a.ldb, a.N2, a.R, a.KD, a.n_tail, a.KC, a.n_kc, JT, a.n_jc, bp,
+                                               a.w, a.C, a.ldc, a.k1, const_cast<double*>(a.S));
     LS_LAUNCHED("pack_b_kernel");
     a.Bp = bp;
     // 32-bit counters inside the kernel
@@ -587,10 +618,8 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         else if (code == 22) kern = expand_tmem_kernel<STORE, FUNC, 2, 2>;
         else return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
     }
-    LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     int per_sm = 0;
-    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T::WARPS * 32, smem));
+    if (const int rc = kernel_setup(reinterpret_cast<const void*>(kern), T::WARPS * 32, smem, per_sm)) return rc;
     if (per_sm < 1) return ls::fail(LS_EGUARD, "expand: tile does not fit on an SM");
     // The occupancy query under-reports the tcgen05 kernel (1 instead of 2 CTAs/SM although
     // registers, shared memory and the 2 x 256 TMEM columns all fit two); use the launch bound.

@@ -208,14 +208,65 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
         if (lane == 0) mbar_arrive(as_full + buf);
     };
 
-    // Prologue: the first unit's A1k (buffer 0), all tasks now.
-    if (my_units > 0) {
-        task_issue(blockIdx.x, 0);
-        for (int task = 0; task < n_tasks; ++task) run_task(blockIdx.x, task, 0);
-        publish(0);
-    }
+    // The first ring stages load while the warps build the first unit's A1k.
     if (threadIdx.x == 0)
         for (int st = 0; st < kNS && st < n_stages; ++st) issue(st);
+    // Prologue: the first unit's A1k (buffer 0), all tasks now, with the global loads of up to
+    // four tasks in flight at once (no accumulators are live yet, so the registers are free);
+    // then the copy for the next unit's first task starts the one-ahead chain.
+    if (my_units > 0) {
+        const int u = blockIdx.x;
+        const int ib = (u % n_ichunks) * IC;
+        const int64_t k = p.k0 + u / n_ichunks;
+        for (int t0 = 0; t0 < n_tasks; t0 += 4) {
+            double av[4][8], sv[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int task = t0 + b;
+                if (task >= n_tasks) break;
+                if (task < n_frag_tasks) {
+                    const int q = 4 * (wj + 2 * task) + t;
+                    sv[b] = q < p.R ? __ldg(p.S + k * p.R + q) : 0.0;
+#pragma unroll
+                    for (int it = 0; it < 4; ++it) {
+                        const int i = ib + 8 * (4 * wi + it) + g;
+                        av[b][it] = (i < p.N1 && q < p.R) ? __ldg(p.A + i + p.lda * q) : 0.0;
+                    }
+                } else {
+                    const int q = 4 * KD + (task - n_frag_tasks);
+                    sv[b] = __ldg(p.S + k * p.R + q);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int i = ib + 32 * wi + 8 * (e >> 1) + 2 * t + (e & 1);
+                        av[b][e] = i < p.N1 ? __ldg(p.A + i + p.lda * q) : 0.0;
+                    }
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int task = t0 + b;
+                if (task >= n_tasks) break;
+                if (task < n_frag_tasks) {
+                    double v[4];
+#pragma unroll
+                    for (int it = 0; it < 4; ++it) v[it] = rn_mul(av[b][it], sv[b]);
+                    tmem::st_x8(tq + 8 * (wj + 2 * task), v);
+                } else {
+                    const int qt = task - n_frag_tasks;
+                    double v0[4], v1[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        v0[e] = rn_mul(av[b][e], sv[b]);
+                        v1[e] = rn_mul(av[b][4 + e], sv[b]);
+                    }
+                    tmem::st_x8(tq + 8 * KD + 16 * qt, v0);
+                    tmem::st_x8(tq + 8 * KD + 16 * qt + 8, v1);
+                }
+            }
+        }
+        if (u + static_cast<int>(gridDim.x) < n_units) task_issue(u + gridDim.x, 0);
+        publish(0);
+    }
 
     double acc[kTM][kTN][2];
     double fsum = 0.0;
