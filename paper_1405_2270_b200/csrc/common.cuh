@@ -21,6 +21,7 @@ inline int fail(int code, const std::string& msg) {
     return code;
 }
 inline int cuda_fail(cudaError_t e, const char* where) {
+    cudaGetLastError();  // clear a non-sticky error so the next launch check does not report it again
     return fail(LS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 

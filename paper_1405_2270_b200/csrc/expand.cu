@@ -479,14 +479,16 @@ using TileLR1 = Tile<8, 1, 4, 4, 1>;     // large ranks: 32-row i-chunk, 256-col
 using TileLR2 = Tile<8, 2, 4, 4, 1>;     // large ranks: 64-row i-chunk, 128-column stages, 1 CTA/SM
 using TileLR1b = Tile<8, 1, 4, 4, 1, 2>; // as TileLR1 with a 2-deep ring of longer stages
 using TileLR16 = Tile<16, 1, 4, 4, 1, 2>; // large ranks: 16 warps (4 per SM sub-partition), 512-column stages
+using TileTmem16 = Tile<16, 4, 4, 4, 1, 2>; // TMEM variant, 1 CTA/SM: 128-row i-chunk, 128-column stages
 
 struct Plan {
-    int id;  // see plan_for; 20 = TileWide geometry with A1k in TMEM
+    int id;  // see plan_for; 20 / 21 = A1k in TMEM (8 warps x 2 CTAs / 16 warps x 1 CTA per SM)
     int KC;
     int ic;
+    int pad = 0;  // 1: run a 2-rank remainder as one zero-padded k-step (TMEM plans have a 1-rank tail)
 };
 
-constexpr int kPlanTmem = 20;
+constexpr int kPlanTmem = 20, kPlanTmem16 = 21;
 // TMEM variant shape (ring depth, j-chunks per stage); LS_EXPAND_TMEM=<ns><jps> overrides.
 struct TmemShape {
     int ns, jps;
@@ -500,14 +502,23 @@ inline TmemShape tmem_shape() {
     return sh;
 }
 
-// The TMEM variant: TileWide geometry, whole rank per stage, A1k double-buffered in 256 TMEM
-// columns (KD <= 14, at most one tail rank); shared memory holds only the A2 ring.
+// The TMEM variants: whole rank per stage, A1k double-buffered in TMEM (at most one tail
+// rank); shared memory holds the A2 ring and the fill staging.
+//  * 8 warps, 2 CTAs/SM, 256 columns each: KD <= 14 (ranks up to 57);
+//  * 16 warps, 1 CTA/SM, 512 columns, 2-deep ring of 16-j-tile stages: as far as the ring fits
+//    (ranks up to ~85).
 bool fits_tmem(int KD, int n_tail) {
-    if (KD > 14 || n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > kTmemCols) return false;
+    if (n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(8)) return false;
     const TmemShape sh = tmem_shape();
     const size_t jt = static_cast<size_t>(TileWide::JT) * sh.jps;
     const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
-    return 2 * (sizeof(double) * (32 + kTmemStgElems + sh.ns * stage) + 1024) <= kSmemPerSM;
+    return 2 * (sizeof(double) * (32 + tmem_stg_elems(8) + sh.ns * stage) + 1024) <= kSmemPerSM;
+}
+bool fits_tmem16(int KD, int n_tail) {
+    if (n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(16)) return false;
+    const size_t jt = TileTmem16::JT;
+    const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
+    return sizeof(double) * (32 + tmem_stg_elems(16) + TileTmem16::NS * stage) + 1024 <= kSmemPerSM;
 }
 
 template <class T>
@@ -522,11 +533,15 @@ bool plan_for(int KD, int n_tail, Plan& out) {
         int id, KC;
     };
     // Measured on B200 (tools/profile_expand.py, tools/profile_rank.py, tools/profile_rank_sweep.py):
-    // the TMEM plan for the BASELINE rank 41 (31.2 TF/s); plan 9 for ranks beyond it (cfg3 rank 328:
+    // the TMEM plan for the BASELINE rank 41 (31.2 TF/s); the 16-warp TMEM plan up to rank ~93
+    // (28-32 TF/s at 1024^2 x 512); plan 9 for ranks beyond it (cfg3 rank 328:
     // 31.3 TF/s, against 28.7 for the 8-warp plan 8 and 20.3 for the 4-warp plan 3; 16-warp tiles
     // with a 64-row i-chunk (29.0) or 16-row warp tiles (no fit) were slower).
-    const Cand cands[] = {{kPlanTmem, 0}, {0, 0}, {9, 4}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
-    for (const Cand& c : cands) {
+    // Up to KD 14 the 2-CTA TileWide with 8-k-step stages beats the 16-warp plan 9 (rank 46:
+    // 27.1 vs 22.0 TF/s); beyond it plan 9 wins (rank 123: 26.4 vs 24.2).
+    const Cand small_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {0, 0}, {0, 8}, {9, 4}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
+    const Cand large_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {0, 0}, {9, 4}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
+    for (const Cand& c : KD <= 14 ? small_r : large_r) {
         if (force >= 0 && c.id != force) continue;
         const int KC = c.KC == 0 ? KD : std::min(KD, c.KC);
         bool ok = false;
@@ -540,10 +555,20 @@ bool plan_for(int KD, int n_tail, Plan& out) {
             case 8: ok = fits<TileLR1b>(KD, KC, n_tail); ic = TileLR1b::IC; break;
             case 9: ok = fits<TileLR16>(KD, KC, n_tail); ic = TileLR16::IC; break;
             case kPlanTmem: ok = fits_tmem(KD, n_tail); ic = TileWide::IC; break;
+            // The 16-warp TMEM plan takes a 2-rank remainder as one more zero-padded k-step: at
+            // ranks 58-90 that beats plan 9 by 12-22% (tools/profile_rank_sweep.py, 512 slabs).
+            // For the 8-warp plan the padding costs what it gains (rank 42: 27.8 vs 28.6 TF/s
+            // for plan 0 with a 2-rank DFMA tail), so it keeps n_tail <= 1.
+            // Below KD 15 the 8-warp plans are faster (rank 42: 26.8 TF/s here vs 28.6 for plan 0).
+            case kPlanTmem16:
+                ok = KD + (n_tail == 2) > 14 && fits_tmem16(KD + (n_tail == 2), n_tail == 2 ? 0 : n_tail);
+                ic = TileTmem16::IC;
+                break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
         }
         if (ok) {
-            out = {c.id, KC, ic};
+            const int pad = c.id == kPlanTmem16 && n_tail == 2;
+            out = {c.id, KC + pad, ic, pad};
             if (const char* e = std::getenv("LS_EXPAND_KC")) out.KC = std::max(1, std::min(KD, std::atoi(e)));
             return true;
         }
@@ -569,8 +594,11 @@ int kernel_setup(const void* kern, int threads, size_t smem, int& per_sm) {
     }
     if (!configured[{kern, dev}]) {
         int optin = 0;
+        cudaFuncAttributes fa{};
         LS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+        LS_CUDA(cudaFuncGetAttributes(&fa, kern));
+        LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - static_cast<int>(fa.sharedSizeBytes)));
         LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared));
         configured[{kern, dev}] = true;
@@ -582,7 +610,7 @@ int kernel_setup(const void* kern, int threads, size_t smem, int& per_sm) {
 
 template <class T, bool STORE, bool FUNC, bool TMEM = false>
 int launch(ExpandArgs& a, cudaStream_t s) {
-    const TmemShape sh = TMEM ? tmem_shape() : TmemShape{T::NS, 1};
+    const TmemShape sh = TMEM ? (T::WARPS == 16 ? TmemShape{T::NS, 1} : tmem_shape()) : TmemShape{T::NS, 1};
     const int JT = T::JT * sh.jps, JC = T::JC * sh.jps;
     if (TMEM) a.KC = a.KD;
     a.n_ichunks = ls::ceil_div(a.N1, T::IC);
@@ -608,15 +636,18 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         a.N2 + JC >= (int64_t(1) << 31))
         return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
     const size_t smem =
-        TMEM ? sizeof(double) * (32 + kTmemStgElems + sh.ns * stage_elems) : smem_bytes<T>(a.KD, a.KC, a.n_tail);
+        TMEM ? sizeof(double) * (32 + tmem_stg_elems(T::WARPS) + sh.ns * stage_elems) : smem_bytes<T>(a.KD, a.KC, a.n_tail);
     void (*kern)(ExpandArgs) = expand_dmma_kernel<T, STORE, FUNC>;
     if constexpr (TMEM) {
         const int code = 10 * sh.ns + sh.jps;
-        if (code == 31) kern = expand_tmem_kernel<STORE, FUNC, 3, 1>;
-        else if (code == 41) kern = expand_tmem_kernel<STORE, FUNC, 4, 1>;
-        else if (code == 51) kern = expand_tmem_kernel<STORE, FUNC, 5, 1>;
-        else if (code == 22) kern = expand_tmem_kernel<STORE, FUNC, 2, 2>;
-        else return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
+        if constexpr (T::WARPS == 16) {
+            kern = expand_tmem_kernel<STORE, FUNC, T::NS, 1, 16>;
+        } else {
+            if (code == 31) kern = expand_tmem_kernel<STORE, FUNC, 3, 1>;
+            else if (code == 41) kern = expand_tmem_kernel<STORE, FUNC, 4, 1>;
+            else if (code == 22) kern = expand_tmem_kernel<STORE, FUNC, 2, 2>;
+            else return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
+        }
     }
     int per_sm = 0;
     if (const int rc = kernel_setup(reinterpret_cast<const void*>(kern), T::WARPS * 32, smem, per_sm)) return rc;
@@ -647,9 +678,14 @@ bool chunk_plan(Plan& out) {
 
 template <bool STORE, bool FUNC>
 int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
+    if (pl.pad && a.n_tail == 2) {
+        a.KD += 1;
+        a.n_tail = 0;
+    }
     a.KC = std::min(pl.KC, a.KD);
     switch (pl.id) {
         case kPlanTmem: return launch<TileWide, STORE, FUNC, true>(a, s);
+        case kPlanTmem16: return launch<TileTmem16, STORE, FUNC, true>(a, s);
         case 0: return launch<TileWide, STORE, FUNC>(a, s);
         case 1: return launch<TileWide3, STORE, FUNC>(a, s);
         case 2: return launch<TileMid, STORE, FUNC>(a, s);
@@ -672,7 +708,7 @@ extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_
     if (!plan_for(KD, n_tail, pl) && !chunk_plan(pl)) return -1;
     const int64_t IC = pl.ic;
     // the TMEM variant writes one partial per warp (no CTA barrier per unit)
-    return ls::ceil_div(N1, IC) * (k1 - k0) * (pl.id == kPlanTmem ? 8 : 1);
+    return ls::ceil_div(N1, IC) * (k1 - k0) * (pl.id == kPlanTmem ? 8 : pl.id == kPlanTmem16 ? 16 : 1);
 }
 
 extern "C" int ls_expand(const double* A_d, int64_t lda, const double* B_d, int64_t ldb,

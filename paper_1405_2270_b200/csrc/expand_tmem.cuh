@@ -60,9 +60,10 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 
 }  // namespace tmem
 
-constexpr int kTmemCols = 256;  // per CTA; two CTAs per SM use all 512 columns
+// TMEM columns per CTA: 8-warp CTAs run two per SM (256 columns each), 16-warp CTAs one (512).
+__host__ __device__ constexpr int tmem_cols(int warps) { return warps == 8 ? 256 : 512; }
 constexpr int kFillSlots = 9;   // per lane: up to 8 A1 values + the slab scale of one fill task
-constexpr int kTmemStgElems = 8 * kFillSlots * 32;  // per CTA (8 warps)
+__host__ __device__ constexpr int tmem_stg_elems(int warps) { return warps * kFillSlots * 32; }  // per CTA
 
 // 8-byte global->shared copy (LDGSTS); src_size 0 writes zeros without reading.
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
@@ -75,9 +76,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Requires: Tile geometry TileWide (8 warps, WI = 4, TM = TN = 4), whole rank in one stage
 // (n_kc == 1), KD <= 14, n_tail <= 1.
 // NS: ring depth; JPS: 64-column j-chunks per ring stage (each warp computes JPS tiles per stage).
-template <bool STORE, bool FUNC, int NS, int JPS>
-__global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p) {
-    constexpr int WARPS = 8, WI = 4, kTM = 4, kTN = 4, IC = 128, JT = 8 * JPS, JC = 64, kNS = NS;
+// WARPS = 8 (WJ = 2 warps along j, 2 CTAs/SM, ranks up to 57) or 16 (WJ = 4, 1 CTA/SM,
+// all 512 TMEM columns: ranks up to 121 as far as TMEM goes).
+template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8>
+__global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_kernel(const ExpandArgs p) {
+    constexpr int WARPS = WARPS_, WI = 4, WJ = WARPS / WI, kTM = 4, kTN = 4, IC = 128, JT = kTM * WJ * JPS,
+                  JC = 8 * kTM * WJ, kNS = NS;
+    constexpr int kTmemCols = tmem_cols(WARPS);
     constexpr int kThreads = WARPS * 32;
     const int KD = p.KD, n_tail = p.n_tail;
     const int CB = 8 * KD + 16 * n_tail;
@@ -97,7 +102,7 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
     uint64_t* as_empty = as_full + 2;                          // [2] A1k buffer released by every warp
     int* released = reinterpret_cast<int*>(smem + 16);         // [kNS] warps done with a ring slot
     uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 24);
-    double* ring = smem + 32 + kTmemStgElems;                   // [kNS][stage_elems]
+    double* ring = smem + 32 + tmem_stg_elems(WARPS);          // [kNS][stage_elems]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -142,9 +147,9 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
     const uint32_t tq = *tmem_base_s + (static_cast<uint32_t>(32 * wi) << 16);  // this warp's lane quarter
     double* stg = smem + 32 + warp * (kFillSlots * 32) + lane;  // this lane's fill staging slots (stride 32)
 
-    // Fill tasks of one unit for this warp: fragment k-steps ks = wj, wj+2, ... (4 values each),
+    // Fill tasks of one unit for this warp: fragment k-steps ks = wj, wj+WJ, ... (4 values each),
     // then (warp wj == 0 only) the tail ranks (8 values each).
-    const int n_frag_tasks = (KD - wj + 1) / 2;
+    const int n_frag_tasks = (KD - wj + WJ - 1) / WJ;
     const int n_tasks = n_frag_tasks + (wj == 0 ? n_tail : 0);
     // A fill task's operands are copied global->shared asynchronously one task ahead (the copy
     // for the following task is issued right after a task is consumed), so the L2 latency of the
@@ -153,7 +158,7 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
         const int ib = (u % n_ichunks) * IC;
         const int64_t k = p.k0 + u / n_ichunks;
         if (task < n_frag_tasks) {
-            const int ks = wj + 2 * task;
+            const int ks = wj + WJ * task;
             const int q = 4 * ks + t;
             cp_async8(stg + 8 * 32, p.S + k * p.R + (q < p.R ? q : 0), q < p.R);
 #pragma unroll
@@ -178,7 +183,7 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
         const double sv = stg[8 * 32];
         const uint32_t col = static_cast<uint32_t>(buf * CB);
         if (task < n_frag_tasks) {
-            const int ks = wj + 2 * task;
+            const int ks = wj + WJ * task;
             double v[4];
 #pragma unroll
             for (int it = 0; it < 4; ++it) v[it] = rn_mul(stg[it * 32], sv);  // Eigen's A1 * scale.asDiagonal()
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
                 const int task = t0 + b;
                 if (task >= n_tasks) break;
                 if (task < n_frag_tasks) {
-                    const int q = 4 * (wj + 2 * task) + t;
+                    const int q = 4 * (wj + WJ * task) + t;
                     sv[b] = q < p.R ? __ldg(p.S + k * p.R + q) : 0.0;
 #pragma unroll
                     for (int it = 0; it < 4; ++it) {
@@ -250,7 +255,7 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
                     double v[4];
 #pragma unroll
                     for (int it = 0; it < 4; ++it) v[it] = rn_mul(av[b][it], sv[b]);
-                    tmem::st_x8(tq + 8 * (wj + 2 * task), v);
+                    tmem::st_x8(tq + 8 * (wj + WJ * task), v);
                 } else {
                     const int qt = task - n_frag_tasks;
                     double v0[4], v1[4];
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(256, 2) expand_tmem_kernel(const ExpandArgs p)
             const double* stage = ring + slot * stage_elems;
 #pragma unroll 1
             for (int h = 0; h < JPS; ++h) {
-                const int jt0 = h * 8 + wj * kTM;  // first j-tile of this warp's tile in the stage
+                const int jt0 = h * (kTM * WJ) + wj * kTM;  // first j-tile of this warp's tile in the stage
 #pragma unroll
                 for (int m = 0; m < kTM; ++m)
 #pragma unroll
