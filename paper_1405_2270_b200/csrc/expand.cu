@@ -507,13 +507,18 @@ inline TmemShape tmem_shape() {
 //  * 8 warps, 2 CTAs/SM, 256 columns each: KD <= 14 (ranks up to 57);
 //  * 16 warps, 1 CTA/SM, 512 columns, 2-deep ring of 16-j-tile stages: as far as the ring fits
 //    (ranks up to ~85).
-bool fits_tmem(int KD, int n_tail) {
+bool fits_tmem_shape(int KD, int n_tail, TmemShape sh) {
     if (n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(8)) return false;
-    const TmemShape sh = tmem_shape();
     const size_t jt = static_cast<size_t>(TileWide::JT) * sh.jps;
     const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
     return 2 * (sizeof(double) * (32 + tmem_stg_elems(8) + sh.ns * stage) + 1024) <= kSmemPerSM;
 }
+// Ring depth 4 where it fits (ranks up to 45), else 3 (up to 57); LS_EXPAND_TMEM overrides.
+TmemShape tmem_shape_for(int KD, int n_tail) {
+    if (std::getenv("LS_EXPAND_TMEM")) return tmem_shape();
+    return fits_tmem_shape(KD, n_tail, {4, 1}) ? TmemShape{4, 1} : TmemShape{3, 1};
+}
+bool fits_tmem(int KD, int n_tail) { return fits_tmem_shape(KD, n_tail, tmem_shape_for(KD, n_tail)); }
 bool fits_tmem16(int KD, int n_tail) {
     if (n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(16)) return false;
     const size_t jt = TileTmem16::JT;
@@ -610,7 +615,8 @@ int kernel_setup(const void* kern, int threads, size_t smem, int& per_sm) {
 
 template <class T, bool STORE, bool FUNC, bool TMEM = false>
 int launch(ExpandArgs& a, cudaStream_t s) {
-    const TmemShape sh = TMEM ? (T::WARPS == 16 ? TmemShape{T::NS, 1} : tmem_shape()) : TmemShape{T::NS, 1};
+    const TmemShape sh =
+        TMEM ? (T::WARPS == 16 ? TmemShape{T::NS, 1} : tmem_shape_for(a.KD, a.n_tail)) : TmemShape{T::NS, 1};
     const int JT = T::JT * sh.jps, JC = T::JC * sh.jps;
     if (TMEM) a.KC = a.KD;
     a.n_ichunks = ls::ceil_div(a.N1, T::IC);
