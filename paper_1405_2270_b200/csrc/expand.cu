@@ -156,7 +156,7 @@ __global__ void pack_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t
             const int qt = static_cast<int>((r / 8) % n_tail);
             const int jt = static_cast<int>(r / (8 * n_tail));
             const int64_t j = (jc * JT + jt) * 8 + g;
-            if (j < N2) v = B[j + ldb * (4 * KD + qt)];
+            if (j < N2 && 4 * KD + qt < R) v = B[j + ldb * (4 * KD + qt)];
         }
         Bp[e] = v;
     }
@@ -507,7 +507,13 @@ inline TmemShape tmem_shape() {
 //  * 8 warps, 2 CTAs/SM, 256 columns each: KD <= 14 (ranks up to 57);
 //  * 16 warps, 1 CTA/SM, 512 columns, 2-deep ring of 16-j-tile stages: as far as the ring fits
 //    (ranks up to ~85).
+// The TMEM kernel always runs one DFMA rank per tile: a zero rank when R mod 4 is 0 or 3.
+// Measured: rank 40 took 1.514 ms and rank 41 (with its real DFMA rank) 1.438 ms at
+// 1024^2 x 512 slabs; with the zero rank rank 40 runs like rank 41. The same holds at ranks
+// 44/45 and 48/49.
+inline int tmem_tail(int n_tail) { return n_tail == 0 ? 1 : n_tail; }
 bool fits_tmem_shape(int KD, int n_tail, TmemShape sh) {
+    n_tail = tmem_tail(n_tail);
     if (n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(8)) return false;
     const size_t jt = static_cast<size_t>(TileWide::JT) * sh.jps;
     const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
@@ -520,6 +526,7 @@ TmemShape tmem_shape_for(int KD, int n_tail) {
 }
 bool fits_tmem(int KD, int n_tail) { return fits_tmem_shape(KD, n_tail, tmem_shape_for(KD, n_tail)); }
 bool fits_tmem16(int KD, int n_tail) {
+    n_tail = tmem_tail(n_tail);
     if (n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(16)) return false;
     const size_t jt = TileTmem16::JT;
     const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
@@ -618,7 +625,10 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     const TmemShape sh =
         TMEM ? (T::WARPS == 16 ? TmemShape{T::NS, 1} : tmem_shape_for(a.KD, a.n_tail)) : TmemShape{T::NS, 1};
     const int JT = T::JT * sh.jps, JC = T::JC * sh.jps;
-    if (TMEM) a.KC = a.KD;
+    if (TMEM) {
+        a.KC = a.KD;
+        a.n_tail = tmem_tail(a.n_tail);
+    }
     a.n_ichunks = ls::ceil_div(a.N1, T::IC);
     a.n_units = a.n_ichunks * (a.k1 - a.k0);
     a.n_jc = ls::ceil_div(a.N2, JC);

@@ -168,12 +168,13 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 cp_async8(stg + it * 32, ok ? p.A + i + p.lda * q : p.A, ok);
             }
         } else {
-            const int q = 4 * KD + (task - n_frag_tasks);
-            cp_async8(stg + 8 * 32, p.S + k * p.R + q, true);
+            const int q = 4 * KD + (task - n_frag_tasks);  // q >= R: the zero rank (see below)
+            cp_async8(stg + 8 * 32, q < p.R ? p.S + k * p.R + q : p.S, q < p.R);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const int i = ib + 32 * wi + 8 * (e >> 1) + 2 * t + (e & 1);
-                cp_async8(stg + e * 32, i < p.N1 ? p.A + i + p.lda * q : p.A, i < p.N1);
+                const bool ok = i < p.N1 && q < p.R;
+                cp_async8(stg + e * 32, ok ? p.A + i + p.lda * q : p.A, ok);
             }
         }
         cp_async_commit();
@@ -239,11 +240,11 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                     }
                 } else {
                     const int q = 4 * KD + (task - n_frag_tasks);
-                    sv[b] = __ldg(p.S + k * p.R + q);
+                    sv[b] = q < p.R ? __ldg(p.S + k * p.R + q) : 0.0;
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         const int i = ib + 32 * wi + 8 * (e >> 1) + 2 * t + (e & 1);
-                        av[b][e] = i < p.N1 ? __ldg(p.A + i + p.lda * q) : 0.0;
+                        av[b][e] = (i < p.N1 && q < p.R) ? __ldg(p.A + i + p.lda * q) : 0.0;
                     }
                 }
             }

@@ -182,7 +182,7 @@ def test_assembly_rejects_mismatched_master(L):  # test_lattice.cpp:196-203
 @pytest.mark.parametrize("dims,R", [((5, 7, 3), 3), ((33, 17, 9), 41), ((130, 66, 4), 45), ((64, 64, 4), 328),
                                     ((2, 2, 2), 1), ((257, 129, 3), 8), ((4, 5, 6), 2), ((200, 3, 2), 43),
                                     ((1, 9, 2), 5), ((130, 66, 4), 61), ((257, 129, 3), 82), ((64, 200, 5), 73),
-                                    ((70, 33, 3), 42), ((129, 64, 2), 90)])
+                                    ((70, 33, 3), 42), ((129, 64, 2), 90), ((100, 70, 3), 40), ((33, 129, 4), 44)])
 def test_expansion_matches_oracle_random(L, orc, dims, R):  # test_canonical.cpp:63-69
     rng = np.random.default_rng(R * 1000 + dims[0])
     f = [np.asfortranarray(rng.uniform(-1, 1, (d, R))) for d in dims]
