@@ -18,8 +18,17 @@
 
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 16, PITCH = BK + 4, NSTAGE = 3;  // pitch 20: conflict-free LDS.64
-constexpr int kThreads = 256;
+// Build-time tile knobs (tools/lab/build_variants.sh with SRC=grid_batch). Measured at cfg4:
+// BN 64 x 3 stages 1.48 ms; BN 128 (16 warps, 1 CTA/SM) with 2/3/4 stages 1.59/1.57/1.56 ms.
+#ifndef GB_BN
+#define GB_BN 64
+#endif
+#ifndef GB_NS
+#define GB_NS 3
+#endif
+constexpr int BM = 128, BN = GB_BN, BK = 16, PITCH = BK + 4, NSTAGE = GB_NS;  // pitch 20: conflict-free LDS.64
+constexpr int kThreads = 32 * 4 * (BN / 32);  // 4 warps along m x BN/32 along f
+constexpr int kMinBlocks = kThreads == 256 ? 2 : 1;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -50,7 +59,7 @@ struct GridBatchArgs {
 
 // VEC: 16-byte copies (V, X 16-byte aligned, even strides); otherwise 8-byte copies.
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads, 2) grid_batch_kernel(const GridBatchArgs p) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) grid_batch_kernel(const GridBatchArgs p) {
     extern __shared__ __align__(16) double sm[];
     double* As = sm;                           // [NSTAGE][BM][PITCH]
     double* Bs = sm + NSTAGE * BM * PITCH;     // [NSTAGE][BN][PITCH]

@@ -6,18 +6,19 @@ set -e
 ROOT=/root/repo
 PKG=$ROOT/paper_1405_2270_b200
 ARCH="-gencode arch=compute_100a,code=sm_100a"
-OTHERS=$(ls $ROOT/build/obj/*.o | grep -v '/expand.o$')
+SRC=${SRC:-expand}  # which csrc/<SRC>.cu the flags apply to
+OTHERS=$(ls $ROOT/build/obj/*.o | grep -v "/$SRC.o$")
 for spec in "$@"; do
   name=${spec%%:*}; flags=${spec#*:}
   d=$ROOT/lab_build/$name/paper_1405_2270_b200
   mkdir -p $d
   cp $PKG/*.py $d/
-  nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include $flags -c $PKG/csrc/expand.cu -o $d/expand.o &
+  nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include $flags -c $PKG/csrc/$SRC.cu -o $d/$SRC.o &
 done
 wait
 for spec in "$@"; do
   name=${spec%%:*}
   d=$ROOT/lab_build/$name/paper_1405_2270_b200
-  nvcc $ARCH -shared -o $d/liblatsum_cuda.so $d/expand.o $OTHERS -lcudart
-  rm $d/expand.o
+  nvcc $ARCH -shared -o $d/liblatsum_cuda.so $d/$SRC.o $OTHERS -lcudart
+  rm $d/$SRC.o
 done
