@@ -378,6 +378,36 @@ def test_cfg4_grid_functional_batch_matches_1d_form(L):
     assert np.array_equal(full, again)  # fixed-order reductions: bitwise run to run
 
 
+@pytest.mark.parametrize("charges,periodic", [
+    (((0.0, 0.0, 0.0, 1.0), (1.25, -0.625, 2.5, 2.0)), False),                       # rank 82: 16-warp TMEM plan
+    (((0.0, 0.0, 0.0, 1.0), (1.25, -0.625, 2.5, 2.0), (-2.5, 1.25, 0.3125, 3.0)), True),  # rank 123: smem plan 9
+])
+def test_fused_energy_matches_1d_form_multi_charge(L, charges, periodic):
+    """The fused full-grid <V, rho> (per-warp or per-unit partials, fixed-order sum) against the 1D
+    rank-term form, on multi-charge lattices whose ranks take the other expansion plans."""
+    import torch
+    spec, rule = cfg(L, 4, charges=charges)
+    pipe = L.DevicePipeline(spec, rule, mode="erf", periodic=periodic)
+    pipe.generate()
+    pipe.assemble()
+    N = pipe.dims
+    rho = []
+    for l in range(3):
+        x = (np.arange(N[l]) + 0.5 - N[l] / 2) * spec.unit.h
+        rho.append(torch.as_tensor(np.exp(-x * x / (2.0 + l)), device="cuda"))
+    e = float(pipe.grid_functional(rho).cpu())
+    one_d = L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w,
+                                                    [r.reshape(-1, 1) for r in rho]).cpu().numpy()[0]
+    assert abs(e - one_d) <= 1e-12 * abs(one_d)
+    # and the stored grid contracted on the host agrees
+    out = torch.empty((N[2], N[1], N[0]), dtype=torch.float64, device="cuda")
+    pipe.expand(out)
+    V = out.cpu().numpy()
+    r = [x.cpu().numpy() for x in rho]
+    host = float(np.einsum("kji,i,j,k->", V, r[0], r[1], r[2]))
+    assert abs(host - one_d) <= 1e-12 * abs(one_d)
+
+
 def test_eval_points_and_scalar_product(L, orc):  # test_canonical.cpp:88-139
     rng = np.random.default_rng(9)
     f = [np.asfortranarray(rng.uniform(-1, 1, (d, 3))) for d in (4, 5, 6)]
