@@ -16,21 +16,24 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--slabs", type=int, default=64)
 ap.add_argument("--ranks", default="60,82,123,164,246,328")
+ap.add_argument("--n1", type=int, default=0, help="rows along i (default --n)")
+ap.add_argument("--n2", type=int, default=0, help="rows along j (default --n)")
 args = ap.parse_args()
 n, ks = args.n, args.slabs
-out = torch.empty((ks, n, n), dtype=torch.float64, device="cuda")
+n1, n2 = args.n1 or n, args.n2 or n
+out = torch.empty((ks, n2, n1), dtype=torch.float64, device="cuda")
 g = torch.Generator(device="cuda").manual_seed(1)
 for R in map(int, args.ranks.split(",")):
-    fac = [torch.rand((R, n), dtype=torch.float64, device="cuda", generator=g) for _ in range(3)]
+    fac = [torch.rand((R, m), dtype=torch.float64, device="cuda", generator=g) for m in (n1, n2, max(ks, 1))]
     w = torch.rand(R, dtype=torch.float64, device="cuda", generator=g)
-    _expand_device(fac, w, (n, n, n), 0, ks, out)
+    _expand_device(fac, w, (n1, n2, ks), 0, ks, out)
     torch.cuda.synchronize()
     best = 1e9
     for _ in range(3):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         e[0].record()
-        _expand_device(fac, w, (n, n, n), 0, ks, out)
+        _expand_device(fac, w, (n1, n2, ks), 0, ks, out)
         e[1].record()
         torch.cuda.synchronize()
         best = min(best, e[0].elapsed_time(e[1]))
-    print(f"R={R:4d}: {best:.3f} ms, {2.0 * R * n * n * ks / best / 1e9:.2f} TF/s")
+    print(f"{n1}x{n2}x{ks} R={R:4d}: {best:.3f} ms, {2.0 * R * n1 * n2 * ks / best / 1e9:.2f} TF/s")
