@@ -3,8 +3,8 @@
 //
 // The shared-memory variant (expand_dmma_kernel) must stop every warp of the CTA at each
 // unit boundary: one barrier before A1k of the next slab overwrites the current one, one
-// after the fill. Here A1k lives in TMEM (256 of 512 columns per CTA, otherwise unused by
-// an FP64 kernel): two buffers, so the warps fill unit u+1's A1k piece by piece while they
+// after the fill. Here A1k lives in TMEM (256 of 512 columns per 8-warp CTA, all 512 for the
+// 16-warp shape; otherwise unused by an FP64 kernel): two buffers, so the warps fill unit u+1's A1k piece by piece while they
 // multiply unit u, and units hand over through mbarriers (as_full / as_empty) instead of
 // CTA barriers. Shared memory then holds the TMA ring of A2 stages and a small per-warp
 // staging area through which the next fill task's A1/S operands arrive by cp.async.
@@ -13,7 +13,8 @@
 //   buffer b, column b*CB + ks*8 + it*2 + {0,1}: A1k(8*(4*wi + it) + g, 4*ks + t) (lo, hi words)
 //   buffer b, column b*CB + 8*KD + qt*16 + n*4 + {0..3}: the two tail-rank values lane (g, t)
 //   needs for i-tile n: A1k(32*wi + 8n + 2t + {0,1}, 4*KD + qt)
-// CB = 8*KD + 16*n_tail columns, so KD <= 14 fits two buffers in 256 columns.
+// CB = 8*KD + 16*n_tail columns: KD <= 14 fits two buffers in 256 columns, KD <= 30 in 512.
+// n_tail is always 1 here (a zero rank when R mod 4 is 0 or 3; see tmem_tail in expand.cu).
 #pragma once
 
 namespace tmem {
@@ -73,11 +74,11 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Requires: Tile geometry TileWide (8 warps, WI = 4, TM = TN = 4), whole rank in one stage
-// (n_kc == 1), KD <= 14, n_tail <= 1.
-// NS: ring depth; JPS: 64-column j-chunks per ring stage (each warp computes JPS tiles per stage).
-// WARPS = 8 (WJ = 2 warps along j, 2 CTAs/SM, ranks up to 57) or 16 (WJ = 4, 1 CTA/SM,
-// all 512 TMEM columns: ranks up to 121 as far as TMEM goes).
+// Requires: 32x32 warp tiles (TM = TN = 4), WI = 4 warps along i (one per TMEM lane quarter),
+// whole rank in one stage (n_kc == 1), n_tail == 1.
+// NS: ring depth; JPS: j-chunks per ring stage (each warp computes JPS tiles per stage).
+// WARPS = 8 (WJ = 2 warps along j, 2 CTAs/SM, KD <= 14) or 16 (WJ = 4, 1 CTA/SM, all 512 TMEM
+// columns; the shared-memory ring limits it to KD <= 23, i.e. ranks up to 93).
 template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8>
 __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_kernel(const ExpandArgs p) {
     constexpr int WARPS = WARPS_, WI = 4, WJ = WARPS / WI, kTM = 4, kTN = 4, IC = 128, JT = kTM * WJ * JPS,
