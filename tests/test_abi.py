@@ -72,6 +72,25 @@ def test_device_entry_points_validate_before_device_work():
                                         None) == _abi.LS_EVALIDATION
 
 
+def test_device_work_without_a_gpu_fails_loudly():
+    """No CPU fallback: a valid call that needs the device returns LS_ECUDA (the headers throw
+    device_error, the Python mirror raises CudaError) when no CUDA device is usable."""
+    import ctypes as C
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    lib = _abi.load()
+    dims = np.array([2, 2, 2], dtype=np.int64)
+    f, w = np.ones((2, 1)), np.ones(1)
+    idx, out = np.zeros(3, dtype=np.int64), np.zeros(1)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    assert lib.ls_h_eval_points(p(dims), 1, p(f), p(f), p(f), p(w), p(idx), 1, p(out)) == _abi.LS_ECUDA
+    assert lib.ls_last_error()
+    import paper_1405_2270_b200 as L
+    with pytest.raises(L.CudaError):
+        L.densify(L.CanonicalTensor3([np.ones((2, 1))] * 3, np.ones(1)))
+
+
 def test_python_mirror_validation():  # lattice.hpp:57-68, grid.hpp:21-27, canonical.hpp:42-56
     with pytest.raises(L.ValidationError):
         L.GridSpec(2.0, 3)
