@@ -429,6 +429,8 @@ def run_e2e(L, spec, rule, k0, k1, args, world, dev):
     del host, buf
     return {"value": round(pts / (el / steps) / 1e9, 4), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps,
+            "d2h_gbs": round(d2h / (el / steps) / 1e9, 1),
+            "bound": "PCIe device-to-host (the 8 B/point grid leaves the GPU every step)",
             "api": "ls_h_lattice_potential (host tau/w/charges in; full grid out to "
                    f"{'pinned' if pinned else 'pageable'} host memory)"}
 
