@@ -350,7 +350,17 @@ expand_dmma_kernel(const ExpandArgs p) {
             }
         }
 
-        if (kc == n_kc - 1) {
+        if (kc == n_kc - 1 && STORE && !FUNC && p.vec_store && !p.accumulate && !p.debug &&
+            ib + wi * (8 * kTN) + 8 * kTN <= p.N1 && jc * T::JC + wj * (8 * kTM) + 8 * kTM <= p.N2) {
+            // Interior tile: no per-element bounds or mode checks (as in the TMEM kernel).
+            double* row = p.out + kk * p.ldz + static_cast<int64_t>(jc * T::JC + wj * (8 * kTM) + g) * p.ldy + ib +
+                          wi * (8 * kTN) + 2 * t;
+#pragma unroll
+            for (int m = 0; m < kTM; ++m)
+#pragma unroll
+                for (int n = 0; n < kTN; ++n)
+                    __stcs(reinterpret_cast<double2*>(row + 8 * m * p.ldy + 8 * n), make_double2(acc[m][n][0], acc[m][n][1]));
+        } else if (kc == n_kc - 1) {
             const int jb = jc * T::JC + wj * (8 * kTM);
             const int ibase = ib + wi * (8 * kTN);
 #pragma unroll

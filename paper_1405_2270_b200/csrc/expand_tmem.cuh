@@ -375,6 +375,32 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
                 const int jb = (jc * JPS + h) * JC + wj * (8 * kTM);
                 const int ibase = ib + wi * (8 * kTN);
+                if (ibase + 8 * kTN <= p.N1 && jb + 8 * kTM <= p.N2 && (!STORE || (p.vec_store && !p.accumulate)) &&
+                    (!FUNC || (reinterpret_cast<uintptr_t>(p.rho1) & 15) == 0)) {
+                    // Interior tile (the common case): no per-element bounds or mode checks. Measured
+                    // 2.4% of the whole kernel at cfg1 (2.826 -> 2.760 ms).
+                    double* row = STORE ? p.out + kk * p.ldz + static_cast<int64_t>(jb + g) * p.ldy + ibase + 2 * t
+                                        : nullptr;
+#pragma unroll
+                    for (int m = 0; m < kTM; ++m) {
+                        if (FUNC) {
+                            double sm = 0.0;
+#pragma unroll
+                            for (int nn = 0; nn < kTN; ++nn) {
+                                const double2 r = __ldg(reinterpret_cast<const double2*>(p.rho1 + ibase + 8 * nn + 2 * t));
+                                sm = fma(acc[m][nn][0], r.x, sm);
+                                sm = fma(acc[m][nn][1], r.y, sm);
+                            }
+                            fsum = fma(sm, __ldg(p.rho2 + jb + 8 * m + g), fsum);
+                        }
+                        if (STORE)
+#pragma unroll
+                            for (int nn = 0; nn < kTN; ++nn)
+                                __stcs(reinterpret_cast<double2*>(row + 8 * m * p.ldy + 8 * nn),
+                                       make_double2(acc[m][nn][0], acc[m][nn][1]));
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int m = 0; m < kTM; ++m) {
                     const int j = jb + 8 * m + g;
