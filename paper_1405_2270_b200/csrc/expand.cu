@@ -40,6 +40,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <utility>
 
 #include "common.cuh"
 
@@ -630,6 +631,29 @@ int kernel_setup(const void* kern, int threads, size_t smem, int& per_sm) {
     return LS_OK;
 }
 
+// The 8-warp TMEM kernel for ring shape `code` (10 * depth + j-chunks per stage) with the
+// k-step count fixed at compile time for KD 1..14 (depth 4 up to KD 11, 3 beyond, as
+// tmem_shape_for picks them); other shapes (LS_EXPAND_TMEM) take the runtime-KD kernel.
+template <bool STORE, bool FUNC, int NS, int... KD>
+void (*tmem8_pick(int kd, std::integer_sequence<int, KD...>))(ExpandArgs) {
+    void (*k)(ExpandArgs) = nullptr;
+    ((kd == KD + 1 ? (k = expand_tmem_kernel<STORE, FUNC, NS, 1, 8, KD + 1>, 0) : 0), ...);
+    return k;
+}
+template <bool STORE, bool FUNC>
+void (*tmem8_kernel(int code, int kd))(ExpandArgs) {
+    if (code == 41 && kd <= 11) return tmem8_pick<STORE, FUNC, 4>(kd, std::make_integer_sequence<int, 11>{});
+    if (code == 31 && kd >= 12 && kd <= 14) {
+        if (kd == 12) return expand_tmem_kernel<STORE, FUNC, 3, 1, 8, 12>;
+        if (kd == 13) return expand_tmem_kernel<STORE, FUNC, 3, 1, 8, 13>;
+        return expand_tmem_kernel<STORE, FUNC, 3, 1, 8, 14>;
+    }
+    if (code == 41) return expand_tmem_kernel<STORE, FUNC, 4, 1>;
+    if (code == 31) return expand_tmem_kernel<STORE, FUNC, 3, 1>;
+    if (code == 22) return expand_tmem_kernel<STORE, FUNC, 2, 2>;
+    return nullptr;
+}
+
 template <class T, bool STORE, bool FUNC, bool TMEM = false>
 int launch(ExpandArgs& a, cudaStream_t s) {
     const TmemShape sh =
@@ -663,16 +687,17 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
     const size_t smem =
         TMEM ? sizeof(double) * (32 + tmem_stg_elems(T::WARPS) + sh.ns * stage_elems) : smem_bytes<T>(a.KD, a.KC, a.n_tail);
-    void (*kern)(ExpandArgs) = expand_dmma_kernel<T, STORE, FUNC>;
-    if constexpr (TMEM) {
+    void (*kern)(ExpandArgs) = nullptr;
+    if constexpr (!TMEM) {
+        kern = expand_dmma_kernel<T, STORE, FUNC>;
+    } else {
         const int code = 10 * sh.ns + sh.jps;
+        if (a.n_tail != 1) return ls::fail(LS_EVALIDATION, "expand: TMEM plan needs exactly one DFMA rank");
         if constexpr (T::WARPS == 16) {
             kern = expand_tmem_kernel<STORE, FUNC, T::NS, 1, 16>;
         } else {
-            if (code == 31) kern = expand_tmem_kernel<STORE, FUNC, 3, 1>;
-            else if (code == 41) kern = expand_tmem_kernel<STORE, FUNC, 4, 1>;
-            else if (code == 22) kern = expand_tmem_kernel<STORE, FUNC, 2, 2>;
-            else return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
+            kern = tmem8_kernel<STORE, FUNC>(code, a.KD);
+            if (!kern) return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
         }
     }
     int per_sm = 0;

@@ -79,13 +79,17 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // NS: ring depth; JPS: j-chunks per ring stage (each warp computes JPS tiles per stage).
 // WARPS = 8 (WJ = 2 warps along j, 2 CTAs/SM, KD <= 14) or 16 (WJ = 4, 1 CTA/SM, all 512 TMEM
 // columns; the shared-memory ring limits it to KD <= 23, i.e. ranks up to 93).
-template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8>
+// KD_ > 0 fixes the k-step count at compile time (the 8-warp shape is instantiated for every
+// KD it covers): the k-step loop is then fully unrolled with immediate shared-memory and TMEM
+// offsets, 2.2% faster at cfg1 than the runtime-KD loop. KD_ = 0 reads p.KD.
+template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8, int KD_ = 0>
 __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_kernel(const ExpandArgs p) {
     constexpr int WARPS = WARPS_, WI = 4, WJ = WARPS / WI, kTM = 4, kTN = 4, IC = 128, JT = kTM * WJ * JPS,
                   JC = 8 * kTM * WJ, kNS = NS;
     constexpr int kTmemCols = tmem_cols(WARPS);
     constexpr int kThreads = WARPS * 32;
-    const int KD = p.KD, n_tail = p.n_tail;
+    const int KD = KD_ > 0 ? KD_ : p.KD;
+    constexpr int n_tail = 1;  // always one DFMA rank (launch() makes a zero rank when needed)
     const int CB = 8 * KD + 16 * n_tail;
     const int frag_elems = JT * KD * 32;
     const int stage_elems = frag_elems + JT * 8 * n_tail;
