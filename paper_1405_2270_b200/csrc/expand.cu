@@ -640,6 +640,18 @@ void (*tmem8_pick(int kd, std::integer_sequence<int, KD...>))(ExpandArgs) {
     ((kd == KD + 1 ? (k = expand_tmem_kernel<STORE, FUNC, NS, 1, 8, KD + 1>, 0) : 0), ...);
     return k;
 }
+// The 16-warp shape, compile-time KD over the range it is planned for (15..23).
+template <bool STORE, bool FUNC, int NS, int... KD>
+void (*tmem16_pick(int kd, std::integer_sequence<int, KD...>))(ExpandArgs) {
+    void (*k)(ExpandArgs) = nullptr;
+    ((kd == KD + 15 ? (k = expand_tmem_kernel<STORE, FUNC, NS, 1, 16, KD + 15>, 0) : 0), ...);
+    return k;
+}
+template <bool STORE, bool FUNC, int NS>
+void (*tmem16_kernel(int kd))(ExpandArgs) {
+    if (auto k = tmem16_pick<STORE, FUNC, NS>(kd, std::make_integer_sequence<int, 9>{})) return k;
+    return expand_tmem_kernel<STORE, FUNC, NS, 1, 16>;
+}
 template <bool STORE, bool FUNC>
 void (*tmem8_kernel(int code, int kd))(ExpandArgs) {
     if (code == 41 && kd <= 11) return tmem8_pick<STORE, FUNC, 4>(kd, std::make_integer_sequence<int, 11>{});
@@ -694,7 +706,7 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         const int code = 10 * sh.ns + sh.jps;
         if (a.n_tail != 1) return ls::fail(LS_EVALIDATION, "expand: TMEM plan needs exactly one DFMA rank");
         if constexpr (T::WARPS == 16) {
-            kern = expand_tmem_kernel<STORE, FUNC, T::NS, 1, 16>;
+            kern = tmem16_kernel<STORE, FUNC, T::NS>(a.KD);
         } else {
             kern = tmem8_kernel<STORE, FUNC>(code, a.KD);
             if (!kern) return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
