@@ -523,9 +523,10 @@ inline TmemShape tmem_shape() {
 // 1024^2 x 512 slabs; with the zero rank rank 40 runs like rank 41. The same holds at ranks
 // 44/45 and 48/49.
 inline int tmem_tail(int n_tail) { return n_tail == 0 ? 1 : n_tail; }
+// The 8-warp shape also takes a 2-rank remainder as two DFMA ranks (the 16-warp one pads it).
 bool fits_tmem_shape(int KD, int n_tail, TmemShape sh) {
     n_tail = tmem_tail(n_tail);
-    if (n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(8)) return false;
+    if (n_tail > 2 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(8)) return false;
     const size_t jt = static_cast<size_t>(TileWide::JT) * sh.jps;
     const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
     return 2 * (sizeof(double) * (32 + tmem_stg_elems(8) + sh.ns * stage) + 1024) <= kSmemPerSM;
@@ -652,6 +653,13 @@ void (*tmem16_kernel(int kd))(ExpandArgs) {
     if (auto k = tmem16_pick<STORE, FUNC, NS>(kd, std::make_integer_sequence<int, 9>{})) return k;
     return expand_tmem_kernel<STORE, FUNC, NS, 1, 16>;
 }
+// Two DFMA ranks (R mod 4 = 2): runtime KD.
+template <bool STORE, bool FUNC>
+void (*tmem8_kernel_t2(int code))(ExpandArgs) {
+    if (code == 41) return expand_tmem_kernel<STORE, FUNC, 4, 1, 8, 0, 2>;
+    if (code == 31) return expand_tmem_kernel<STORE, FUNC, 3, 1, 8, 0, 2>;
+    return nullptr;
+}
 template <bool STORE, bool FUNC>
 void (*tmem8_kernel(int code, int kd))(ExpandArgs) {
     if (code == 41 && kd <= 11) return tmem8_pick<STORE, FUNC, 4>(kd, std::make_integer_sequence<int, 11>{});
@@ -704,11 +712,12 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         kern = expand_dmma_kernel<T, STORE, FUNC>;
     } else {
         const int code = 10 * sh.ns + sh.jps;
-        if (a.n_tail != 1) return ls::fail(LS_EVALIDATION, "expand: TMEM plan needs exactly one DFMA rank");
+        if (a.n_tail != 1 && !(a.n_tail == 2 && T::WARPS == 8))
+            return ls::fail(LS_EVALIDATION, "expand: TMEM plan needs one DFMA rank (two with 8 warps)");
         if constexpr (T::WARPS == 16) {
             kern = tmem16_kernel<STORE, FUNC, T::NS>(a.KD);
         } else {
-            kern = tmem8_kernel<STORE, FUNC>(code, a.KD);
+            kern = a.n_tail == 2 ? tmem8_kernel_t2<STORE, FUNC>(code) : tmem8_kernel<STORE, FUNC>(code, a.KD);
             if (!kern) return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
         }
     }

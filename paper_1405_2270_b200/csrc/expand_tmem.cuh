@@ -82,14 +82,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // KD_ > 0 fixes the k-step count at compile time (the 8-warp shape is instantiated for every
 // KD it covers): the k-step loop is then fully unrolled with immediate shared-memory and TMEM
 // offsets, 2.2% faster at cfg1 than the runtime-KD loop. KD_ = 0 reads p.KD.
-template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8, int KD_ = 0>
+template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8, int KD_ = 0, int NT_ = 1>
 __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_kernel(const ExpandArgs p) {
     constexpr int WARPS = WARPS_, WI = 4, WJ = WARPS / WI, kTM = 4, kTN = 4, IC = 128, JT = kTM * WJ * JPS,
                   JC = 8 * kTM * WJ, kNS = NS;
     constexpr int kTmemCols = tmem_cols(WARPS);
     constexpr int kThreads = WARPS * 32;
     const int KD = KD_ > 0 ? KD_ : p.KD;
-    constexpr int n_tail = 1;  // always one DFMA rank (launch() makes a zero rank when needed)
+    constexpr int n_tail = NT_;  // 1 or 2 DFMA ranks (launch() makes a zero rank when R mod 4 is 0 or 3)
     const int CB = 8 * KD + 16 * n_tail;
     const int frag_elems = JT * KD * 32;
     const int stage_elems = frag_elems + JT * 8 * n_tail;
@@ -319,17 +319,18 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 for (int m = 0; m < kTM; ++m)
 #pragma unroll
                     for (int nn = 0; nn < kTN; ++nn) acc[m][nn][0] = acc[m][nn][1] = 0.0;
-                if (n_tail) {
-                    // Rank remainder (R mod 4 = 1) on DFMA before the DMMAs. (Placing it after the
+#pragma unroll
+                for (int qt = 0; qt < n_tail; ++qt) {
+                    // Rank remainder (R mod 4) on DFMA before the DMMAs. (Placing it after the
                     // DMMA loop, where it would overlap the accumulator drain, measured 12% slower:
                     // it then lengthens the exposed drain before the epilogue.)
-                    const double* tbp = stage + frag_elems + jt0 * 8 + g;
+                    const double* tbp = stage + frag_elems + jt0 * 8 * n_tail + qt * 8 + g;
                     double bt[kTM];
 #pragma unroll
-                    for (int m = 0; m < kTM; ++m) bt[m] = tbp[m * 8];
+                    for (int m = 0; m < kTM; ++m) bt[m] = tbp[m * 8 * n_tail];
                     double at0[4], at1[4];
-                    tmem::ld_x8(tb + 8 * KD, at0);
-                    tmem::ld_x8(tb + 8 * KD + 8, at1);
+                    tmem::ld_x8(tb + 8 * KD + 16 * qt, at0);
+                    tmem::ld_x8(tb + 8 * KD + 16 * qt + 8, at1);
                     const double atx[8] = {at0[0], at0[1], at0[2], at0[3], at1[0], at1[1], at1[2], at1[3]};
 #pragma unroll
                     for (int nn = 0; nn < kTN; ++nn)
