@@ -43,76 +43,12 @@
 #include <utility>
 
 #include "common.cuh"
+#include "k3.cuh"
 
 namespace {
 
+using namespace ls_k3;
 
-struct ExpandArgs {
-    const double* A;
-    const double* B;
-    const double* Bp;   // A2 packed per stage (see pack_b_kernel)
-    const double* C;
-    const double* w;
-    int64_t lda, ldb, ldc;
-    int64_t N1, N2, N3;
-    int R;            // rank
-    int KD;           // DMMA k-steps (4 ranks each); ranks >= 4*KD go to the DFMA tail
-    int n_tail;       // R - 4*KD in {0, 1, 2}
-    int KC;           // k-steps per stage
-    int n_kc;         // k-chunks: ceil(KD / KC)
-    int64_t n_jt;     // packed j-tiles (multiple of JT)
-    int64_t n_jc;     // j-chunks per unit
-    int64_t k0, k1;
-    double* out;
-    int64_t ldy, ldz;
-    int vec_store;    // 16-byte pair stores legal (aligned base, even strides)
-    const double* rho1;
-    const double* rho2;
-    const double* rho3;
-    double* partial;
-    int64_t n_ichunks;
-    int64_t n_units;
-    int debug;        // development knobs (LS_EXPAND_DEBUG): 1 no stores (sink), 2 fill once, 4 no tail,
-                      // 8 scale once, 16 no epilogue at all
-    int accumulate;   // add into out / partial instead of overwriting (rank-chunked expansions)
-    const double* S;  // per-slab scales S(k, q) = w_q * A3(k, q), [k][q] (TMEM variant)
-};
-
-__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "LS_WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra LS_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 
 // A2 packed so that every pipeline stage (k-chunk kc, j-chunk jc) is one contiguous block of
 // stage_elems = JT*KC*32 + JT*8*n_tail doubles at Bp + (kc * n_jc + jc) * stage_elems:
@@ -438,7 +374,6 @@ expand_dmma_kernel(const ExpandArgs p) {
     }
 }
 
-#include "expand_tmem.cuh"
 
 __global__ void sum_partials_kernel(const double* __restrict__ part, int64_t count,
                                     double* __restrict__ out) {
@@ -632,48 +567,6 @@ int kernel_setup(const void* kern, int threads, size_t smem, int& per_sm) {
     return LS_OK;
 }
 
-// The 8-warp TMEM kernel for ring shape `code` (10 * depth + j-chunks per stage) with the
-// k-step count fixed at compile time for KD 1..14 (depth 4 up to KD 11, 3 beyond, as
-// tmem_shape_for picks them); other shapes (LS_EXPAND_TMEM) take the runtime-KD kernel.
-template <bool STORE, bool FUNC, int NS, int... KD>
-void (*tmem8_pick(int kd, std::integer_sequence<int, KD...>))(ExpandArgs) {
-    void (*k)(ExpandArgs) = nullptr;
-    ((kd == KD + 1 ? (k = expand_tmem_kernel<STORE, FUNC, NS, 1, 8, KD + 1>, 0) : 0), ...);
-    return k;
-}
-// The 16-warp shape, compile-time KD over the range it is planned for (15..23).
-template <bool STORE, bool FUNC, int NS, int... KD>
-void (*tmem16_pick(int kd, std::integer_sequence<int, KD...>))(ExpandArgs) {
-    void (*k)(ExpandArgs) = nullptr;
-    ((kd == KD + 15 ? (k = expand_tmem_kernel<STORE, FUNC, NS, 1, 16, KD + 15>, 0) : 0), ...);
-    return k;
-}
-template <bool STORE, bool FUNC, int NS>
-void (*tmem16_kernel(int kd))(ExpandArgs) {
-    if (auto k = tmem16_pick<STORE, FUNC, NS>(kd, std::make_integer_sequence<int, 9>{})) return k;
-    return expand_tmem_kernel<STORE, FUNC, NS, 1, 16>;
-}
-// Two DFMA ranks (R mod 4 = 2): runtime KD.
-template <bool STORE, bool FUNC>
-void (*tmem8_kernel_t2(int code))(ExpandArgs) {
-    if (code == 41) return expand_tmem_kernel<STORE, FUNC, 4, 1, 8, 0, 2>;
-    if (code == 31) return expand_tmem_kernel<STORE, FUNC, 3, 1, 8, 0, 2>;
-    return nullptr;
-}
-template <bool STORE, bool FUNC>
-void (*tmem8_kernel(int code, int kd))(ExpandArgs) {
-    if (code == 41 && kd <= 11) return tmem8_pick<STORE, FUNC, 4>(kd, std::make_integer_sequence<int, 11>{});
-    if (code == 31 && kd >= 12 && kd <= 14) {
-        if (kd == 12) return expand_tmem_kernel<STORE, FUNC, 3, 1, 8, 12>;
-        if (kd == 13) return expand_tmem_kernel<STORE, FUNC, 3, 1, 8, 13>;
-        return expand_tmem_kernel<STORE, FUNC, 3, 1, 8, 14>;
-    }
-    if (code == 41) return expand_tmem_kernel<STORE, FUNC, 4, 1>;
-    if (code == 31) return expand_tmem_kernel<STORE, FUNC, 3, 1>;
-    if (code == 22) return expand_tmem_kernel<STORE, FUNC, 2, 2>;
-    return nullptr;
-}
-
 template <class T, bool STORE, bool FUNC, bool TMEM = false>
 int launch(ExpandArgs& a, cudaStream_t s) {
     const TmemShape sh =
@@ -715,9 +608,10 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         if (a.n_tail != 1 && !(a.n_tail == 2 && T::WARPS == 8))
             return ls::fail(LS_EVALIDATION, "expand: TMEM plan needs one DFMA rank (two with 8 warps)");
         if constexpr (T::WARPS == 16) {
-            kern = tmem16_kernel<STORE, FUNC, T::NS>(a.KD);
+            static_assert(T::NS == 2, "the 16-warp TMEM kernels are built with a 2-deep ring");
+            kern = tmem16_kernel(STORE, FUNC, a.KD);
         } else {
-            kern = a.n_tail == 2 ? tmem8_kernel_t2<STORE, FUNC>(code) : tmem8_kernel<STORE, FUNC>(code, a.KD);
+            kern = tmem8_kernel(STORE, FUNC, code, a.KD, a.n_tail);
             if (!kern) return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
         }
     }

@@ -17,6 +17,10 @@
 // n_tail is always 1 here (a zero rank when R mod 4 is 0 or 3; see tmem_tail in expand.cu).
 #pragma once
 
+#include "k3.cuh"
+
+namespace ls_k3 {
+
 namespace tmem {
 
 // Issue a 32-lane x 8-column load (4 doubles per thread); the registers are valid after wait_ld().
@@ -60,11 +64,6 @@ __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::be
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 }  // namespace tmem
-
-// TMEM columns per CTA: 8-warp CTAs run two per SM (256 columns each), 16-warp CTAs one (512).
-__host__ __device__ constexpr int tmem_cols(int warps) { return warps == 8 ? 256 : 512; }
-constexpr int kFillSlots = 9;   // per lane: up to 8 A1 values + the slab scale of one fill task
-__host__ __device__ constexpr int tmem_stg_elems(int warps) { return warps * kFillSlots * 32; }  // per CTA
 
 // 8-byte global->shared copy (LDGSTS); src_size 0 writes zeros without reading.
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
@@ -469,3 +468,5 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_s), "r"(kTmemCols)
                      : "memory");
 }
+
+}  // namespace ls_k3

@@ -1,0 +1,91 @@
+// k3.cuh -- definitions shared by the K3 translation units: the expansion launch arguments,
+// the DMMA / mbarrier / TMA helpers, the TMEM kernel constants and the entry points that hand
+// the host launcher a TMEM kernel instantiation (expand_tmem8.cu, expand_tmem16.cu, compiled in
+// parallel with expand.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace ls_k3 {
+
+struct ExpandArgs {
+    const double* A;
+    const double* B;
+    const double* Bp;   // A2 packed per stage (see pack_b_kernel)
+    const double* C;
+    const double* w;
+    int64_t lda, ldb, ldc;
+    int64_t N1, N2, N3;
+    int R;            // rank
+    int KD;           // DMMA k-steps (4 ranks each); ranks >= 4*KD go to the DFMA tail
+    int n_tail;       // R - 4*KD in {0, 1, 2}
+    int KC;           // k-steps per stage
+    int n_kc;         // k-chunks: ceil(KD / KC)
+    int64_t n_jt;     // packed j-tiles (multiple of JT)
+    int64_t n_jc;     // j-chunks per unit
+    int64_t k0, k1;
+    double* out;
+    int64_t ldy, ldz;
+    int vec_store;    // 16-byte pair stores legal (aligned base, even strides)
+    const double* rho1;
+    const double* rho2;
+    const double* rho3;
+    double* partial;
+    int64_t n_ichunks;
+    int64_t n_units;
+    int debug;        // development knobs (LS_EXPAND_DEBUG): 1 no stores (sink), 2 fill once, 4 no tail,
+                      // 8 scale once, 16 no epilogue at all
+    int accumulate;   // add into out / partial instead of overwriting (rank-chunked expansions)
+    const double* S;  // per-slab scales S(k, q) = w_q * A3(k, q), [k][q] (TMEM variant)
+};
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "LS_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LS_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// TMEM columns per CTA: 8-warp CTAs run two per SM (256 columns each), 16-warp CTAs one (512).
+__host__ __device__ constexpr int tmem_cols(int warps) { return warps == 8 ? 256 : 512; }
+constexpr int kFillSlots = 9;   // per lane: up to 8 A1 values + the slab scale of one fill task
+__host__ __device__ constexpr int tmem_stg_elems(int warps) { return warps * kFillSlots * 32; }  // per CTA
+
+using KernelFn = void (*)(ExpandArgs);
+
+// 8-warp TMEM kernel for ring shape `code` (10 * depth + j-chunks per stage), KD k-steps and
+// nt DFMA ranks; nullptr if the shape is not built. Compile-time KD for KD 1..14 with nt = 1.
+KernelFn tmem8_kernel(bool store, bool func, int code, int kd, int nt);
+// 16-warp TMEM kernel (2-deep ring, one DFMA rank); compile-time KD for KD 15..23.
+KernelFn tmem16_kernel(bool store, bool func, int kd);
+
+}  // namespace ls_k3
