@@ -33,7 +33,8 @@
 // No CTA barrier per stage: each warp releases a ring slot after its last
 // DMMA of the stage and the last one refills it. Units are spread over a
 // persistent grid (CTAs per SM x SM count). expand_tmem.cuh holds the default
-// variant for ranks up to 57, with A1k resident in tensor memory.
+// variant for ranks up to 93, with A1k resident in tensor memory (instantiated in
+// expand_tmem8.cu / expand_tmem16.cu); k3.cuh the definitions they share.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
