@@ -296,7 +296,19 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         mbar_wait(as_full + buf, static_cast<unsigned>((n >> 1) & 1));
         tmem::fence_after();
         const uint32_t tb = tq + static_cast<uint32_t>(buf * CB);
-        if (FUNC) fsum = 0.0;
+        // rho1 of this lane's eight i columns, held for the whole unit (zero beyond N1, where the
+        // accumulators are zero too).
+        double r1[kTN][2];
+        if (FUNC) {
+            fsum = 0.0;
+#pragma unroll
+            for (int nn = 0; nn < kTN; ++nn)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = ib + wi * (8 * kTN) + 8 * nn + 2 * t + e;
+                    r1[nn][e] = i < p.N1 ? __ldg(p.rho1 + i) : 0.0;
+                }
+        }
         int next_task = 0;
 
         for (int jc = 0; jc < per_unit; ++jc, ++st) {
@@ -379,8 +391,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
                 const int jb = (jc * JPS + h) * JC + wj * (8 * kTM);
                 const int ibase = ib + wi * (8 * kTN);
-                if (ibase + 8 * kTN <= p.N1 && jb + 8 * kTM <= p.N2 && (!STORE || (p.vec_store && !p.accumulate)) &&
-                    (!FUNC || (reinterpret_cast<uintptr_t>(p.rho1) & 15) == 0)) {
+                if (ibase + 8 * kTN <= p.N1 && jb + 8 * kTM <= p.N2 && (!STORE || (p.vec_store && !p.accumulate))) {
                     // Interior tile (the common case): no per-element bounds or mode checks. Measured
                     // 2.4% of the whole kernel at cfg1 (2.826 -> 2.760 ms).
                     double* row = STORE ? p.out + kk * p.ldz + static_cast<int64_t>(jb + g) * p.ldy + ibase + 2 * t
@@ -391,9 +402,8 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                             double sm = 0.0;
 #pragma unroll
                             for (int nn = 0; nn < kTN; ++nn) {
-                                const double2 r = __ldg(reinterpret_cast<const double2*>(p.rho1 + ibase + 8 * nn + 2 * t));
-                                sm = fma(acc[m][nn][0], r.x, sm);
-                                sm = fma(acc[m][nn][1], r.y, sm);
+                                sm = fma(acc[m][nn][0], r1[nn][0], sm);
+                                sm = fma(acc[m][nn][1], r1[nn][1], sm);
                             }
                             fsum = fma(sm, __ldg(p.rho2 + jb + 8 * m + g), fsum);
                         }
@@ -413,9 +423,8 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                         double sm = 0.0;
 #pragma unroll
                         for (int nn = 0; nn < kTN; ++nn) {
-                            const int i = ibase + 8 * nn + 2 * t;
-                            if (i < p.N1) sm = fma(acc[m][nn][0], __ldg(p.rho1 + i), sm);
-                            if (i + 1 < p.N1) sm = fma(acc[m][nn][1], __ldg(p.rho1 + i + 1), sm);
+                            sm = fma(acc[m][nn][0], r1[nn][0], sm);
+                            sm = fma(acc[m][nn][1], r1[nn][1], sm);
                         }
                         fsum = fma(sm, __ldg(p.rho2 + j), fsum);
                     }
