@@ -353,8 +353,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 }
                 {
                     const double* bsw = stage + jt0 * (KD * 32) + lane;
-#pragma unroll 1
-                    for (int ks = 0; ks < KD; ++ks) {
+                    auto kstep = [&](int ks) {
                         double a[kTM], b[kTN];
                         uint32_t rb[8];
                         tmem::ld_x8_issue(tb + 8 * ks, rb);
@@ -366,6 +365,15 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                         for (int m = 0; m < kTM; ++m)
 #pragma unroll
                             for (int nn = 0; nn < kTN; ++nn) dmma_884(acc[m][nn][0], acc[m][nn][1], a[m], b[nn]);
+                    };
+                    if constexpr (KD_ > 0) {
+                        // compile-time k-step count: fully unrolled (2.2% faster at cfg1 than the
+                        // rolled loop with the same constant bounds)
+#pragma unroll
+                        for (int ks = 0; ks < (KD_ > 0 ? KD_ : 1); ++ks) kstep(ks);
+                    } else {
+#pragma unroll 1
+                        for (int ks = 0; ks < KD; ++ks) kstep(ks);
                     }
                 }
                 if (h == JPS - 1) {
