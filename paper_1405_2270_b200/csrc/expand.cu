@@ -521,7 +521,7 @@ bool plan_for(int KD, int n_tail, Plan& out) {
             // for plan 0 with a 2-rank DFMA tail), so it keeps n_tail <= 1.
             // Below KD 15 the 8-warp plans are faster (rank 42: 26.8 TF/s here vs 28.6 for plan 0).
             case kPlanTmem16:
-                ok = KD + (n_tail == 2) > 14 && fits_tmem16(KD + (n_tail == 2), n_tail == 2 ? 0 : n_tail);
+                ok = (force == kPlanTmem16 || KD + (n_tail == 2) > 14) && fits_tmem16(KD + (n_tail == 2), n_tail == 2 ? 0 : n_tail);
                 ic = TileTmem16::IC;
                 break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
