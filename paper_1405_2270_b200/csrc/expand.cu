@@ -622,7 +622,22 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     // The occupancy query under-reports the tcgen05 kernel (1 instead of 2 CTAs/SM although
     // registers, shared memory and the 2 x 256 TMEM columns all fit two); use the launch bound.
     if (TMEM) per_sm = T::MINB;
-    const int64_t grid = std::min<int64_t>(a.n_units, (int64_t)ls::sm_count() * per_sm);
+    int64_t grid = std::min<int64_t>(a.n_units, (int64_t)ls::sm_count() * per_sm);
+    // Store-only TMEM launches may split their last round of units at stage granularity
+    // (expand_tmem.cuh) when that shortens the busiest CTA by more than one unit fill: cfg1 goes
+    // from 28 units (448 stages) to 27 units + 11 stages (+0.45% measured); at 512^3 it would
+    // not help (56 stages either way) and the extra partial-unit fills cost 1.6%.
+    a.split_tail = 0;
+    if (TMEM && STORE && !FUNC) {
+        const int64_t G = (int64_t)ls::sm_count() * per_sm;
+        const int64_t full = a.n_units / G, tail = a.n_units - full * G;
+        const int64_t whole = ls::ceil_div(a.n_units, G) * a.n_jc;
+        const int64_t split = full * a.n_jc + ls::ceil_div(tail * a.n_jc, G);
+        if (tail > 0 && split + 2 <= whole) {
+            a.split_tail = 1;
+            grid = std::min<int64_t>(a.n_units * a.n_jc, G);
+        }
+    }
     if (std::getenv("LS_EXPAND_VERBOSE"))
         std::fprintf(stderr, "ls_expand: tile %dx%d warps, IC %d, KC %d/%d, smem %zu B, %d CTA/SM, grid %lld, %s\n",
                      T::WARPS, T::WI, T::IC, a.KC, a.KD, smem, per_sm, static_cast<long long>(grid),

@@ -115,13 +115,31 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     const int wi = warp & 3;  // i-tiles, and the TMEM lane quarter this warp may access
     const int wj = warp >> 2;
 
-    const int my_units = n_units > static_cast<int>(blockIdx.x)
-                             ? (n_units - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
-                             : 0;
-    const int n_stages = my_units * per_unit;
+    // Work of this CTA: whole units b + n*G over the full rounds. For store-only launches the
+    // partial last round is split at stage granularity instead (balanced contiguous ranges of its
+    // stages), so every CTA finishes within one stage of the others: at cfg1 (8192 units on 296
+    // CTAs) the whole-unit tail left 1.2% of the GPU idle. Functional launches keep whole units
+    // (one writer per per-warp partial).
+    const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+    const bool kSplitTail = STORE && !FUNC && p.split_tail;
+    const int n_full = kSplitTail ? n_units / G : 0;
+    int t0 = 0, t1 = 0, tu0 = 0, n_tu = 0;  // this CTA's stages [t0, t1) of the tail round
+    if (kSplitTail) {
+        const int tail_stages = (n_units - n_full * G) * per_unit;
+        t0 = static_cast<int>(static_cast<int64_t>(tail_stages) * b / G);
+        t1 = static_cast<int>(static_cast<int64_t>(tail_stages) * (b + 1) / G);
+        if (t1 > t0) {
+            tu0 = t0 / per_unit;
+            n_tu = (t1 - 1) / per_unit - tu0 + 1;
+        }
+    }
+    const int my_units = kSplitTail ? n_full + n_tu : (n_units > b ? (n_units - 1 - b) / G + 1 : 0);
+    const int full_stages = n_full * per_unit;
+    const int n_stages = kSplitTail ? full_stages + (t1 - t0) : my_units * per_unit;
+    auto unit_of = [&](int n) { return n < n_full || !kSplitTail ? b + n * G : n_full * G + tu0 + (n - n_full); };
 
     auto issue = [&](int st) {
-        const int c = st % per_unit;
+        const int c = (kSplitTail && st >= full_stages) ? (t0 + st - full_stages) % per_unit : st % per_unit;
         const double* src = p.Bp + static_cast<int64_t>(c) * stage_elems;
         uint64_t* bar = full + (st % kNS);
         mbar_arrive_expect_tx(bar, stage_bytes);
@@ -205,11 +223,12 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
             tmem::st_x8(tq + col + 8 * KD + 16 * qt + 8, v1);
         }
     };
-    // Consume task `task` of unit u into buffer buf, then start the copy for the task after it.
-    auto run_task = [&](int u, int task, int buf) {
+    // Consume task `task` of this CTA's unit number nu into buffer buf, then start the copy for
+    // the task after it (the next unit's first task after the last one).
+    auto run_task = [&](int nu, int task, int buf) {
         task_consume(buf, task);
-        if (task + 1 < n_tasks) task_issue(u, task + 1);
-        else if (u + static_cast<int>(gridDim.x) < n_units) task_issue(u + gridDim.x, 0);
+        if (task + 1 < n_tasks) task_issue(unit_of(nu), task + 1);
+        else if (nu + 1 < my_units) task_issue(unit_of(nu + 1), 0);
     };
     auto publish = [&](int buf) {
         tmem::wait_st();
@@ -225,7 +244,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     // four tasks in flight at once (no accumulators are live yet, so the registers are free);
     // then the copy for the next unit's first task starts the one-ahead chain.
     if (my_units > 0) {
-        const int u = blockIdx.x;
+        const int u = unit_of(0);
         const int ib = (u % n_ichunks) * IC;
         const int64_t k = p.k0 + u / n_ichunks;
         for (int t0 = 0; t0 < n_tasks; t0 += 4) {
@@ -274,21 +293,27 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 }
             }
         }
-        if (u + static_cast<int>(gridDim.x) < n_units) task_issue(u + gridDim.x, 0);
+        if (my_units > 1) task_issue(unit_of(1), 0);
         publish(0);
     }
 
     double acc[kTM][kTN][2];
     double fsum = 0.0;
     int st = 0;
-    // Fill schedule for the next unit: tasks spread evenly over stages [first_fill, per_unit),
-    // offset by warp so the warps of an SM sub-partition do not fill in the same stage.
-    // (Finishing the fill earlier in the unit measured no faster.)
-    const int first_fill = per_unit > 2 ? 2 : 0;
-    const int fill_w = per_unit - first_fill;
-    auto fill_stage = [&](int task) { return first_fill + ((task * WARPS + warp) * fill_w) / (WARPS * n_tasks); };
     for (int n = 0; n < my_units; ++n) {
-        const int unit = blockIdx.x + n * gridDim.x;
+        const int unit = unit_of(n);
+        // j-chunk range of this unit (partial only for the first and last unit of a split tail)
+        const int jc_lo = (kSplitTail && n == n_full) ? t0 % per_unit : 0;
+        const int jc_hi = (kSplitTail && n >= n_full && n == my_units - 1) ? (t1 - 1) % per_unit + 1 : per_unit;
+        // Fill schedule for the next unit: tasks spread evenly over this unit's stages from the
+        // third on, offset by warp so the warps of an SM sub-partition do not fill in the same
+        // stage. (Finishing the fill earlier in the unit measured no faster.)
+        const int n_here = jc_hi - jc_lo;
+        const int first_fill = n_here > 2 ? 2 : 0;
+        const int fill_w = n_here - first_fill;
+        auto fill_stage = [&](int task) {
+            return jc_lo + first_fill + ((task * WARPS + warp) * fill_w) / (WARPS * n_tasks);
+        };
         const int buf = n & 1;
         const bool has_next = n + 1 < my_units;
         const int ib = (unit % n_ichunks) * IC;
@@ -311,7 +336,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         }
         int next_task = 0;
 
-        for (int jc = 0; jc < per_unit; ++jc, ++st) {
+        for (int jc = jc_lo; jc < jc_hi; ++jc, ++st) {
             // Fill task(s) for the next unit: loads now, product + TMEM store after the DMMAs.
             int target = next_task;
             if (has_next)
@@ -391,7 +416,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                     // This stage's fill task(s) for the next unit, after the DMMAs were issued (no fill
                     // state stays live across the DMMA loop, which keeps its operand registers free).
                     if (fill_now) {
-                        for (; next_task < target; ++next_task) run_task(unit + gridDim.x, next_task, buf ^ 1);
+                        for (; next_task < target; ++next_task) run_task(n + 1, next_task, buf ^ 1);
                         if (next_task == n_tasks) publish(buf ^ 1);
                     }
                 }
@@ -465,7 +490,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         if (has_next && next_task < n_tasks) {  // tiny units: finish the fill now
             if (next_task == 0 && n >= 1)
                 mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1));
-            for (; next_task < n_tasks; ++next_task) run_task(unit + gridDim.x, next_task, buf ^ 1);
+            for (; next_task < n_tasks; ++next_task) run_task(n + 1, next_task, buf ^ 1);
             publish(buf ^ 1);
         }
         if (FUNC) {

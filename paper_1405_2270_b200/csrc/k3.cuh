@@ -37,6 +37,7 @@ struct ExpandArgs {
                       // 8 scale once, 16 no epilogue at all
     int accumulate;   // add into out / partial instead of overwriting (rank-chunked expansions)
     const double* S;  // per-slab scales S(k, q) = w_q * A3(k, q), [k][q] (TMEM variant)
+    int split_tail;   // TMEM store-only: split the last round of units at stage granularity
 };
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {

@@ -139,3 +139,27 @@ def test_lattice_fuzz(env, orc, case, Lc, nn, idx, Z, periodic, mode, M):
     f = [np.asfortranarray(res.tensor.factor(l)) for l in range(3)]
     want_grid = orc.densify_slabs(f[0], f[1], f[2], np.ascontiguousarray(res.tensor.weights()))
     assert float(np.max(np.abs(V - want_grid)) / np.max(np.abs(want_grid))) <= 1e-13
+
+
+@pytest.mark.parametrize("R", [9, 41])
+def test_split_tail_schedule(env, orc, R):
+    """A store-only TMEM launch whose last round of units is split at stage granularity:
+    600 units (2 i-chunks x 300 slabs) of 20 stages on 296 CTAs. Checked against the oracle."""
+    torch, _abi = env
+    rng = np.random.default_rng(300 + R)
+    dims = (256, 1280, 300)
+    f = [np.asfortranarray(rng.uniform(0.05, 1.0, (d, R))) for d in dims]
+    w = rng.uniform(0.05, 1.0, R)
+    dev = torch.device("cuda")
+    fac = [torch.as_tensor(x.T.copy(), device=dev) for x in f]
+    wd = torch.as_tensor(w, device=dev)
+    out = torch.empty((dims[2], dims[1], dims[0]), dtype=torch.float64, device=dev)
+    lib = _abi.load()
+    p = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.ls_expand(p(fac[0]), dims[0], p(fac[1]), dims[1], p(fac[2]), dims[2], p(wd), *dims, R, 0, dims[2],
+                         p(out), 0, 0, None, None, None, None, s) == 0, lib.ls_last_error()
+    got = out.cpu().numpy()
+    for k in list(range(0, 300, 37)) + [299]:
+        want = orc.densify_slabs(f[0], f[1], f[2], w, k, k + 1)[:, :, 0]
+        assert float(np.max(np.abs(got[k].T - want)) / np.max(np.abs(want))) <= 1e-13, k
