@@ -18,6 +18,8 @@ __global__ void assemble_axis_kernel(const double* __restrict__ master, int64_t 
                                      const int64_t* __restrict__ ia, int64_t n, int64_t L,
                                      int periodic, int64_t out_len, double* __restrict__ out,
                                      int64_t ld_out) {
+    pdl_wait();  // the master comes from the preceding generator launch
+    pdl_trigger();
     const int c = blockIdx.y;  // column nu*R + q
     const int nu = c / R;
     const int q = c % R;
@@ -56,9 +58,9 @@ extern "C" int ls_assemble_axis(const double* master_d, int64_t ld_master, int R
     const int64_t cols = (int64_t)M0 * R;
     if (cols > 65535) return ls::fail(LS_EGUARD, "assemble_axis: more than 65535 columns");
     const int64_t blocks = std::min<int64_t>(ls::ceil_div(out_len, kAsmThreads), 2048);
-    assemble_axis_kernel<<<dim3((unsigned)blocks, (unsigned)cols), kAsmThreads, 0,
-                           ls::as_stream(stream)>>>(master_d, ld_master, R, ia_d, n, L, periodic,
-                                                    out_len, out_d, ld_out);
+    LS_CUDA(ls::launch_pdl(assemble_axis_kernel, dim3((unsigned)blocks, (unsigned)cols), dim3(kAsmThreads), 0,
+                           ls::as_stream(stream), master_d, ld_master, R, ia_d, n, L, periodic, out_len, out_d,
+                           ld_out));
     LS_LAUNCHED("assemble_axis_kernel");
     return LS_OK;
 }

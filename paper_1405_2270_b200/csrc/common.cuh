@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdint>
 #include <string>
+#include <utility>
 
 #include "latsum_cuda.h"
 
@@ -64,6 +65,31 @@ int sm_count();
 // pool (no OS round trip per call). Idempotent per device.
 void ensure_pool();
 
+}  // namespace ls
+
+// Programmatic dependent launch (PDL) along the step's kernel chain (generator -> assembly ->
+// prep -> expansion): a kernel launched with launch_pdl may start while its predecessor in the
+// stream still runs; it must call pdl_wait() before touching anything the predecessor writes.
+// pdl_trigger() lets the next kernel in the chain start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+namespace ls {
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 }  // namespace ls
 
 // Rounded FP64 primitives that the compiler can never contract into FMA:

@@ -62,6 +62,8 @@ __global__ void pack_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t
                               int KC, int n_kc, int JT, int64_t n_jc, double* __restrict__ Bp,
                               const double* __restrict__ w, const double* __restrict__ C, int64_t ldc, int64_t k1,
                               double* __restrict__ S) {
+    pdl_wait();  // B, C, w may come from the preceding assembly / generator launches
+    pdl_trigger();
     const int64_t frag = static_cast<int64_t>(JT) * KC * 32;
     const int64_t stage_elems = frag + static_cast<int64_t>(JT) * 8 * n_tail;
     const int64_t total = static_cast<int64_t>(n_kc) * n_jc * stage_elems;
@@ -119,6 +121,7 @@ struct Tile {
 template <class T, bool STORE, bool FUNC>
 __global__ void __launch_bounds__(T::WARPS * 32, T::MINB)
 expand_dmma_kernel(const ExpandArgs p) {
+    pdl_wait();  // the packed A2 and the factors come from the preceding launches
     constexpr int WARPS = T::WARPS;
     constexpr int WI = T::WI;
     constexpr int kTM = T::TM;
@@ -591,8 +594,8 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bp), (bp_elems + s_elems) * sizeof(double), s));
     a.S = TMEM ? bp + bp_elems : nullptr;
     const int64_t pb = std::min<int64_t>(ls::ceil_div(static_cast<int64_t>(bp_elems + s_elems), 256), 4096);
-    pack_b_kernel<<<(unsigned)pb, 256, 0, s>>>(a.B, a.ldb, a.N2, a.R, a.KD, a.n_tail, a.KC, a.n_kc, JT, a.n_jc, bp,
-                                               a.w, a.C, a.ldc, a.k1, const_cast<double*>(a.S));
+    LS_CUDA(ls::launch_pdl(pack_b_kernel, dim3((unsigned)pb), dim3(256), 0, s, a.B, a.ldb, a.N2, a.R, a.KD,
+                           a.n_tail, a.KC, a.n_kc, JT, a.n_jc, bp, a.w, a.C, a.ldc, a.k1, const_cast<double*>(a.S)));
     LS_LAUNCHED("pack_b_kernel");
     a.Bp = bp;
     // 32-bit counters inside the kernel
@@ -643,7 +646,7 @@ int launch(ExpandArgs& a, cudaStream_t s) {
                      T::WARPS, T::WI, T::IC, a.KC, a.KD, smem, per_sm, static_cast<long long>(grid),
                      TMEM ? "A1k in TMEM" : "A1k in smem");
     if (grid > 0) {
-        kern<<<(unsigned)grid, T::WARPS * 32, smem, s>>>(a);
+        LS_CUDA(ls::launch_pdl(kern, dim3((unsigned)grid), dim3(T::WARPS * 32), smem, s, a));
         LS_LAUNCHED("expand_dmma_kernel");
     }
     LS_CUDA(cudaFreeAsync(bp, s));

@@ -166,6 +166,9 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     tmem::fence_before();
     __syncthreads();
     tmem::fence_after();
+    // TMEM allocation and barrier set-up overlap the tail of the preceding (prep) launch; the
+    // packed A2, the scale table and the factors are read only after it completes.
+    pdl_wait();
     const uint32_t tq = *tmem_base_s + (static_cast<uint32_t>(32 * wi) << 16);  // this warp's lane quarter
     double* stg = smem + 32 + warp * (kFillSlots * 32) + lane;  // this lane's fill staging slots (stride 32)
 

@@ -17,6 +17,7 @@ constexpr int kGenThreads = 256;
 //   x = t * ((i + 0.5 - len/2) * h);  out = exp(-x*x)
 __global__ void gen_midpoint_kernel(const double* __restrict__ tau, int64_t len, double h,
                                     double* __restrict__ out, int64_t ld) {
+    pdl_trigger();  // the assembly may start launching (it waits for this grid before reading)
     const int q = blockIdx.y;
     const double t = tau[q];
     const double half_len = static_cast<double>(len) / 2.0;
@@ -33,6 +34,7 @@ __global__ void gen_midpoint_kernel(const double* __restrict__ tau, int64_t len,
 // blockDim + 1 vertices bounding them.
 __global__ void gen_erf_kernel(const double* __restrict__ tau, int64_t len, double h,
                                double* __restrict__ out, int64_t ld) {
+    pdl_trigger();
     __shared__ double ev[kGenThreads + 1];
     const int q = blockIdx.y;
     const double t = tau[q];
