@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         tmem::fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(as_empty + buf);
+        if (has_next && n_tasks == 0) publish(buf ^ 1);  // no fill share (KD = 1, wj = 1): still arrive
         if (has_next && next_task < n_tasks) {  // tiny units: finish the fill now
             if (next_task == 0 && n >= 1)
                 mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1));

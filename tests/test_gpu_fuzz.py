@@ -163,3 +163,28 @@ def test_split_tail_schedule(env, orc, R):
     for k in list(range(0, 300, 37)) + [299]:
         want = orc.densify_slabs(f[0], f[1], f[2], w, k, k + 1)[:, :, 0]
         assert float(np.max(np.abs(got[k].T - want)) / np.max(np.abs(want))) <= 1e-13, k
+
+
+@pytest.mark.parametrize("R", [1, 4, 5])
+def test_single_kstep_ranks_multi_unit(env, orc, R):
+    """Ranks with one DMMA k-step (KD = 1) on a grid where every CTA runs many units: the warps
+    without a fill share must still hand the next A1k buffer over (regression: a hang)."""
+    torch, _abi = env
+    rng = np.random.default_rng(500 + R)
+    dims = (1024, 64, 1200)  # 8 i-chunks x 1200 slabs = 9600 units of one stage
+    f = [np.asfortranarray(rng.uniform(0.05, 1.0, (d, R))) for d in dims]
+    w = rng.uniform(0.05, 1.0, R)
+    dev = torch.device("cuda")
+    fac = [torch.as_tensor(x.T.copy(), device=dev) for x in f]
+    wd = torch.as_tensor(w, device=dev)
+    out = torch.empty((dims[2], dims[1], dims[0]), dtype=torch.float64, device=dev)
+    lib = _abi.load()
+    p = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.ls_expand(p(fac[0]), dims[0], p(fac[1]), dims[1], p(fac[2]), dims[2], p(wd), *dims, R, 0, dims[2],
+                         p(out), 0, 0, None, None, None, None, s) == 0, lib.ls_last_error()
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    for k in (0, 599, 1199):
+        want = orc.densify_slabs(f[0], f[1], f[2], w, k, k + 1)[:, :, 0]
+        assert float(np.max(np.abs(got[k].T - want)) / np.max(np.abs(want))) <= 1e-13, k
