@@ -9,7 +9,7 @@
 // It is a GEMM with a fused reduction epilogue. Rows m = j + N2*k of V^T (K = N1 along i)
 // times X (K x F):
 //   C[m, f] = sum_i V(i, m) X(i, f)            FP64 DMMA m8n8k4, 128 x 64 CTA tiles, K by 16
-//   part[m_tile, f] = sum_{m in tile} C[m, f] * (Y(j,f) * Z(k,f))    fixed-order epilogue
+//   part[m_tile, f] = sum_{m in tile} C[m, f] * Y(j,f) * Z(k,f)      fixed-order epilogue
 // then out[f] = scale * sum over m-tiles in ascending order (grid_batch_reduce_kernel), so the
 // result is bitwise reproducible. Operands stream global -> shared with cp.async (3 stages);
 // the f-tiles of one m-tile are adjacent in the launch order, so V is read from HBM once and
@@ -144,21 +144,42 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) grid_batch_kernel(const 
     double s[4][2];
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) s[ni][0] = s[ni][1] = 0.0;
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
-        const int64_t m = m0 + wm * 32 + 8 * mi + g;
-        if (m >= p.M) continue;
-        const int64_t j = m % p.N2, k = m / p.N2;
+    const int64_t mb = m0 + wm * 32 + g;  // this lane's rows: mb + 8 mi
+    const int64_t kb = mb / p.N2;
+    if (mb + 24 < p.M && (mb + 24) / p.N2 == kb) {
+        // All four rows lie in one slab k (the common case): Z(k, f) factors out of the row sum,
+        // halving the weight loads and products.
+        const int64_t jb = mb - kb * p.N2;
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int f = f0 + wn * 32 + 8 * ni + 2 * t + e;
                 if (f < p.F) {
-                    const double w = rn_mul(__ldg(p.Y + j + p.ldyy * f), __ldg(p.Z + k + p.ldzz * f));
-                    s[ni][e] = fma(acc[mi][ni][e], w, s[ni][e]);
+                    const double* y = p.Y + jb + p.ldyy * f;
+                    double sy = 0.0;
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) sy = fma(acc[mi][ni][e], __ldg(y + 8 * mi), sy);
+                    s[ni][e] = rn_mul(sy, __ldg(p.Z + kb + p.ldzz * f));
                 }
             }
+    } else {
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+            const int64_t m = mb + 8 * mi;
+            if (m >= p.M) continue;
+            const int64_t j = m % p.N2, k = m / p.N2;
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int f = f0 + wn * 32 + 8 * ni + 2 * t + e;
+                    if (f < p.F) {
+                        const double w = rn_mul(__ldg(p.Y + j + p.ldyy * f), __ldg(p.Z + k + p.ldzz * f));
+                        s[ni][e] = fma(acc[mi][ni][e], w, s[ni][e]);
+                    }
+                }
+        }
     }
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni)
