@@ -248,6 +248,7 @@ def run_ours(args, rank, world, local_rank):
         "peak_source": peak_src, "traffic": traffic,
         "algorithmic": f"2*R*points FLOP = {flops:.4e} per launch (R={pipe.Rt}), 8 B/point written",
         "kernel_ms": round(exp_mean, 4),
+        "kernel": expand_plan_name(lib, pipe.Rt),
         "hbm_leg": {"achieved_gbs": round(out_gbs, 1), "peak_gbs": hbm_gbs, "frac": round(out_gbs / hbm_gbs, 4),
                     "peak_source": hbm_src},
         "share_of_step": round(exp_mean / ms_step, 4),
@@ -287,6 +288,12 @@ def run_ours(args, rank, world, local_rank):
             "assembly_note": "generator + assembly are inside every step (replicated per rank)",
         }
         print(json.dumps(line), flush=True)
+
+
+def expand_plan_name(lib, R):
+    import ctypes as C
+    buf = C.create_string_buffer(256)
+    return buf.value.decode() if lib.ls_expand_plan_name(R, buf, 256) == 0 else None
 
 
 def _ev_ms(fn, reps=3):

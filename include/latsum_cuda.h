@@ -96,6 +96,9 @@ int ls_expand(const double* A_d, int64_t lda, const double* B_d, int64_t ldb, co
               int64_t k1, double* out_d, int64_t ldy, int64_t ldz, const double* rho1_d,
               const double* rho2_d, const double* rho3_d, double* partial_d, void* stream);
 int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_t k0, int64_t k1);
+/* Human-readable description of the expansion plan ls_expand picks for rank R (kernel, CTA
+ * shape, where A1k lives, k-steps, DFMA ranks) into out (NUL-terminated, at most len bytes). */
+int ls_expand_plan_name(int R, char* out, int len);
 /* Deterministic fixed-order sum of count doubles into *out_d (device). */
 int ls_sum_partials(const double* partial_d, int64_t count, double* out_d, void* stream);
 

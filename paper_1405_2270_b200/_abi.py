@@ -52,6 +52,7 @@ SIGNATURES = {
     "ls_functional_batch": (_i, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i, _i64, _i64, _i64, _vp, _i64, _vp, _i64,
                                  _vp, _i64, _i, _d, _vp, _vp]),
     "ls_maxdiff_accumulate": (_i, [_vp, _vp, _i64, _vp, _i, _vp]),
+    "ls_expand_plan_name": (_i, [_i, C.c_char_p, _i]),
     "ls_grid_functional_batch": (_i, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i, _d,
                                       _i, _vp, _vp]),
     "ls_probe_error": (_i, [_vp, _vp, _i, _i64, _d, _vp, _vp, _i64, _vp, _vp]),

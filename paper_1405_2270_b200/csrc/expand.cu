@@ -696,6 +696,27 @@ extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_
     return ls::ceil_div(N1, IC) * (k1 - k0) * (pl.id == kPlanTmem ? 8 : pl.id == kPlanTmem16 ? 16 : 1);
 }
 
+extern "C" int ls_expand_plan_name(int R, char* out, int len) {
+    if (R < 0 || !out || len < 1) return ls::fail(LS_EVALIDATION, "expand_plan_name: bad arguments");
+    int KD, n_tail;
+    split_rank(std::max(R, 1), KD, n_tail);
+    Plan pl;
+    const bool whole = plan_for(KD, n_tail, pl);
+    if (!whole && !chunk_plan(pl)) return ls::fail(LS_EGUARD, "expand_plan_name: no tile plan");
+    const int kd = pl.pad && n_tail == 2 ? KD + 1 : KD;
+    const int nt = pl.id == kPlanTmem || pl.id == kPlanTmem16 ? (pl.pad ? 1 : tmem_tail(n_tail)) : n_tail;
+    const char* shape = pl.id == kPlanTmem     ? "expand_tmem_kernel, 8 warps x 2 CTAs/SM, A1k in TMEM"
+                        : pl.id == kPlanTmem16 ? "expand_tmem_kernel, 16 warps x 1 CTA/SM, A1k in TMEM"
+                        : pl.id == 9           ? "expand_dmma_kernel TileLR16, 16 warps x 1 CTA/SM, A1k in smem"
+                                               : "expand_dmma_kernel, A1k in smem";
+    std::snprintf(out, static_cast<size_t>(len), "%s; plan %d, KD %d (%s), %d DFMA rank(s)%s", shape, pl.id, kd,
+                  (pl.id == kPlanTmem && kd <= 14) || (pl.id == kPlanTmem16 && kd >= 15 && kd <= 23)
+                      ? "compiled"
+                      : "runtime",
+                  nt, whole ? "" : ", 256-rank chunks");
+    return LS_OK;
+}
+
 extern "C" int ls_expand(const double* A_d, int64_t lda, const double* B_d, int64_t ldb,
                          const double* C_d, int64_t ldc, const double* w_d, int64_t N1, int64_t N2,
                          int64_t N3, int R, int64_t k0, int64_t k1, double* out_d, int64_t ldy,
