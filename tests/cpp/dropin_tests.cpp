@@ -7,6 +7,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <fstream>
 #include <iterator>
@@ -704,6 +705,216 @@ TEST(DevicePotential, GridFunctionalsMatchScalarProduct) {  // full-grid batch v
                  validation_error);
 }
 
+
+// ------------------------------------------------------------------ factor algebra and 1D convolution
+TEST(Convolve1d, DeltaAndBoxIdentities) {  // test_canonical.cpp:230-246
+    Vector a(7);
+    for (Index i = 0; i < 7; ++i) a[i] = 0.5 * static_cast<double>(i) - 1.25;
+    Vector delta = Vector::Zero(5);
+    delta[5 / 2] = 1.0;  // centred unit impulse: "same" mode must give a back unchanged
+    Vector same = convolve1d(a, delta, ConvMode::same);
+    EXPECT_TRUE((same.array() == a.array()).all());
+    Vector box = Vector::Ones(3);
+    Vector tri = convolve1d(box, box, ConvMode::full);  // 1 2 3 2 1
+    ASSERT_EQ(tri.size(), 5);
+    const double want[5] = {1.0, 2.0, 3.0, 2.0, 1.0};
+    for (Index i = 0; i < 5; ++i) EXPECT_EQ(tri[i], want[i]);
+}
+
+TEST(Convolve1d, FullLengthAndCommutativity) {  // test_canonical.cpp:248-258
+    std::mt19937 gen(2024);
+    std::uniform_real_distribution<double> u(-2.0, 2.0);
+    Vector a(9), b(5);
+    for (Index i = 0; i < 9; ++i) a[i] = u(gen);
+    for (Index i = 0; i < 5; ++i) b[i] = u(gen);
+    Vector ab = convolve1d(a, b, ConvMode::full), ba = convolve1d(b, a, ConvMode::full);
+    ASSERT_EQ(ab.size(), 13);
+    ASSERT_EQ(ba.size(), 13);
+    EXPECT_LT((ab - ba).cwiseAbs().maxCoeff(), 1e-14);
+}
+
+TEST(ConvolveCanonical, MatchesDenseConvolution) {  // test_canonical.cpp:260-274
+    std::mt19937 gen(77);
+    for (ConvMode mode : {ConvMode::full, ConvMode::same}) {
+        for (int trial = 0; trial < 4; ++trial) {
+            const Dims3 d = random_dims(gen, 2, 5);
+            CanonicalTensor3 a = random_tensor(gen, d, 2), b = random_tensor(gen, d, 3);
+            CanonicalTensor3 c = convolve1d_canonical(a, b, mode);
+            EXPECT_EQ(c.rank(), 6);
+            // dense 3D convolution of the two materialised tensors by scalar loops
+            const DenseTensor3 da = scalar_oracle(a), db = scalar_oracle(b);
+            Dims3 full{2 * d[0] - 1, 2 * d[1] - 1, 2 * d[2] - 1};
+            std::vector<double> conv(static_cast<size_t>(full[0] * full[1] * full[2]), 0.0);
+            for (Index k = 0; k < d[2]; ++k)
+                for (Index j = 0; j < d[1]; ++j)
+                    for (Index i = 0; i < d[0]; ++i)
+                        for (Index kk = 0; kk < d[2]; ++kk)
+                            for (Index jj = 0; jj < d[1]; ++jj)
+                                for (Index ii = 0; ii < d[0]; ++ii)
+                                    conv[static_cast<size_t>((i + ii) + full[0] * ((j + jj) + full[1] * (k + kk)))] +=
+                                        da(i, j, k) * db(ii, jj, kk);
+            const Dims3 out = c.dims();
+            const Index off[3] = {mode == ConvMode::same ? d[0] / 2 : 0, mode == ConvMode::same ? d[1] / 2 : 0,
+                                  mode == ConvMode::same ? d[2] / 2 : 0};
+            const DenseTensor3 dc = scalar_oracle(c);
+            double md = 0.0, mx = 0.0;
+            for (Index k = 0; k < out[2]; ++k)
+                for (Index j = 0; j < out[1]; ++j)
+                    for (Index i = 0; i < out[0]; ++i) {
+                        const double w = conv[static_cast<size_t>((i + off[0]) +
+                                                                  full[0] * ((j + off[1]) + full[1] * (k + off[2])))];
+                        md = std::max(md, std::abs(dc(i, j, k) - w));
+                        mx = std::max(mx, std::abs(w));
+                    }
+            EXPECT_LT(md / mx, 1e-12);
+        }
+    }
+}
+
+TEST(Algebra, ZeroOperands) {  // test_canonical.cpp:162-168, 186-193
+    std::mt19937 gen(5);
+    CanonicalTensor3 a = random_tensor(gen, {4, 3, 5}, 3);
+    CanonicalTensor3 zero(Dims3{4, 3, 5});
+    CanonicalTensor3 h = hadamard(a, zero);  // anything times the zero tensor is the zero tensor
+    EXPECT_EQ(h.rank(), 0);
+    EXPECT_TRUE((h.dims() == Dims3{4, 3, 5}));
+    CanonicalTensor3 s = add(a, zero);  // and adding it changes nothing, bit for bit
+    EXPECT_EQ(s.rank(), a.rank());
+    EXPECT_EQ(max_norm_diff(densify(s), densify(a)), 0.0);
+}
+
+TEST(AddCoalescing, RejectsMismatchedInputs) {  // test_canonical.cpp:219-228
+    std::mt19937 gen(8);
+    CanonicalTensor3 a = random_tensor(gen, {3, 4, 3}, 2), b = random_tensor(gen, {3, 4, 3}, 2);
+    EXPECT_THROW(add_coalescing(a, b, 1), validation_error);  // the other two axes differ
+    EXPECT_THROW(add_coalescing(a, random_tensor(gen, {3, 4, 3}, 4), 1), validation_error);  // ranks differ
+    EXPECT_THROW(add_coalescing(a, a, -1), validation_error);
+    EXPECT_THROW(add_coalescing(a, a, 3), validation_error);
+}
+
+TEST(CanonicalProperty, RandomTrialsAgainstScalarOracles) {  // test_canonical.cpp (100 random trials)
+    std::mt19937 gen(100);
+    for (int trial = 0; trial < 100; ++trial) {
+        const Dims3 d = random_dims(gen, 1, 6);
+        std::uniform_int_distribution<Index> rk(0, 5);
+        CanonicalTensor3 a = random_tensor(gen, d, rk(gen)), b = random_tensor(gen, d, rk(gen));
+        const DenseTensor3 da = scalar_oracle(a), db = scalar_oracle(b);
+        const DenseTensor3 ga = densify(a);
+        EXPECT_LE(max_norm_diff(ga, da), 1e-13 * std::max(1.0, max_abs(da)));
+        double dot = 0.0, na = 0.0, nb = 0.0;
+        for (Index e = 0; e < da.size(); ++e) {
+            dot += da.data()[e] * db.data()[e];
+            na += da.data()[e] * da.data()[e];
+            nb += db.data()[e] * db.data()[e];
+        }
+        EXPECT_LE(std::abs(scalar_product(a, b) - dot), 1e-11 * std::max(1.0, std::sqrt(na * nb)));
+        std::uniform_int_distribution<Index> pi(0, d[0] - 1), pj(0, d[1] - 1), pk(0, d[2] - 1);
+        const Index i = pi(gen), j = pj(gen), k = pk(gen);
+        EXPECT_LE(std::abs(eval_point(a, i, j, k) - da(i, j, k)), 1e-13 * std::max(1.0, max_abs(da)));
+    }
+}
+
+TEST(ScalarProduct, SelfProductIsNonNegative) {  // test_canonical.cpp:124-131
+    std::mt19937 gen(14);
+    for (int trial = 0; trial < 20; ++trial) {
+        CanonicalTensor3 a = random_tensor(gen, random_dims(gen), 4);
+        const DenseTensor3 da = scalar_oracle(a);
+        double n2 = 0.0;
+        for (Index e = 0; e < da.size(); ++e) n2 += da.data()[e] * da.data()[e];
+        EXPECT_GE(scalar_product(a, a), -1e-12 * std::max(1.0, n2));
+    }
+}
+
+// ------------------------------------------------------------------ lattice specification and windows
+TEST(LatticeSpec, ValidatesShapeAndCharges) {  // test_lattice.cpp:103-109
+    EXPECT_NO_THROW(make_spec({1, 3, 2}, 8, 2.0, {Charge{{0.0, 0.0, 0.0}, 1.0}}).validate());
+    EXPECT_THROW(make_spec({1, 0, 2}, 8, 2.0, {Charge{{0.0, 0.0, 0.0}, 1.0}}).validate(), validation_error);
+    EXPECT_THROW(make_spec({1, 1, 1}, 8, 2.0, {}).validate(), validation_error);
+    EXPECT_THROW(make_spec({1, 1, 1}, 8, 2.0, {Charge{{0.0, 0.0, 0.0}, 0.0}}).validate(), validation_error);
+    EXPECT_THROW(make_spec({1, 1, 1}, 7, 2.0, {Charge{{0.0, 0.0, 0.0}, 1.0}}).validate(), validation_error);
+}
+
+TEST(DirectSum, EquivalentChargePlacementsCoincideBitwise) {  // test_lattice.cpp:174-187
+    // A charge on the face between cells k and k+1 is vertex n of cell k or vertex 0 of cell k+1:
+    // both descriptions must select the same master window.
+    const Index n = 8, N = 3 * n;
+    EXPECT_EQ(window_start_box(N, n, n, 1), window_start_box(N, n, 0, 2));
+    LatticeSpec spec = make_spec({3, 1, 1}, n, 2.0, {Charge{{1.0, 0.0, 0.0}, 1.0}});
+    QuadratureRule rule = sinc_quadrature(1e-4, spec.unit.h(), std::sqrt(3.0) * 6.0, 8, 1.0);
+    CanonicalTensor3 master = build_lattice_master(spec, rule);
+    for (Index q = 0; q < master.rank(); q += 3) {
+        Vector lo = window_apply(master.factor(0).col(q), WindowOp(window_start_box(N, n, n, 1), 2 * N, N));
+        Vector hi = window_apply(master.factor(0).col(q), WindowOp(window_start_box(N, n, 0, 2), 2 * N, N));
+        EXPECT_TRUE((lo.array() == hi.array()).all());
+    }
+}
+
+// ------------------------------------------------------------------ Gaussian bases, potential matrix
+TEST(GaussianBasis, SamplesCenteredWideAndRejects) {  // test_project.cpp:32-88
+    GridSpec g{2.0, 8};
+    Rank1Basis b = sample_gaussian_basis(g, {GaussianBasisSpec{{0.0, 0.25, -0.5}, 0.3}, GaussianBasisSpec{{0.0, 0.0, 0.0}, 1e300}});
+    ASSERT_EQ(b.size(), 2);
+    EXPECT_EQ(b.n, 8);
+    EXPECT_EQ(b.h, 0.25);
+    for (Index i = 0; i < 8; ++i) {
+        const double d = g.midpoint(i) - 0.25;
+        EXPECT_NEAR(b.funcs[0][1][i], std::exp(-d * d / (2.0 * 0.09)), 1e-15);  // midpoint samples
+        EXPECT_EQ(b.funcs[0][0][i], b.funcs[0][0][7 - i]);                     // centred: exactly even
+        for (int l = 0; l < 3; ++l) EXPECT_EQ(b.funcs[1][static_cast<size_t>(l)][i], 1.0);  // huge width: ones
+    }
+    EXPECT_THROW(sample_gaussian_basis(g, {}), validation_error);
+    EXPECT_THROW(sample_gaussian_basis(g, {GaussianBasisSpec{{0.0, 0.0, 0.0}, 0.0}}), validation_error);
+    EXPECT_THROW(sample_gaussian_basis(g, {GaussianBasisSpec{{0.0, 0.0, 0.0}, -1.0}}), validation_error);
+    EXPECT_THROW(sample_gaussian_basis(g, {GaussianBasisSpec{{std::numeric_limits<double>::quiet_NaN(), 0.0, 0.0}, 1.0}}),
+                 validation_error);
+}
+
+TEST(PotentialMatrix, MatchesDenseTripleLoopOracle) {  // test_project.cpp:112-125
+    std::mt19937 gen(61);
+    GridSpec g{2.0, 6};
+    CanonicalTensor3 P = random_tensor(gen, {6, 6, 6}, 3);
+    std::vector<GaussianBasisSpec> specs{GaussianBasisSpec{{0.1, -0.2, 0.3}, 0.4}, GaussianBasisSpec{{-0.3, 0.0, 0.2}, 0.6},
+                                         GaussianBasisSpec{{0.0, 0.5, -0.5}, 0.8}};
+    Rank1Basis basis = sample_gaussian_basis(g, specs);
+    for (bool vol : {false, true}) {
+        Matrix V = potential_matrix(basis, P, vol);
+        const DenseTensor3 dp = scalar_oracle(P);
+        const double scale = vol ? g.h() * g.h() * g.h() : 1.0;
+        for (Index a = 0; a < 3; ++a)
+            for (Index c = 0; c < 3; ++c) {
+                double want = 0.0;
+                for (Index k = 0; k < 6; ++k)
+                    for (Index j = 0; j < 6; ++j)
+                        for (Index i = 0; i < 6; ++i)
+                            want += dp(i, j, k) * basis.funcs[static_cast<size_t>(a)][0][i] * basis.funcs[static_cast<size_t>(c)][0][i] *
+                                    basis.funcs[static_cast<size_t>(a)][1][j] * basis.funcs[static_cast<size_t>(c)][1][j] *
+                                    basis.funcs[static_cast<size_t>(a)][2][k] * basis.funcs[static_cast<size_t>(c)][2][k];
+                EXPECT_NEAR(V(a, c), scale * want, 1e-11 * std::max(1.0, std::abs(scale * want)));
+            }
+    }
+    CanonicalTensor3 wrong = random_tensor(gen, {6, 6, 5}, 2);  // basis grid 6^3, potential 6x6x5
+    EXPECT_THROW(potential_matrix(basis, wrong, false), validation_error);
+}
+
+// ------------------------------------------------------------------ series and extrapolation
+TEST(Richardson, EliminatesLeadingGrowthExactly) {  // test_lattice.cpp (Richardson)
+    const double a = 1.75, c = 0.5, L = 8.0;
+    // p(L) = a + c L (linear growth), p(2L) = a + 2 c L
+    EXPECT_EQ(richardson_extrapolate(a + c * L, a + 2.0 * c * L, RichardsonOrder::linear), a);
+    // p(L) = a + c L^2 (quadratic growth), p(2L) = a + 4 c L^2
+    EXPECT_EQ(richardson_extrapolate(a + c * L * L, a + 4.0 * c * L * L, RichardsonOrder::quadratic), a);
+}
+
+TEST(Series, ShapesAndRejectsBadLists) {  // test_lattice.cpp (Series)
+    EXPECT_TRUE((series_cells(SeriesKind::line, 5) == std::array<Index, 3>{5, 1, 1}));
+    EXPECT_TRUE((series_cells(SeriesKind::plane, 5) == std::array<Index, 3>{5, 5, 1}));
+    EXPECT_TRUE((series_cells(SeriesKind::cube, 5) == std::array<Index, 3>{5, 5, 5}));
+    GridSpec unit{2.0, 8};
+    EXPECT_THROW(center_value_series(SeriesKind::line, {}, unit, 1e-4), validation_error);
+    EXPECT_THROW(center_value_series(SeriesKind::line, {2, 2}, unit, 1e-4), validation_error);
+    EXPECT_THROW(center_value_series(SeriesKind::line, {4, 2}, unit, 1e-4), validation_error);
+}
+
 // ------------------------------------------------------------------ bundle / CSV formats
 std::string golden_dir() {
     const char* d = std::getenv("LATSUM_GOLDEN_DIR");
@@ -803,6 +1014,44 @@ TEST(Csv, ReadsChargesAndBasis) {  // test_bundle.cpp:88-140
     EXPECT_THROW(read_charges_csv(tmp_path("nope.csv")), validation_error);
     EXPECT_EQ(format_double(0.1), std::string("0.10000000000000001"));
     for (const auto& f : {c, bpath, bad}) std::remove(f.c_str());
+}
+
+
+TEST(FormatDouble, RoundTripsExactly) {  // bundle.hpp format_double
+    std::mt19937_64 gen(9);
+    std::uniform_real_distribution<double> u(-1e6, 1e6);
+    const double specials[] = {0.0, -0.0, 1.0 / 3.0, 0.1, 1e-300, 6.02214076e23, std::numeric_limits<double>::max(),
+                               std::numeric_limits<double>::denorm_min()};
+    for (double x : specials) EXPECT_EQ(std::strtod(format_double(x).c_str(), nullptr), x);
+    for (int e = 0; e < 200; ++e) {
+        const double x = u(gen) * std::pow(10.0, static_cast<double>(static_cast<int>(gen() % 40) - 20));
+        EXPECT_EQ(std::strtod(format_double(x).c_str(), nullptr), x);
+    }
+}
+
+TEST(Bundle, RankZeroAndLatticeResultsRoundTrip) {  // test_bundle.cpp (rank zero, lattice results)
+    const std::string path = tmp_path("r0.bin");
+    TensorBundle z;
+    z.tensor = CanonicalTensor3(Dims3{3, 2, 4});
+    z.h = 0.5;
+    save_bundle(path, z);
+    TensorBundle zr = load_bundle(path);
+    EXPECT_EQ(zr.tensor.rank(), 0);
+    EXPECT_TRUE((zr.tensor.dims() == Dims3{3, 2, 4}));
+    EXPECT_EQ(zr.h, 0.5);
+    // a lattice sum written and read back densifies to the same grid, bit for bit
+    LatticeSpec spec = make_spec({2, 1, 2}, 8, 2.0, {Charge{{0.25, 0.0, -0.5}, 1.5}});
+    QuadratureRule rule = sinc_quadrature(1e-4, spec.unit.h(), std::sqrt(3.0) * 4.0, 8, 1.0);
+    SumResult sum = assembled_box_sum(spec, build_lattice_master(spec, rule));
+    TensorBundle b;
+    b.tensor = sum.tensor;
+    b.h = spec.unit.h();
+    b.origin = {-2.0 + 0.125, -1.0 + 0.125, -2.0 + 0.125};
+    save_bundle(path, b);
+    TensorBundle br = load_bundle(path);
+    EXPECT_EQ(br.origin[0], b.origin[0]);
+    EXPECT_EQ(max_norm_diff(densify(br.tensor), densify(sum.tensor)), 0.0);
+    std::remove(path.c_str());
 }
 
 int main(int argc, char** argv) { return minitest::run_all(argc, argv); }
