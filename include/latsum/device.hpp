@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <utility>
 
 #include "latsum/canonical.hpp"
@@ -109,6 +110,14 @@ private:
     Dims3 dims_{0, 0, 0};
     Index rank_ = 0;
 };
+
+// Which expansion plan the device path uses for a tensor of rank R (kernel, CTA shape, where
+// A1k lives, k-steps, DFMA ranks), e.g. for logs next to timings.
+inline std::string expansion_plan(Index R) {
+    char buf[256];
+    cuda::check(ls_expand_plan_name(static_cast<int>(R), buf, static_cast<int>(sizeof(buf))), "expansion_plan");
+    return buf;
+}
 
 // RAII device buffer for callers without the CUDA headers.
 class DeviceBuffer {

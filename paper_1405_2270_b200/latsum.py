@@ -499,6 +499,13 @@ def functional_batch(P: CanonicalTensor3, rho: Sequence[np.ndarray], scale: floa
     return out.cpu().numpy()[:F]
 
 
+def expansion_plan(R: int) -> str:
+    """The expansion plan the device path takes for rank R (ls_expand_plan_name)."""
+    buf = C.create_string_buffer(256)
+    call("ls_expand_plan_name", int(R), buf, 256)
+    return buf.value.decode()
+
+
 def grid_functional_batch(P: CanonicalTensor3, rho: Sequence[np.ndarray], scale: float = 1.0,
                           max_chunk_points: int = 1 << 28) -> np.ndarray:
     """Full-grid form of functional_batch: P is expanded on the device in

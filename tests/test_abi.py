@@ -91,6 +91,18 @@ def test_device_work_without_a_gpu_fails_loudly():
         L.densify(L.CanonicalTensor3([np.ones((2, 1))] * 3, np.ones(1)))
 
 
+def test_expansion_plan_names():
+    """Plan selection is host logic (no device needed): BASELINE rank 41 takes the 8-warp TMEM
+    kernel compiled for KD 10; 2-charge rank 82 the 16-warp TMEM one; cfg3's 328 the smem plan."""
+    assert L.expansion_plan(41).startswith("expand_tmem_kernel, 8 warps x 2 CTAs/SM")
+    assert "KD 10 (compiled)" in L.expansion_plan(41)
+    assert L.expansion_plan(82).startswith("expand_tmem_kernel, 16 warps x 1 CTA/SM")
+    assert "TileLR16" in L.expansion_plan(328)
+    assert "256-rank chunks" in L.expansion_plan(600)
+    with pytest.raises(L.ValidationError):
+        L.expansion_plan(-1)
+
+
 def test_python_mirror_validation():  # lattice.hpp:57-68, grid.hpp:21-27, canonical.hpp:42-56
     with pytest.raises(L.ValidationError):
         L.GridSpec(2.0, 3)
