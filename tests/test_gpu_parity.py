@@ -252,6 +252,12 @@ def test_cfg1_sampled_slabs_match_oracle(L, orc):
     scale = float(v.abs().max())
     assert float((v - torch.flip(v, dims=[2])).abs().max()) <= 1e-13 * scale
     assert float((out[100] - out[100].T).abs().max()) <= 1e-13 * scale
+    # every slab, including the last round's units that the store-only schedule splits at stage
+    # granularity: z-mirror symmetry of the whole grid, chunk by chunk
+    for k0 in range(0, N[2] // 2, 128):
+        lo = out[k0:k0 + 128]
+        hi = torch.flip(out[N[2] - k0 - 128:N[2] - k0], dims=[0])
+        assert float((lo - hi).abs().max()) <= 1e-13 * scale, k0
 
 
 def test_cfg2_functional_and_slabs(L, orc):
