@@ -476,13 +476,20 @@ TmemShape tmem_shape_for(int KD, int n_tail) {
     return fits_tmem_shape(KD, n_tail, {4, 1}) ? TmemShape{4, 1} : TmemShape{3, 1};
 }
 bool fits_tmem(int KD, int n_tail) { return fits_tmem_shape(KD, n_tail, tmem_shape_for(KD, n_tail)); }
-bool fits_tmem16(int KD, int n_tail) {
+// k-steps per stage of the 16-warp TMEM plan: the whole rank where the 2-deep ring holds it
+// (KD <= 23), else two stages of ceil(KD / 2) (KD 24..30); 0 if it does not fit at all.
+int tmem16_stage_ks(int KD, int n_tail) {
     n_tail = tmem_tail(n_tail);
-    if (n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(16)) return false;
+    if (n_tail > 1 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(16)) return 0;
     const size_t jt = TileTmem16::JT;
-    const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
-    return sizeof(double) * (32 + tmem_stg_elems(16) + TileTmem16::NS * stage) + 1024 <= kSmemPerSM;
+    for (int kc : {KD, (KD + 1) / 2}) {
+        const size_t stage = jt * kc * 32 + jt * 8 * n_tail;
+        if (sizeof(double) * (32 + tmem_stg_elems(16) + TileTmem16::NS * stage) + 1024 <= kSmemPerSM) return kc;
+        if (KD > 30) break;  // chunked instantiations exist for KD 24..30 only
+    }
+    return 0;
 }
+bool fits_tmem16(int KD, int n_tail) { return tmem16_stage_ks(KD, n_tail) > 0; }
 
 template <class T>
 bool fits(int KD, int KC, int n_tail) {
@@ -531,7 +538,7 @@ bool plan_for(int KD, int n_tail, Plan& out) {
         }
         if (ok) {
             const int pad = c.id == kPlanTmem16 && n_tail == 2;
-            out = {c.id, KC + pad, ic, pad};
+            out = {c.id, c.id == kPlanTmem16 ? tmem16_stage_ks(KD + pad, pad ? 0 : n_tail) : KC + pad, ic, pad};
             if (const char* e = std::getenv("LS_EXPAND_KC")) out.KC = std::max(1, std::min(KD, std::atoi(e)));
             return true;
         }
@@ -577,7 +584,7 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         TMEM ? (T::WARPS == 16 ? TmemShape{T::NS, 1} : tmem_shape_for(a.KD, a.n_tail)) : TmemShape{T::NS, 1};
     const int JT = T::JT * sh.jps, JC = T::JC * sh.jps;
     if (TMEM) {
-        a.KC = a.KD;
+        if (T::WARPS == 8) a.KC = a.KD;  // the 16-warp plan keeps its planned stage size (k-chunks)
         a.n_tail = tmem_tail(a.n_tail);
     }
     a.n_ichunks = ls::ceil_div(a.N1, T::IC);
@@ -613,7 +620,7 @@ int launch(ExpandArgs& a, cudaStream_t s) {
             return ls::fail(LS_EVALIDATION, "expand: TMEM plan needs one DFMA rank (two with 8 warps)");
         if constexpr (T::WARPS == 16) {
             static_assert(T::NS == 2, "the 16-warp TMEM kernels are built with a 2-deep ring");
-            kern = tmem16_kernel(STORE, FUNC, a.KD);
+            kern = tmem16_kernel(STORE, FUNC, a.KD, a.KC);
         } else {
             kern = tmem8_kernel(STORE, FUNC, code, a.KD, a.n_tail);
             if (!kern) return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
@@ -636,7 +643,7 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         const int64_t full = a.n_units / G, tail = a.n_units - full * G;
         const int64_t whole = ls::ceil_div(a.n_units, G) * a.n_jc;
         const int64_t split = full * a.n_jc + ls::ceil_div(tail * a.n_jc, G);
-        if (tail > 0 && split + 2 <= whole) {
+        if (tail > 0 && split + 2 <= whole && a.n_kc == 1) {
             a.split_tail = 1;
             grid = std::min<int64_t>(a.n_units * a.n_jc, G);
         }
@@ -712,7 +719,7 @@ extern "C" int ls_expand_plan_name(int R, char* out, int len) {
     std::snprintf(out, static_cast<size_t>(len), "%s; plan %d, KD %d (%s), %d DFMA rank(s)%s", shape, pl.id, kd,
                   (pl.id == kPlanTmem && kd <= 14) || (pl.id == kPlanTmem16 && kd >= 15 && kd <= 23)
                       ? "compiled"
-                      : "runtime",
+                      : (pl.id == kPlanTmem16 && kd >= 24 && kd <= 30 ? "compiled, two stages per tile" : "runtime"),
                   nt, whole ? "" : ", 256-rank chunks");
     return LS_OK;
 }

@@ -81,7 +81,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // KD_ > 0 fixes the k-step count at compile time (the 8-warp shape is instantiated for every
 // KD it covers): the k-step loop is then fully unrolled with immediate shared-memory and TMEM
 // offsets, 2.2% faster at cfg1 than the runtime-KD loop. KD_ = 0 reads p.KD.
-template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8, int KD_ = 0, int NT_ = 1>
+// KC_ > 0 (16-warp shape, compile-time KD_ only): stages of KC_ k-steps, two per j-chunk, for
+// ranks whose whole-rank stage no longer fits the shared-memory ring (KD 24..30); the
+// accumulators persist across the two stages of a tile.
+template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8, int KD_ = 0, int NT_ = 1, int KC_ = 0>
 __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_kernel(const ExpandArgs p) {
     constexpr int WARPS = WARPS_, WI = 4, WJ = WARPS / WI, kTM = 4, kTN = 4, IC = 128, JT = kTM * WJ * JPS,
                   JC = 8 * kTM * WJ, kNS = NS;
@@ -90,11 +93,15 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     const int KD = KD_ > 0 ? KD_ : p.KD;
     constexpr int n_tail = NT_;  // 1 or 2 DFMA ranks (launch() makes a zero rank when R mod 4 is 0 or 3)
     const int CB = 8 * KD + 16 * n_tail;
-    const int frag_elems = JT * KD * 32;
+    constexpr bool kChunked = KC_ > 0;
+    static_assert(!kChunked || (KD_ > KC_ && KD_ <= 2 * KC_ && JPS == 1), "k-chunked stages: two per tile");
+    const int KCs = kChunked ? KC_ : KD;          // k-steps per stage
+    constexpr int n_kc = kChunked ? 2 : 1;        // stages per tile
+    const int frag_elems = JT * KCs * 32;
     const int stage_elems = frag_elems + JT * 8 * n_tail;
     const int n_ichunks = static_cast<int>(p.n_ichunks);
     const int n_units = static_cast<int>(p.n_units);
-    const int per_unit = static_cast<int>(p.n_jc);
+    const int per_unit = static_cast<int>(p.n_jc) * n_kc;
     const unsigned stage_bytes = static_cast<unsigned>(stage_elems * sizeof(double));
 
     // Shared-memory header (256 bytes): 16 mbarrier slots, then the slot counters and the TMEM
@@ -121,7 +128,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     // CTAs) the whole-unit tail left 1.2% of the GPU idle. Functional launches keep whole units
     // (one writer per per-warp partial).
     const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
-    const bool kSplitTail = STORE && !FUNC && p.split_tail;
+    const bool kSplitTail = STORE && !FUNC && !kChunked && p.split_tail;
     const int n_full = kSplitTail ? n_units / G : 0;
     int t0 = 0, t1 = 0, tu0 = 0, n_tu = 0;  // this CTA's stages [t0, t1) of the tail round
     if (kSplitTail) {
@@ -139,7 +146,9 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     auto unit_of = [&](int n) { return n < n_full || !kSplitTail ? b + n * G : n_full * G + tu0 + (n - n_full); };
 
     auto issue = [&](int st) {
-        const int c = (kSplitTail && st >= full_stages) ? (t0 + st - full_stages) % per_unit : st % per_unit;
+        const int w = (kSplitTail && st >= full_stages) ? (t0 + st - full_stages) % per_unit : st % per_unit;
+        // packed stage (k-chunk kcs, j-chunk jc) sits at (kcs * n_jc + jc) (pack_b_kernel)
+        const int c = kChunked ? (w % n_kc) * static_cast<int>(p.n_jc) + w / n_kc : w;
         const double* src = p.Bp + static_cast<int64_t>(c) * stage_elems;
         uint64_t* bar = full + (st % kNS);
         mbar_arrive_expect_tx(bar, stage_bytes);
@@ -339,11 +348,13 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         }
         int next_task = 0;
 
-        for (int jc = jc_lo; jc < jc_hi; ++jc, ++st) {
+        for (int w = jc_lo; w < jc_hi; ++w, ++st) {
+            const int jc = kChunked ? w / n_kc : w;  // j-chunk of this stage
+            const int kc = kChunked ? w % n_kc : 0;  // k-chunk of this stage
             // Fill task(s) for the next unit: loads now, product + TMEM store after the DMMAs.
             int target = next_task;
             if (has_next)
-                while (target < n_tasks && fill_stage(target) <= jc) ++target;
+                while (target < n_tasks && fill_stage(target) <= w) ++target;
             const bool fill_now = target > next_task;
             if (fill_now && next_task == 0 && n >= 1)  // buffer buf^1 was read by unit n-1
                 mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1));
@@ -354,6 +365,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
 #pragma unroll 1
             for (int h = 0; h < JPS; ++h) {
                 const int jt0 = h * (kTM * WJ) + wj * kTM;  // first j-tile of this warp's tile in the stage
+                if (kc == 0) {
 #pragma unroll
                 for (int m = 0; m < kTM; ++m)
 #pragma unroll
@@ -379,14 +391,16 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                             acc[m][nn][1] = fma(atx[2 * nn + 1], bt[m], acc[m][nn][1]);
                         }
                 }
+                }  // kc == 0
                 {
-                    const double* bsw = stage + jt0 * (KD * 32) + lane;
+                    const double* bsw = stage + jt0 * (KCs * 32) + lane;
+                    const int ks0 = kc * KCs;  // first k-step of this stage
                     auto kstep = [&](int ks) {
                         double a[kTM], b[kTN];
                         uint32_t rb[8];
                         tmem::ld_x8_issue(tb + 8 * ks, rb);
 #pragma unroll
-                        for (int m = 0; m < kTM; ++m) a[m] = bsw[m * (KD * 32) + ks * 32];
+                        for (int m = 0; m < kTM; ++m) a[m] = bsw[m * (KCs * 32) + (ks - ks0) * 32];
                         tmem::wait_ld(rb);
                         tmem::unpack(rb, b);
 #pragma unroll
@@ -394,7 +408,15 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
 #pragma unroll
                             for (int nn = 0; nn < kTN; ++nn) dmma_884(acc[m][nn][0], acc[m][nn][1], a[m], b[nn]);
                     };
-                    if constexpr (KD_ > 0) {
+                    if constexpr (kChunked) {
+                        if (kc == 0) {
+#pragma unroll
+                            for (int ks = 0; ks < KC_; ++ks) kstep(ks);
+                        } else {
+#pragma unroll
+                            for (int ks = KC_; ks < (KD_ > 0 ? KD_ : 1); ++ks) kstep(ks);
+                        }
+                    } else if constexpr (KD_ > 0) {
                         // compile-time k-step count: fully unrolled (2.2% faster at cfg1 than the
                         // rolled loop with the same constant bounds)
 #pragma unroll
@@ -424,6 +446,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                     }
                 }
 
+                if (kChunked && kc != n_kc - 1) continue;  // the tile continues in the next stage
                 // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
                 const int jb = (jc * JPS + h) * JC + wj * (8 * kTM);
                 const int ibase = ib + wi * (8 * kTN);

@@ -7,7 +7,8 @@
 namespace ls_k3 {
 namespace {
 
-// Compile-time k-step count over the range the 16-warp plan covers (KD 15..23), 2-deep ring.
+// Compile-time k-step count over the range the 16-warp plan covers with whole-rank stages
+// (KD 15..23), 2-deep ring.
 template <bool STORE, bool FUNC, int... KD>
 KernelFn pick(int kd, std::integer_sequence<int, KD...>) {
     KernelFn k = nullptr;
@@ -15,18 +16,27 @@ KernelFn pick(int kd, std::integer_sequence<int, KD...>) {
     return k;
 }
 
+// KD 24..30: two stages of ceil(KD / 2) k-steps per tile.
+template <bool STORE, bool FUNC, int... KD>
+KernelFn pick_chunked(int kd, std::integer_sequence<int, KD...>) {
+    KernelFn k = nullptr;
+    ((kd == KD + 24 ? (k = expand_tmem_kernel<STORE, FUNC, 2, 1, 16, KD + 24, 1, (KD + 25) / 2>, 0) : 0), ...);
+    return k;
+}
+
 template <bool STORE, bool FUNC>
-KernelFn kernel(int kd) {
+KernelFn kernel(int kd, int kc) {
+    if (kc < kd) return kc == (kd + 1) / 2 ? pick_chunked<STORE, FUNC>(kd, std::make_integer_sequence<int, 7>{}) : nullptr;
     if (KernelFn k = pick<STORE, FUNC>(kd, std::make_integer_sequence<int, 9>{})) return k;
     return expand_tmem_kernel<STORE, FUNC, 2, 1, 16>;
 }
 
 }  // namespace
 
-KernelFn tmem16_kernel(bool store, bool func, int kd) {
-    if (store && func) return kernel<true, true>(kd);
-    if (store) return kernel<true, false>(kd);
-    if (func) return kernel<false, true>(kd);
+KernelFn tmem16_kernel(bool store, bool func, int kd, int kc) {
+    if (store && func) return kernel<true, true>(kd, kc);
+    if (store) return kernel<true, false>(kd, kc);
+    if (func) return kernel<false, true>(kd, kc);
     return nullptr;
 }
 

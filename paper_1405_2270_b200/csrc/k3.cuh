@@ -102,7 +102,8 @@ using KernelFn = void (*)(ExpandArgs);
 // 8-warp TMEM kernel for ring shape `code` (10 * depth + j-chunks per stage), KD k-steps and
 // nt DFMA ranks; nullptr if the shape is not built. Compile-time KD for KD 1..14 with nt = 1.
 KernelFn tmem8_kernel(bool store, bool func, int code, int kd, int nt);
-// 16-warp TMEM kernel (2-deep ring, one DFMA rank); compile-time KD for KD 15..23.
-KernelFn tmem16_kernel(bool store, bool func, int kd);
+// 16-warp TMEM kernel (2-deep ring, one DFMA rank); compile-time KD for KD 15..23 with whole-
+// rank stages (kc == kd) and for KD 24..30 with two stages of kc = ceil(kd / 2) k-steps.
+KernelFn tmem16_kernel(bool store, bool func, int kd, int kc);
 
 }  // namespace ls_k3

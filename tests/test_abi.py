@@ -97,6 +97,7 @@ def test_expansion_plan_names():
     assert L.expansion_plan(41).startswith("expand_tmem_kernel, 8 warps x 2 CTAs/SM")
     assert "KD 10 (compiled)" in L.expansion_plan(41)
     assert L.expansion_plan(82).startswith("expand_tmem_kernel, 16 warps x 1 CTA/SM")
+    assert "two stages per tile" in L.expansion_plan(113)
     assert "TileLR16" in L.expansion_plan(328)
     assert "256-rank chunks" in L.expansion_plan(600)
     with pytest.raises(L.ValidationError):
