@@ -41,6 +41,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 #include <utility>
 
 #include "common.cuh"
@@ -220,7 +221,7 @@ expand_dmma_kernel(const ExpandArgs p) {
             for (int e = threadIdx.x; e < n_tail * IC; e += kThreads) {
                 const int q = 4 * KD + e / IC;
                 const int i = ib + e % IC;
-                tail[e] = i < p.N1 ? rn_mul(__ldg(p.A + i + p.lda * q), sc[q]) : 0.0;
+                tail[e] = (i < p.N1 && q < p.R) ? rn_mul(__ldg(p.A + i + p.lda * q), sc[q]) : 0.0;
             }
             if (FUNC) {
                 fsum = 0.0;
@@ -587,6 +588,7 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         if (T::WARPS == 8) a.KC = a.KD;  // the 16-warp plan keeps its planned stage size (k-chunks)
         a.n_tail = tmem_tail(a.n_tail);
     }
+
     a.n_ichunks = ls::ceil_div(a.N1, T::IC);
     a.n_units = a.n_ichunks * (a.k1 - a.k0);
     a.n_jc = ls::ceil_div(a.N2, JC);
