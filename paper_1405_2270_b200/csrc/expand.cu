@@ -530,9 +530,11 @@ bool plan_for(int KD, int n_tail, Plan& out) {
             // ranks 58-90 that beats plan 9 by 12-22% (tools/profile_rank_sweep.py, 512 slabs).
             // For the 8-warp plan the padding costs what it gains (rank 42: 27.8 vs 28.6 TF/s
             // for plan 0 with a 2-rank DFMA tail), so it keeps n_tail <= 1.
-            // Below KD 15 the 8-warp plans are faster (rank 42: 26.8 TF/s here vs 28.6 for plan 0).
+            // Below KD 15 it only takes ranks the 8-warp TMEM plan cannot (rank 54: a 2-rank
+            // remainder at KD 13 overflows 256 columns); the 8-warp plan is faster at ranks 33-45.
             case kPlanTmem16:
-                ok = (force == kPlanTmem16 || KD + (n_tail == 2) > 14) && fits_tmem16(KD + (n_tail == 2), n_tail == 2 ? 0 : n_tail);
+                ok = (force == kPlanTmem16 || KD + (n_tail == 2) > 14 || !fits_tmem(KD, n_tail)) &&
+                     fits_tmem16(KD + (n_tail == 2), n_tail == 2 ? 0 : n_tail);
                 ic = TileTmem16::IC;
                 break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
@@ -719,7 +721,7 @@ extern "C" int ls_expand_plan_name(int R, char* out, int len) {
                         : pl.id == 9           ? "expand_dmma_kernel TileLR16, 16 warps x 1 CTA/SM, A1k in smem"
                                                : "expand_dmma_kernel, A1k in smem";
     std::snprintf(out, static_cast<size_t>(len), "%s; plan %d, KD %d (%s), %d DFMA rank(s)%s", shape, pl.id, kd,
-                  (pl.id == kPlanTmem && kd <= 14) || (pl.id == kPlanTmem16 && kd >= 15 && kd <= 23)
+                  (pl.id == kPlanTmem && kd <= 14) || (pl.id == kPlanTmem16 && kd >= 14 && kd <= 23)
                       ? "compiled"
                       : (pl.id == kPlanTmem16 && kd >= 24 && kd <= 30 ? "compiled, two stages per tile" : "runtime"),
                   nt, whole ? "" : ", 256-rank chunks");

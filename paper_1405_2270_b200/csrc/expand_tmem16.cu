@@ -8,11 +8,11 @@ namespace ls_k3 {
 namespace {
 
 // Compile-time k-step count over the range the 16-warp plan covers with whole-rank stages
-// (KD 15..23), 2-deep ring.
+// (KD 14..23; 14 for rank 54, whose 2-rank remainder the 8-warp plan cannot hold), 2-deep ring.
 template <bool STORE, bool FUNC, int... KD>
 KernelFn pick(int kd, std::integer_sequence<int, KD...>) {
     KernelFn k = nullptr;
-    ((kd == KD + 15 ? (k = expand_tmem_kernel<STORE, FUNC, 2, 1, 16, KD + 15>, 0) : 0), ...);
+    ((kd == KD + 14 ? (k = expand_tmem_kernel<STORE, FUNC, 2, 1, 16, KD + 14>, 0) : 0), ...);
     return k;
 }
 
@@ -27,7 +27,7 @@ KernelFn pick_chunked(int kd, std::integer_sequence<int, KD...>) {
 template <bool STORE, bool FUNC>
 KernelFn kernel(int kd, int kc) {
     if (kc < kd) return kc == (kd + 1) / 2 ? pick_chunked<STORE, FUNC>(kd, std::make_integer_sequence<int, 7>{}) : nullptr;
-    if (KernelFn k = pick<STORE, FUNC>(kd, std::make_integer_sequence<int, 9>{})) return k;
+    if (KernelFn k = pick<STORE, FUNC>(kd, std::make_integer_sequence<int, 10>{})) return k;
     return expand_tmem_kernel<STORE, FUNC, 2, 1, 16>;
 }
 
