@@ -84,13 +84,14 @@ int ls_assemble_axis(const double* master_d, int64_t ld_master, int R, int M0, c
  * z-slab range [k0, k1): V(i,j,k) = sum_q (A(i,q) * (w_q*C(k,q))) * B(j,q),
  * written to out_d[(k-k0)*ldz + j*ldy + i] (ldy >= N1, ldz >= ldy*N2; pass
  * 0 for the dense defaults ldy = N1, ldz = N1*N2). FP64 DMMA tensor-core
- * tiles; one z-shard per call, no inter-GPU traffic.
+ * tiles with the scaled left factor resident in tensor memory for ranks up
+ * to 121, in shared memory beyond (ls_expand_plan_name); one z-shard per
+ * call, no inter-GPU traffic. Bitwise deterministic run to run.
  * Optional fused epilogue (BASELINE functional): when rho1_d
- * is non-NULL, partial_d[u] receives the separable-rho weighted sum
- *     sum_{i,j in unit u} V(i,j,k) * rho1(i) * rho2(j) * rho3(k)
- * for every work unit u (deterministic order); reduce with
- * ls_sum_partials. out_d may be NULL to skip storing the grid.
- * ls_expand_partial_count() gives the number of units for a shape. */
+ * is non-NULL, partial_d receives ls_expand_partial_count() partial sums of
+ *     sum_{i,j,k} V(i,j,k) * rho1(i) * rho2(j) * rho3(k)
+ * (one per work unit and warp, each in a fixed order); reduce them with
+ * ls_sum_partials. out_d may be NULL to skip storing the grid. */
 int ls_expand(const double* A_d, int64_t lda, const double* B_d, int64_t ldb, const double* C_d,
               int64_t ldc, const double* w_d, int64_t N1, int64_t N2, int64_t N3, int R, int64_t k0,
               int64_t k1, double* out_d, int64_t ldy, int64_t ldz, const double* rho1_d,
