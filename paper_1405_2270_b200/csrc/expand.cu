@@ -439,7 +439,7 @@ struct Plan {
     int pad = 0;  // 1: run a 2-rank remainder as one zero-padded k-step (TMEM plans have a 1-rank tail)
 };
 
-constexpr int kPlanTmem = 20, kPlanTmem16 = 21;
+constexpr int kPlanTmem = 20, kPlanTmem16 = 21, kPlanSplitK = 22;
 // TMEM variant shape (ring depth, j-chunks per stage); LS_EXPAND_TMEM=<ns><jps> overrides.
 struct TmemShape {
     int ns, jps;
@@ -510,8 +510,8 @@ bool plan_for(int KD, int n_tail, Plan& out) {
     // with a 64-row i-chunk (29.0) or 16-row warp tiles (no fit) were slower).
     // Up to KD 14 the 2-CTA TileWide with 8-k-step stages beats the 16-warp plan 9 (rank 46:
     // 27.1 vs 22.0 TF/s); beyond it plan 9 wins (rank 123: 26.4 vs 24.2).
-    const Cand small_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {0, 0}, {0, 8}, {9, 4}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
-    const Cand large_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {0, 0}, {9, 4}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
+    const Cand small_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {kPlanSplitK, 0}, {0, 0}, {0, 8}, {9, 4}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
+    const Cand large_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {kPlanSplitK, 0}, {0, 0}, {9, 4}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
     for (const Cand& c : KD <= 14 ? small_r : large_r) {
         if (force >= 0 && c.id != force) continue;
         const int KC = c.KC == 0 ? KD : std::min(KD, c.KC);
@@ -537,6 +537,8 @@ bool plan_for(int KD, int n_tail, Plan& out) {
                      fits_tmem16(KD + (n_tail == 2), n_tail == 2 ? 0 : n_tail);
                 ic = TileTmem16::IC;
                 break;
+            // beyond the double-buffered TMEM plans (rank 122 on; cfg3's 328)
+            case kPlanSplitK: ok = (force == kPlanSplitK || KD >= 30) && fits_splitk(KD, tmem_tail(n_tail)); ic = 64; break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
         }
         if (ok) {
@@ -682,6 +684,9 @@ int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
     switch (pl.id) {
         case kPlanTmem: return launch<TileWide, STORE, FUNC, true>(a, s);
         case kPlanTmem16: return launch<TileTmem16, STORE, FUNC, true>(a, s);
+        case kPlanSplitK:
+            a.n_tail = tmem_tail(a.n_tail);
+            return launch_splitk(a, STORE, FUNC, s, ls::sm_count(), kernel_setup);
         case 0: return launch<TileWide, STORE, FUNC>(a, s);
         case 1: return launch<TileWide3, STORE, FUNC>(a, s);
         case 2: return launch<TileMid, STORE, FUNC>(a, s);
@@ -704,7 +709,7 @@ extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_
     if (!plan_for(KD, n_tail, pl) && !chunk_plan(pl)) return -1;
     const int64_t IC = pl.ic;
     // the TMEM variant writes one partial per warp (no CTA barrier per unit)
-    return ls::ceil_div(N1, IC) * (k1 - k0) * (pl.id == kPlanTmem ? 8 : pl.id == kPlanTmem16 ? 16 : 1);
+    return ls::ceil_div(N1, IC) * (k1 - k0) * (pl.id == kPlanTmem ? 8 : pl.id == kPlanTmem16 || pl.id == kPlanSplitK ? 16 : 1);
 }
 
 extern "C" int ls_expand_plan_name(int R, char* out, int len) {
@@ -715,9 +720,10 @@ extern "C" int ls_expand_plan_name(int R, char* out, int len) {
     const bool whole = plan_for(KD, n_tail, pl);
     if (!whole && !chunk_plan(pl)) return ls::fail(LS_EGUARD, "expand_plan_name: no tile plan");
     const int kd = pl.pad && n_tail == 2 ? KD + 1 : KD;
-    const int nt = pl.id == kPlanTmem || pl.id == kPlanTmem16 ? (pl.pad ? 1 : tmem_tail(n_tail)) : n_tail;
+    const int nt = pl.id == kPlanTmem || pl.id == kPlanTmem16 || pl.id == kPlanSplitK ? (pl.pad ? 1 : tmem_tail(n_tail)) : n_tail;
     const char* shape = pl.id == kPlanTmem     ? "expand_tmem_kernel, 8 warps x 2 CTAs/SM, A1k in TMEM"
                         : pl.id == kPlanTmem16 ? "expand_tmem_kernel, 16 warps x 1 CTA/SM, A1k in TMEM"
+                        : pl.id == kPlanSplitK ? "expand_splitk_kernel, 16 warps x 1 CTA/SM, A1k halves in TMEM lane quarters"
                         : pl.id == 9           ? "expand_dmma_kernel TileLR16, 16 warps x 1 CTA/SM, A1k in smem"
                                                : "expand_dmma_kernel, A1k in smem";
     std::snprintf(out, static_cast<size_t>(len), "%s; plan %d, KD %d (%s), %d DFMA rank(s)%s", shape, pl.id, kd,

@@ -106,4 +106,9 @@ KernelFn tmem8_kernel(bool store, bool func, int code, int kd, int nt);
 // rank stages (kc == kd) and for KD 24..30 with two stages of kc = ceil(kd / 2) k-steps.
 KernelFn tmem16_kernel(bool store, bool func, int kd, int kc);
 
+// Split-K TMEM plan for ranks beyond the double-buffered TMEM plans (expand_splitk.cu).
+bool fits_splitk(int KD, int n_tail);
+int launch_splitk(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_count,
+                  int (*setup)(const void*, int, size_t, int&));
+
 }  // namespace ls_k3
