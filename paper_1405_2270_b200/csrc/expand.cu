@@ -537,8 +537,10 @@ bool plan_for(int KD, int n_tail, Plan& out) {
                      fits_tmem16(KD + (n_tail == 2), n_tail == 2 ? 0 : n_tail);
                 ic = TileTmem16::IC;
                 break;
-            // beyond the double-buffered TMEM plans (rank 122 on; cfg3's 328)
-            case kPlanSplitK: ok = (force == kPlanSplitK || KD >= 30) && fits_splitk(KD, tmem_tail(n_tail)); ic = 64; break;
+            // Beyond the double-buffered TMEM plans. At ranks 122-164 the smem plan 9 measured
+            // 2-4% faster on 1024^2 slabs (the split-K unit's exposed A1k fill weighs more there);
+            // from rank ~180 on split-K wins: rank 246 29.2 vs 28.9 TF/s, cfg3's 328 32.0 vs 30.8.
+            case kPlanSplitK: ok = (force == kPlanSplitK || KD >= 44) && fits_splitk(KD, tmem_tail(n_tail)); ic = 64; break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
         }
         if (ok) {
