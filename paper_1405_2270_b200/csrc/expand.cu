@@ -32,9 +32,13 @@
 //    4-rank DMMA step.
 // No CTA barrier per stage: each warp releases a ring slot after its last
 // DMMA of the stage and the last one refills it. Units are spread over a
-// persistent grid (CTAs per SM x SM count). expand_tmem.cuh holds the default
-// variant for ranks up to 93, with A1k resident in tensor memory (instantiated in
-// expand_tmem8.cu / expand_tmem16.cu); k3.cuh the definitions they share.
+// persistent grid (CTAs per SM x SM count). Plans by rank (plan_for):
+//   * ranks <= 121: expand_tmem.cuh, A1k double-buffered in tensor memory (8 warps x 2 CTAs
+//     or 16 warps x 1 CTA per SM; instantiated in expand_tmem8.cu / expand_tmem16.cu);
+//   * ranks >= 176 (KD <= 120): expand_splitk.cu, A1k k-halves in different TMEM lane
+//     quarters with a pair reduction;
+//   * otherwise this file's expand_dmma_kernel with A1k in shared memory;
+// k3.cuh holds the definitions they share.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
