@@ -23,7 +23,10 @@ namespace {
 #ifndef LS_SK_KC
 #define LS_SK_KC 6
 #endif
-constexpr int kSkWarps = 16, kSkIC = 64, kSkJT = 16, kSkNS = 2, kSkKC = LS_SK_KC;
+#ifndef LS_SK_NS
+#define LS_SK_NS 2
+#endif
+constexpr int kSkWarps = 16, kSkIC = 64, kSkJT = 16, kSkNS = LS_SK_NS, kSkKC = LS_SK_KC;
 constexpr int kSkRedElems = 8 * 32 * 32;  // 8 warp pairs x 32 lanes x 32 accumulators
 
 // A2 of stage (k-chunk kc, j-chunk jc) at Bp + (kc * n_jc + jc) * stage_elems:
@@ -94,8 +97,9 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
     extern __shared__ __align__(128) double smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);          // [2] A2 stage landed
     uint64_t* ready = full + kSkNS;                               // [8] pair partial written
-    int* released = reinterpret_cast<int*>(smem + 16);            // [2] warps done with a slot
-    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 17);
+    int* released = reinterpret_cast<int*>(smem + 16);            // [kSkNS <= 8] warps done with a slot
+    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 20);
+    static_assert(kSkNS + 8 <= 16 && kSkNS <= 8, "header: ring + pair barriers, counters, TMEM base");
     double* red = smem + 32;                                      // [8][32 accumulators][32 lanes]
     double* ring = red + kSkRedElems;                             // [2][stage_elems]
 
