@@ -143,14 +143,23 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
     if (threadIdx.x == 0)
         for (int st = 0; st < kSkNS && st < n_stages; ++st) issue(st);
 
-    // This warp's share of unit u's A1k: k-steps kl = wj, wj + 4, ... of its half (the four
-    // i-tiles of its rows), then (kh == 0, wj == 0) the tail ranks. Rounds like Eigen's
-    // A1 * scale.asDiagonal().
-    auto fill = [&](int u) {
+    // A1k buffers: double-buffered when two fit in 512 columns (KD <= 60), else one. With two,
+    // the warps write the next unit's A1k into the idle buffer piece by piece between the
+    // current unit's stages; with one, after the unit barrier (exposed, ~1% of a cfg3 unit).
+    const int CB = 8 * KH + 16 * n_tail;
+    const bool dbuf = 2 * CB <= 512;
+    // This warp's fill tasks of a unit: frag task f writes k-step kl = wj + 4 f of its half (the
+    // four i-tiles of its rows); then (kh == 0, wj == 0) one task per tail rank.
+    const int n_frag_tasks = nks > wj ? (nks - wj + 3) / 4 : 0;
+    const int n_tasks = n_frag_tasks + ((kh == 0 && wj == 0) ? n_tail : 0);
+    // Tasks [t0, t1) of unit u into buffer buf. Rounds like Eigen's A1 * scale.asDiagonal().
+    auto fill = [&](int u, int buf, int t0, int t1) {
         const int ib = (u % n_ichunks) * kSkIC + 32 * rg;
         const double* S = p.S + (p.k0 + u / n_ichunks) * p.R;
-#pragma unroll 4
-        for (int kl = wj; kl < nks; kl += 4) {
+        const uint32_t col = static_cast<uint32_t>(buf * CB);
+#pragma unroll 1
+        for (int task = t0; task < t1 && task < n_frag_tasks; ++task) {
+            const int kl = wj + 4 * task;
             const int qq = 4 * (kh * KH + kl) + t;
             const double sv = qq < p.R ? __ldg(S + qq) : 0.0;
             double v[4];
@@ -159,26 +168,25 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
                 const int i = ib + 8 * it + g;
                 v[it] = (i < p.N1 && qq < p.R) ? rn_mul(__ldg(p.A + i + p.lda * qq), sv) : 0.0;
             }
-            tmem::st_x8(tq + 8 * kl, v);
+            tmem::st_x8(tq + col + 8 * kl, v);
         }
-        if (kh == 0 && wj == 0) {
-            for (int qt = 0; qt < n_tail; ++qt) {
-                const int qq = 4 * KD + qt;
-                const double sv = qq < p.R ? __ldg(S + qq) : 0.0;
-                double v0[4], v1[4];
+        for (int task = t0 > n_frag_tasks ? t0 : n_frag_tasks; task < t1 && task < n_tasks; ++task) {
+            const int qt = task - n_frag_tasks;
+            const int qq = 4 * KD + qt;
+            const double sv = qq < p.R ? __ldg(S + qq) : 0.0;
+            double v0[4], v1[4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int i = ib + 8 * (e >> 1) + 2 * t + (e & 1);
-                    const double x = (i < p.N1 && qq < p.R) ? rn_mul(__ldg(p.A + i + p.lda * qq), sv) : 0.0;
-                    if (e < 4) v0[e] = x;
-                    else v1[e - 4] = x;
-                }
-                tmem::st_x8(tq + 8 * KH + 16 * qt, v0);
-                tmem::st_x8(tq + 8 * KH + 16 * qt + 8, v1);
+            for (int e = 0; e < 8; ++e) {
+                const int i = ib + 8 * (e >> 1) + 2 * t + (e & 1);
+                const double x = (i < p.N1 && qq < p.R) ? rn_mul(__ldg(p.A + i + p.lda * qq), sv) : 0.0;
+                if (e < 4) v0[e] = x;
+                else v1[e - 4] = x;
             }
+            tmem::st_x8(tq + col + 8 * KH + 16 * qt, v0);
+            tmem::st_x8(tq + col + 8 * KH + 16 * qt + 8, v1);
         }
-        tmem::wait_st();
     };
+    if (dbuf && my_units > 0) fill(b, 0, 0, n_tasks);  // prologue: the first unit, all tasks
 
     double acc[kTM][kTN][2];
     double fsum = 0.0;
@@ -187,14 +195,22 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
         const int unit = b + n * G;
         const int ib = (unit % n_ichunks) * kSkIC;
         const int64_t kk = unit / n_ichunks;
-        // Single-buffered A1k: every warp is past the previous unit before it is overwritten.
+        const int buf = dbuf ? (n & 1) : 0;
+        // Unit barrier: every warp is past the previous unit (its buffer may be overwritten) and
+        // has written its share of this unit's A1k (double-buffered: during the previous unit).
+        tmem::wait_st();
         tmem::fence_before();
         __syncthreads();
         tmem::fence_after();
-        fill(unit);
-        tmem::fence_before();
-        __syncthreads();
-        tmem::fence_after();
+        if (!dbuf) {
+            fill(unit, 0, 0, n_tasks);
+            tmem::wait_st();
+            tmem::fence_before();
+            __syncthreads();
+            tmem::fence_after();
+        }
+        const uint32_t tb = tq + static_cast<uint32_t>(buf * CB);
+        const bool fill_next = dbuf && n + 1 < my_units;
         double r1[kTN][2];
         if (FUNC) {
             fsum = 0.0;
@@ -226,8 +242,8 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
 #pragma unroll
                         for (int m = 0; m < kTM; ++m) bt[m] = tbp[m * 8 * n_tail];
                         double at0[4], at1[4];
-                        tmem::ld_x8(tq + 8 * KH + 16 * qt, at0);
-                        tmem::ld_x8(tq + 8 * KH + 16 * qt + 8, at1);
+                        tmem::ld_x8(tb + 8 * KH + 16 * qt, at0);
+                        tmem::ld_x8(tb + 8 * KH + 16 * qt + 8, at1);
                         const double atx[8] = {at0[0], at0[1], at0[2], at0[3], at1[0], at1[1], at1[2], at1[3]};
 #pragma unroll
                         for (int nn = 0; nn < kTN; ++nn)
@@ -247,7 +263,7 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
                     if (kl0 + kk2 >= nks) break;
                     double a[kTM], bb[kTN];
                     uint32_t rb[8];
-                    tmem::ld_x8_issue(tq + 8 * (kl0 + kk2), rb);
+                    tmem::ld_x8_issue(tb + 8 * (kl0 + kk2), rb);
 #pragma unroll
                     for (int m = 0; m < kTM; ++m) a[m] = bsw[m * (KC * 32) + kk2 * 32];
                     tmem::wait_ld(rb);
@@ -268,6 +284,11 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     if (st + kSkNS < n_stages) issue(st + kSkNS);
                 }
+            }
+            // double-buffered: this stage's share of the next unit's fill tasks, after the DMMAs
+            if (fill_next) {
+                const int f0 = (w * n_tasks) / per_unit, f1 = ((w + 1) * n_tasks) / per_unit;
+                if (f1 > f0) fill(b + (n + 1) * G, buf ^ 1, f0, f1);
             }
             if (kc != n_kc - 1) continue;
 

@@ -24,7 +24,7 @@ def env():
 def _cases(n=120, seed=20261019):
     rng = np.random.default_rng(seed)
     ranks = [1, 2, 3, 4, 5, 8, 40, 41, 42, 43, 45, 46, 57, 58, 61, 70, 73, 82, 89, 93, 94, 105, 113, 121, 123, 164,
-             257, 300, 520]
+             178, 181, 199, 240, 257, 300, 520]
     for c in range(n):
         R = int(rng.choice(ranks))
         big = rng.integers(0, 4) == 0  # some cases span several 128-row i-chunks and j-chunks
