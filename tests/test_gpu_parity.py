@@ -291,6 +291,38 @@ def test_cfg2_functional_and_slabs(L, orc):
     assert abs(e_batch - e_1d) <= 1e-12 * abs(e_1d)
 
 
+def test_cfg2_whole_grid_one_gpu(L, orc):
+    """The whole 2048^3 grid (8.6e9 points, 64 GiB) in one device buffer: element offsets pass
+    2^32, so any 32-bit index in the store path would land in the wrong slab or fault. The last
+    slabs are checked against the oracle, the grid against its z-mirror, and the fused energy of
+    the stored grid against the streamed functional."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < 72 * 2**30:
+        pytest.skip("needs 72 GiB of free HBM")
+    spec, rule = cfg(L, 32)
+    pipe = L.DevicePipeline(spec, rule, mode="erf")
+    N = spec.target_dims()
+    out = torch.empty((N[2], N[1], N[0]), dtype=torch.float64, device="cuda")
+    pipe.step(out)
+    torch.cuda.synchronize()
+    _, fo, wo = oracle_assembled(orc, spec, rule, "erf", False)
+    for k in (N[2] - 1, N[2] // 2 + 3):
+        want = orc.densify_slabs(fo[0], fo[1], fo[2], wo, k, k + 1)[:, :, 0]
+        assert rel(out[k].cpu().numpy().T, want) <= 1e-12, k
+    scale = float(out[N[2] // 2].abs().max())
+    for k0 in range(0, N[2] // 2, 128):
+        lo = out[k0:k0 + 128]
+        hi = torch.flip(out[N[2] - k0 - 128:N[2] - k0], dims=[0])
+        assert float((lo - hi).abs().max()) <= 1e-13 * scale, k0
+    h = spec.unit.h
+    x = (np.arange(N[0]) + 0.5 - N[0] / 2) * h
+    r1 = torch.as_tensor(np.exp(-x * x / 2.0), device="cuda")
+    e_stored = float(torch.einsum("kji,i->kj", out, r1).mul_(r1).sum(dim=1).dot(r1))
+    e_fused = float(pipe.grid_functional([r1] * 3).cpu())
+    assert abs(e_stored - e_fused) <= 1e-12 * abs(e_fused)
+
+
 def test_cfg3_multi_atom_rank_328(L, orc):
     import torch
     rng = np.random.default_rng(20241019)
