@@ -10,7 +10,7 @@
 // times X (K x F):
 //   C[m, f] = sum_i V(i, m) X(i, f)            FP64 DMMA m8n8k4, 128 x 64 CTA tiles, K by 16
 //   part[m_tile, f] = sum_{m in tile} C[m, f] * Y(j,f) * Z(k,f)      fixed-order epilogue
-// then out[f] = scale * sum over m-tiles in ascending order (grid_batch_reduce_kernel), so the
+// then out[f] = scale * sum over m-tiles in a fixed order (grid_batch_reduce_kernel), so the
 // result is bitwise reproducible. Operands stream global -> shared with cp.async (3 stages);
 // the f-tiles of one m-tile are adjacent in the launch order, so V is read from HBM once and
 // re-read from L2. 2 * N1 * N2 * N3 * F FLOP; at cfg4 (256^3, F = 1024) 3.4e10.
@@ -198,14 +198,34 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) grid_batch_kernel(const 
     }
 }
 
-__global__ void grid_batch_reduce_kernel(const double* __restrict__ part, int64_t n_mtiles, int F, double scale,
-                                         int accumulate, double* __restrict__ out) {
-    const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f >= F) return;
-    double s = 0.0;
-    for (int64_t m = 0; m < n_mtiles; ++m) s += part[m * F + f];
-    s = rn_mul(s, scale);
-    out[f] = accumulate ? out[f] + s : s;
+// out[f] = scale * sum over m-tiles, in a fixed order: warp w of the block sums m-tiles
+// w, w + 8, w + 16, ... (four independent chains interleaved by m mod 32; the tail goes to the first), then the
+// block adds the 8 warp sums in ascending w. Lanes take 32 consecutive f, so loads coalesce.
+// The order depends only on n_mtiles, so the result is bitwise reproducible.
+constexpr int kRedWarps = 8;
+__global__ void __launch_bounds__(32 * kRedWarps) grid_batch_reduce_kernel(const double* __restrict__ part,
+                                                                          int64_t n_mtiles, int F, double scale,
+                                                                          int accumulate, double* __restrict__ out) {
+    __shared__ double red[kRedWarps][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int f = blockIdx.x * 32 + lane;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    if (f < F) {
+        int64_t m = w;
+        for (; m + 3 * kRedWarps < n_mtiles; m += 4 * kRedWarps)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) s[c] += part[(m + c * kRedWarps) * F + f];
+        for (; m < n_mtiles; m += kRedWarps) s[0] += part[m * F + f];
+    }
+    red[w][lane] = (s[0] + s[1]) + (s[2] + s[3]);
+    __syncthreads();
+    if (w == 0 && f < F) {
+        double t = red[0][lane];
+#pragma unroll
+        for (int v = 1; v < kRedWarps; ++v) t += red[v][lane];
+        t = rn_mul(t, scale);
+        out[f] = accumulate ? out[f] + t : t;
+    }
 }
 
 }  // namespace
@@ -237,8 +257,8 @@ extern "C" int ls_grid_functional_batch(const double* V_d, int64_t N1, int64_t N
     const dim3 grid(static_cast<unsigned>(ls::ceil_div(F, BN)), static_cast<unsigned>(n_mtiles));
     kern<<<grid, kThreads, smem, s>>>(a);
     LS_LAUNCHED("grid_batch_kernel");
-    grid_batch_reduce_kernel<<<static_cast<unsigned>(ls::ceil_div(F, 128)), 128, 0, s>>>(part, n_mtiles, F, scale,
-                                                                                        accumulate, out_d);
+    grid_batch_reduce_kernel<<<static_cast<unsigned>(ls::ceil_div(F, 32)), 32 * kRedWarps, 0, s>>>(
+        part, n_mtiles, F, scale, accumulate, out_d);
     LS_LAUNCHED("grid_batch_reduce_kernel");
     LS_CUDA(cudaFreeAsync(part, s));
     return LS_OK;
