@@ -393,6 +393,39 @@ def test_grid_functional_batch_random(L, orc, dims, R, F):
     assert np.all(np.abs(chunked - want) <= 1e-13 * mag + 1e-300)
 
 
+@pytest.mark.parametrize("pad_y,pad_z", [(0, 0), (2, 0), (2, 6), (0, 2)])
+def test_grid_functional_batch_strides(pad_y, pad_z):
+    """ls_grid_functional_batch on a padded device grid: one row stride (pad_z = 0) takes the
+    tensor-map feed, whose row stride is then ldy, not N1; padded slabs take the cp.async feed.
+    N1 = 50 is not a multiple of the 16-wide K chunk (the TMA box's tail arrives as zeros)."""
+    import ctypes as C
+    import torch
+    from paper_1405_2270_b200 import _abi
+    rng = np.random.default_rng(11 + pad_y + 10 * pad_z)
+    N1, N2, N3, F = 50, 37, 9, 77
+    V = rng.uniform(-1, 1, (N1, N2, N3))
+    G = [rng.uniform(-1, 1, (d, F)) for d in (N1, N2, N3)]
+    ldy = N1 + pad_y
+    ldz = ldy * N2 + pad_z
+    buf = np.full(N3 * ldz, np.nan)
+    for k in range(N3):
+        for j in range(N2):
+            buf[k * ldz + j * ldy: k * ldz + j * ldy + N1] = V[:, j, k]
+    dev = torch.device("cuda")
+    Vd = torch.as_tensor(buf, device=dev)
+    Gd = [torch.as_tensor(np.asfortranarray(g).T.copy(), device=dev) for g in G]  # column f at f * ld
+    out = torch.zeros(F, dtype=torch.float64, device=dev)
+    lib = _abi.load()
+    p = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.ls_grid_functional_batch(p(Vd), N1, N2, N3, ldy, ldz, p(Gd[0]), N1, p(Gd[1]), N2, p(Gd[2]), N3, F,
+                                        C.c_double(1.0), 0, p(out), s) == 0, lib.ls_last_error()
+    got = out.cpu().numpy()
+    want = np.einsum("ijk,if,jf,kf->f", V, *G)
+    mag = np.einsum("ijk,if,jf,kf->f", np.abs(V), *[np.abs(g) for g in G])
+    assert np.all(np.abs(got - want) <= 1e-13 * mag)
+
+
 def test_cfg4_grid_functional_batch_matches_1d_form(L):
     """cfg4: 1024 separable Gaussian test functions over the whole 256^3 periodic potential,
     full-grid form (expansion + fused GEMM) vs the 1D rank-term form (scalar_product)."""
