@@ -322,9 +322,10 @@ def _ev_ms(fn, reps=3, batch_ms=2.0):
 
 def run_other_configs(L, dev):
     """The other BASELINE configs, measured live on this GPU (device time, inputs in HBM):
-    cfg0 full step; cfg3 (8 atoms, rank 328) assembly and one 8-GPU z-shard of the expansion;
-    cfg4 (periodic n=256, L=256) assembly, 256^3 expansion and the batch of 1024 functionals.
-    cfg2 (2048^3) is the N=8 point of the scaling run; its 1-GPU numbers are in profiles/."""
+    cfg0 full step; cfg2 (2048^3, 64 GiB) full step and energy on one GPU (its 8-way z-sharded
+    form is the N=8 point of the scaling run); cfg3 (8 atoms, rank 328) assembly and one 8-GPU
+    z-shard of the expansion; cfg4 (periodic n=256, L=256) assembly, 256^3 expansion and the
+    batch of 1024 functionals."""
     import torch
     out = {}
     # cfg0
@@ -335,6 +336,37 @@ def run_other_configs(L, dev):
     t = _ev_ms(lambda: pipe.step(grid))
     out["cfg0"] = {"grid": list(pipe.dims), "rank": pipe.Rt, "step_ms": round(t, 4),
                    "gpts": round(float(np.prod(pipe.dims)) / (t * 1e-3) / 1e9, 2)}
+    del grid
+    torch.cuda.empty_cache()
+    # cfg2 on one GPU: the whole 2048^3 grid (64 GiB) resident in HBM -- full step -- and the
+    # energy <V, rho> in its full-grid (fused, V not stored) and 1D rank-term forms
+    spec2 = L.LatticeSpec((32, 32, 32), L.GridSpec(B, n_CELL), [L.Charge((0.0, 0.0, 0.0), 1.0)])
+    rule2 = L.sinc_quadrature(EPS, spec2.unit.h, math.sqrt(3.0) * 32 * B, M_QUAD, C0)
+    pipe2 = L.DevicePipeline(spec2, rule2, mode="erf", device=dev)
+    N2d = pipe2.dims
+    pts2 = float(np.prod(N2d))
+    if torch.cuda.mem_get_info(dev)[0] > 8 * pts2 + (4 << 30):
+        grid = torch.empty(tuple(reversed(N2d)), dtype=torch.float64, device=dev)
+        t2 = _ev_ms(lambda: pipe2.step(grid))
+        del grid
+        torch.cuda.empty_cache()
+        out["cfg2_1gpu"] = {"grid": list(N2d), "rank": pipe2.Rt, "step_ms": round(t2, 3),
+                            "gpts": round(pts2 / (t2 * 1e-3) / 1e9, 1),
+                            "tflops": round(2 * pipe2.Rt * pts2 / (t2 * 1e-3) / 1e12, 2)}
+    else:
+        out["cfg2_1gpu"] = {"skipped": "less than 68 GiB of free HBM"}
+    x2 = [(np.arange(N2d[l]) + 0.5 - N2d[l] / 2.0) * spec2.unit.h for l in range(3)]
+    r2 = [np.exp(-x * x / 2.0) for x in x2]  # as run_energy: rho = exp(-|x|^2/2), box centre
+    rho2 = [torch.as_tensor(r, device=dev) for r in r2]
+    X2 = [torch.as_tensor(r.reshape(-1, 1), device=dev) for r in r2]
+    one_d = lambda: L.DevicePipeline.functional_batch_device([pipe2.factor(l).T for l in range(3)], pipe2.w, X2)  # noqa: E731
+    t_full = _ev_ms(lambda: pipe2.grid_functional(rho2))
+    t_1d = _ev_ms(one_d)
+    e_full = float(pipe2.grid_functional(rho2)[0])
+    e_1d = float(one_d()[0])
+    out["cfg2_1gpu"].update({"energy_full_grid_ms": round(t_full, 3), "energy_1d_ms": round(t_1d, 4),
+                             "energy": e_full, "energy_rel_diff_vs_1d": abs(e_full - e_1d) / abs(e_1d)})
+    del pipe2, rho2, X2
     # calibration of the cfg1 lattice (the reference CLI's dominant cost): GPU-evaluated probes
     spec1 = L.LatticeSpec((16, 16, 16), L.GridSpec(B, n_CELL), [L.Charge((0.0, 0.0, 0.0), 1.0)])
     L.calibrate_for_lattice(spec1, EPS)
@@ -343,7 +375,6 @@ def run_other_configs(L, dev):
     out["calibration_cfg1"] = {"eps": EPS, "M": cal.M, "C0": cal.C0,
                                "ms": round((time.perf_counter() - t0) * 1e3, 3),
                                "note": "calibrate_for_lattice, host-timed; picks the BASELINE M=20"}
-    del grid
     # cfg3: 8 atoms at seeded vertices in [0.1b, 0.9b]^3, Z in 1..8, L = 32
     rng = np.random.default_rng(20241019)
     h = B / n_CELL
