@@ -179,10 +179,11 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     from paper_1405_2270_b200.distributed import ShardedPotential
     L, spec, rule = make_problem(world)
-    dev = torch.device("cuda", local_rank)
+    dev_idx = local_rank % torch.cuda.device_count()  # one GPU per rank; see main() for the plumbing test
+    dev = torch.device("cuda", dev_idx)
     torch.cuda.set_device(dev)
     lib = L.load_library()
-    lib.ls_set_device(local_rank)
+    lib.ls_set_device(dev_idx)
     N1, N2, N3 = spec.target_dims()
     shard = ShardedPotential(spec, rule, mode="erf", device=dev)
     pipe, k0, k1 = shard.pipe, shard.k0, shard.k1
@@ -195,7 +196,7 @@ def run_ours(args, rank, world, local_rank):
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_idx) as clk:
         for _ in range(args.warmup):
             shard.step(out, stream)
         torch.cuda.synchronize()
@@ -611,8 +612,15 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # NCCL, one GPU per rank. LS_BENCH_BACKEND=gloo exists only to exercise the N>1 plumbing
+        # on a single GPU (ranks then share it, so such a run's numbers are not measurements).
+        backend = os.environ.get("LS_BENCH_BACKEND", "nccl")
+        dev_idx = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(dev_idx)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
