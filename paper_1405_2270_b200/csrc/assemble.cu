@@ -4,15 +4,83 @@
 // c = (nu, q) of the per-axis factor is the sum over the L lattice shifts of
 // the windowed master column, added strictly left to right in ascending k
 // (the reference's eight-stream blocks keep that order, lattice.hpp:240-271).
-// One thread per output entry keeps exactly that recurrence, so the result is
-// bit-identical to the reference. Consecutive threads own consecutive i, so
-// every one of the L loads of a warp is a coalesced 256-byte row of the
-// master column; the loads are independent and the adds form one chain.
+// Every output keeps exactly that recurrence in one thread, so the result is
+// bit-identical to the reference; the adds of one output form a dependent
+// chain that cannot be reassociated.
+//
+//  * assemble_box_kernel: box sums, out[o] = sum_k m[s0 + o - k n] with
+//    o = i + j n. Outputs j and j + 1 of the same residue i read the same
+//    master entries one shift apart, so a thread owns eight consecutive j of
+//    one i: eight independent chains fed by a sliding register window, one new
+//    load per shift instead of eight (cfg3: 8 charges x 41 ranks x 2048
+//    outputs x 32 shifts per axis).
+//  * assemble_axis_kernel: periodic sums (out_len = n, one chain per residue,
+//    no reuse): each element is read once, so the loads stream from L2/HBM
+//    with two groups of eight in flight ahead of the adds.
 #include "common.cuh"
 
 namespace {
 
 constexpr int kAsmThreads = 256;
+constexpr int kJ = 8;  // outputs (consecutive j) per thread in the box kernel
+
+// lattice.hpp:98 / :104-106 at k = 0; the window for shift k starts k*n lower.
+__device__ __forceinline__ int64_t window_start(int periodic, int64_t N, int64_t L, int64_t n, int64_t ia) {
+    return periodic ? N + (L / 2) * n - ia : N - ia;
+}
+
+__global__ void assemble_box_kernel(const double* __restrict__ master, int64_t ld_master, int R,
+                                    const int64_t* __restrict__ ia, int64_t n, int64_t L,
+                                    double* __restrict__ out, int64_t ld_out) {
+    pdl_wait();  // the master comes from the preceding generator launch
+    pdl_trigger();
+    const int c = blockIdx.y;  // column nu*R + q
+    const int nu = c / R;
+    const int q = c % R;
+    const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t n_jb = (L + kJ - 1) / kJ;
+    if (x >= n_jb * n) return;
+    const int64_t i = x % n;  // consecutive threads: consecutive i, coalesced loads and stores
+    const int64_t j0 = (x / n) * kJ;
+    // value d (d = j - k) is m[b + d n]; d >= -(L-1) always, d > L-1 only for padded chains
+    const double* col = master + ld_master * q + window_start(0, L * n, L, n, ia[nu]) + i;
+    double win[kJ], acc[kJ], cur[kJ], nxt[kJ];
+    // shift k = 0: the window holds d = j0 .. j0 + 7 (slot d - j0) and starts every chain;
+    // d > L - 1 only in the last block's padded chains (zero, never stored)
+#pragma unroll
+    for (int e = 0; e < kJ; ++e) acc[e] = win[e] = j0 + e <= L - 1 ? __ldg(col + (j0 + e) * n) : 0.0;
+    // shift k brings in d = j0 - k (always <= L - 1) into slot (-k) mod 8; chain jj reads slot
+    // (jj - k) mod 8. pk points at the entry of shift k0; loads past the last shift are
+    // redirected to pk (a valid address) and never used.
+    const double* pk = col + (j0 - 1) * n;
+#pragma unroll
+    for (int s = 0; s < kJ; ++s) cur[s] = __ldg(1 + s < L ? pk - s * n : pk);
+    int64_t k0 = 1;  // k0 = 1 mod 8, so every slot index is static
+    for (; k0 + kJ <= L; k0 += kJ, pk -= kJ * n) {
+#pragma unroll
+        for (int s = 0; s < kJ; ++s) nxt[s] = __ldg(k0 + kJ + s < L ? pk - (kJ + s) * n : pk);
+#pragma unroll
+        for (int s = 0; s < kJ; ++s) {
+            win[(kJ - 1 - s) & (kJ - 1)] = cur[s];
+#pragma unroll
+            for (int jj = 0; jj < kJ; ++jj) acc[jj] = rn_add(acc[jj], win[(jj - 1 - s) & (kJ - 1)]);
+        }
+#pragma unroll
+        for (int s = 0; s < kJ; ++s) cur[s] = nxt[s];
+    }
+#pragma unroll
+    for (int s = 0; s < kJ; ++s) {  // the last, partial block of shifts
+        if (k0 + s < L) {
+            win[(kJ - 1 - s) & (kJ - 1)] = cur[s];
+#pragma unroll
+            for (int jj = 0; jj < kJ; ++jj) acc[jj] = rn_add(acc[jj], win[(jj - 1 - s) & (kJ - 1)]);
+        }
+    }
+    double* o = out + ld_out * c + i + j0 * n;
+#pragma unroll
+    for (int jj = 0; jj < kJ; ++jj)
+        if (j0 + jj < L) o[jj * n] = acc[jj];
+}
 
 __global__ void assemble_axis_kernel(const double* __restrict__ master, int64_t ld_master, int R,
                                      const int64_t* __restrict__ ia, int64_t n, int64_t L,
@@ -23,22 +91,27 @@ __global__ void assemble_axis_kernel(const double* __restrict__ master, int64_t 
     const int c = blockIdx.y;  // column nu*R + q
     const int nu = c / R;
     const int q = c % R;
-    const int64_t N = L * n;
-    // lattice.hpp:98 / :104-106 at k = 0; the window for shift k starts k*n lower.
-    const int64_t s0 = periodic ? N + (L / 2) * n - ia[nu] : N - ia[nu];
-    const double* base = master + ld_master * q + s0;
+    const double* base = master + ld_master * q + window_start(periodic, L * n, L, n, ia[nu]);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < out_len;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double* p = base + i;
         double acc = p[0];
         int64_t k = 1;
-        // Loads are hoisted in groups of 8; the adds stay in ascending-k order.
+        // Two groups of 8 loads in flight ahead of the adds, which stay in ascending-k order.
+        double cur[8], nxt[8];
+        if (k + 8 <= L) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) cur[u] = __ldg(p - (k + u) * n);
+        }
         for (; k + 8 <= L; k += 8) {
-            double v[8];
+            if (k + 16 <= L) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __ldg(p - (k + u) * n);
+                for (int u = 0; u < 8; ++u) nxt[u] = __ldg(p - (k + 8 + u) * n);
+            }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc = rn_add(acc, v[u]);
+            for (int u = 0; u < 8; ++u) acc = rn_add(acc, cur[u]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
         }
         for (; k < L; ++k) acc = rn_add(acc, __ldg(p - k * n));
         out[i + ld_out * c] = acc;
@@ -57,10 +130,20 @@ extern "C" int ls_assemble_axis(const double* master_d, int64_t ld_master, int R
         return ls::fail(LS_EVALIDATION, "assemble_axis: leading dimension too small");
     const int64_t cols = (int64_t)M0 * R;
     if (cols > 65535) return ls::fail(LS_EGUARD, "assemble_axis: more than 65535 columns");
-    const int64_t blocks = std::min<int64_t>(ls::ceil_div(out_len, kAsmThreads), 2048);
-    LS_CUDA(ls::launch_pdl(assemble_axis_kernel, dim3((unsigned)blocks, (unsigned)cols), dim3(kAsmThreads), 0,
-                           ls::as_stream(stream), master_d, ld_master, R, ia_d, n, L, periodic, out_len, out_d,
-                           ld_out));
+    const cudaStream_t s = ls::as_stream(stream);
+    if (!periodic && L > 1) {
+        const int64_t threads = ls::ceil_div(L, kJ) * n;
+        const int64_t blocks = ls::ceil_div(threads, kAsmThreads);
+        if (blocks > 0x7fffffff) return ls::fail(LS_EGUARD, "assemble_axis: too many output blocks");
+        LS_CUDA(ls::launch_pdl(assemble_box_kernel, dim3((unsigned)blocks, (unsigned)cols), dim3(kAsmThreads), 0, s,
+                               master_d, ld_master, R, ia_d, n, L, out_d, ld_out));
+        LS_LAUNCHED("assemble_box_kernel");
+        return LS_OK;
+    }
+    // periodic: 64-thread blocks spread the few, long chains (n per column) over the SMs
+    const int64_t blocks = std::min<int64_t>(ls::ceil_div(out_len, 64), 4096);
+    LS_CUDA(ls::launch_pdl(assemble_axis_kernel, dim3((unsigned)blocks, (unsigned)cols), dim3(64), 0, s, master_d,
+                           ld_master, R, ia_d, n, L, periodic, out_len, out_d, ld_out));
     LS_LAUNCHED("assemble_axis_kernel");
     return LS_OK;
 }

@@ -3,15 +3,22 @@
 // Reference: build_newton_master (newton.hpp:57-75) fills column q of each
 // axis factor with gaussian_sample_vector(len, h, tau_q) (midpoint samples,
 // newton.hpp:43-52), and the BASELINE generator uses the erf-difference cell
-// integrals of gaussian_moment_vector (newton.hpp:21-37). Here every (q, i)
-// entry is one thread; the erf mode evaluates each cell vertex once in shared
+// integrals of gaussian_moment_vector (newton.hpp:21-37). Here every (q, i, len-1-i)
+// mirrored pair of entries is one thread; the erf mode evaluates each cell vertex once in shared
 // memory and differences neighbours, which is bit-identical to evaluating
-// erf(t*x_{i+1}) and erf(t*x_i) separately as the reference does.
+// erf(t*x_{i+1}) and erf(t*x_i) separately as the reference does, and only the
+// lower half of each (exactly even) column is evaluated.
 #include "common.cuh"
 
 namespace {
 
 constexpr int kGenThreads = 256;
+
+// Both generators produce exactly even columns: cell len-1-i mirrors cell i, bit for bit, in
+// the reference as here (test_newton.cpp:71-77, :93). The midpoint of cell len-1-i is the exact
+// negation of cell i's ((i + 0.5 - len/2) is exact), and erf is odd, so the vertex erf values
+// mirror with a sign flip and (-a) - (-b) rounds exactly like b - a. Each thread therefore
+// evaluates one cell of the lower half and writes it and its mirror: half the exp/erf calls.
 
 // newton.hpp:46-50 with GridSpec::midpoint (grid.hpp:32-34):
 //   x = t * ((i + 0.5 - len/2) * h);  out = exp(-x*x)
@@ -21,38 +28,44 @@ __global__ void gen_midpoint_kernel(const double* __restrict__ tau, int64_t len,
     const int q = blockIdx.y;
     const double t = tau[q];
     const double half_len = static_cast<double>(len) / 2.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+    double* col = out + ld * q;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len / 2;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double mid = rn_mul(rn_sub(rn_add(static_cast<double>(i), 0.5), half_len), h);
         const double x = rn_mul(t, mid);
-        out[i + ld * q] = exp(-rn_mul(x, x));
+        const double v = exp(-rn_mul(x, x));
+        col[i] = v;
+        col[len - 1 - i] = v;
     }
 }
 
 // newton.hpp:28-36: t == 0 -> h; else sqrt(pi)/(2t) * (erf(t*v(i+1)) - erf(t*v(i))),
-// v(i) = (i - len/2) * h. Block b covers cells [i0, i0 + blockDim) and the
-// blockDim + 1 vertices bounding them.
+// v(i) = (i - len/2) * h. Block b covers the lower-half cells [i0, i0 + blockDim) and the
+// blockDim + 1 vertices bounding them; cell len-1-i gets the same value (see above).
 __global__ void gen_erf_kernel(const double* __restrict__ tau, int64_t len, double h,
                                double* __restrict__ out, int64_t ld) {
     pdl_trigger();
     __shared__ double ev[kGenThreads + 1];
     const int q = blockIdx.y;
     const double t = tau[q];
+    const int64_t half = len / 2;
     const int64_t i0 = blockIdx.x * (int64_t)kGenThreads;
     const int64_t i = i0 + threadIdx.x;
+    double* col = out + ld * q;
     if (t == 0.0) {
-        if (i < len) out[i + ld * q] = h;
+        if (i < half) col[i] = col[len - 1 - i] = h;
         return;
     }
-    const int64_t half = len / 2;
     for (int v = threadIdx.x; v <= kGenThreads; v += kGenThreads) {
         const int64_t vi = i0 + v;
-        if (vi <= len) ev[v] = erf(rn_mul(t, rn_mul(static_cast<double>(vi - half), h)));
+        if (vi <= half) ev[v] = erf(rn_mul(t, rn_mul(static_cast<double>(vi - half), h)));
     }
     __syncthreads();
-    if (i < len) {
+    if (i < half) {
         const double scale = sqrt(CUDART_PI) / rn_mul(2.0, t);
-        out[i + ld * q] = rn_mul(scale, rn_sub(ev[threadIdx.x + 1], ev[threadIdx.x]));
+        const double v = rn_mul(scale, rn_sub(ev[threadIdx.x + 1], ev[threadIdx.x]));
+        col[i] = v;
+        col[len - 1 - i] = v;
     }
 }
 
@@ -68,11 +81,11 @@ extern "C" int ls_gen_master(int mode, const double* tau_d, int R, int64_t len, 
     if (R > 65535) return ls::fail(LS_EGUARD, "gen_master: rank above 65535");
     const cudaStream_t s = ls::as_stream(stream);
     if (mode == LS_GEN_MIDPOINT) {
-        const int64_t blocks = std::min<int64_t>(ls::ceil_div(len, kGenThreads), 4096);
+        const int64_t blocks = std::min<int64_t>(ls::ceil_div(len / 2, kGenThreads), 4096);
         gen_midpoint_kernel<<<dim3((unsigned)blocks, R), kGenThreads, 0, s>>>(tau_d, len, h, out_d, ld);
         LS_LAUNCHED("gen_midpoint_kernel");
     } else if (mode == LS_GEN_ERF) {
-        const int64_t blocks = ls::ceil_div(len, kGenThreads);
+        const int64_t blocks = ls::ceil_div(len / 2, kGenThreads);
         if (blocks > 0x7fffffff) return ls::fail(LS_EGUARD, "gen_master: length too large");
         gen_erf_kernel<<<dim3((unsigned)blocks, R), kGenThreads, 0, s>>>(tau_d, len, h, out_d, ld);
         LS_LAUNCHED("gen_erf_kernel");
