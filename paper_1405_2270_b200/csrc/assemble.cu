@@ -16,13 +16,14 @@
 //    outputs x 32 shifts per axis).
 //  * assemble_axis_kernel: periodic sums (out_len = n, one chain per residue,
 //    no reuse): each element is read once, so the loads stream from L2/HBM
-//    with two groups of eight in flight ahead of the adds.
+//    with three groups of eight in flight ahead of the adds.
 #include "common.cuh"
 
 namespace {
 
 constexpr int kAsmThreads = 256;
 constexpr int kJ = 8;  // outputs (consecutive j) per thread in the box kernel
+constexpr int kPGroups = 4;  // groups of 8 loads per chain in the periodic kernel's register ring
 
 // lattice.hpp:98 / :104-106 at k = 0; the window for shift k starts k*n lower.
 __device__ __forceinline__ int64_t window_start(int periodic, int64_t N, int64_t L, int64_t n, int64_t ia) {
@@ -96,24 +97,38 @@ __global__ void assemble_axis_kernel(const double* __restrict__ master, int64_t 
          i += (int64_t)gridDim.x * blockDim.x) {
         const double* p = base + i;
         double acc = p[0];
-        int64_t k = 1;
-        // Two groups of 8 loads in flight ahead of the adds, which stay in ascending-k order.
-        double cur[8], nxt[8];
-        if (k + 8 <= L) {
+        // Groups of 8 shifts; kPGroups - 1 groups of loads stay in flight ahead of the adds,
+        // which keep ascending-k order. Loads past the last shift are redirected to p.
+        double buf[kPGroups][8];
+        const int64_t n_full = (L - 1) / 8;  // full groups of shifts 1 + 8g .. 8 + 8g
 #pragma unroll
-            for (int u = 0; u < 8; ++u) cur[u] = __ldg(p - (k + u) * n);
-        }
-        for (; k + 8 <= L; k += 8) {
-            if (k + 16 <= L) {
+        for (int g = 0; g < kPGroups - 1; ++g)
 #pragma unroll
-                for (int u = 0; u < 8; ++u) nxt[u] = __ldg(p - (k + 8 + u) * n);
+            for (int u = 0; u < 8; ++u) buf[g][u] = __ldg(g < n_full ? p - (1 + 8 * g + u) * n : p);
+        int64_t g0 = 0;
+        for (; g0 + kPGroups <= n_full; g0 += kPGroups) {
+#pragma unroll
+            for (int gg = 0; gg < kPGroups; ++gg) {
+                const int64_t gl = g0 + gg + kPGroups - 1;  // group to load into the slot freed last
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    buf[(gg + kPGroups - 1) % kPGroups][u] = __ldg(gl < n_full ? p - (1 + 8 * gl + u) * n : p);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = rn_add(acc, buf[gg][u]);
             }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = rn_add(acc, cur[u]);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
         }
-        for (; k < L; ++k) acc = rn_add(acc, __ldg(p - k * n));
+#pragma unroll
+        for (int gg = 0; gg < kPGroups; ++gg) {  // the remaining (< kPGroups) full groups
+            if (g0 + gg < n_full) {
+                const int64_t gl = g0 + gg + kPGroups - 1;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    buf[(gg + kPGroups - 1) % kPGroups][u] = __ldg(gl < n_full ? p - (1 + 8 * gl + u) * n : p);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = rn_add(acc, buf[gg][u]);
+            }
+        }
+        for (int64_t k = 1 + 8 * n_full; k < L; ++k) acc = rn_add(acc, __ldg(p - k * n));
         out[i + ld_out * c] = acc;
     }
 }
