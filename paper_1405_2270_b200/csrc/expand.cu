@@ -544,7 +544,7 @@ bool plan_for(int KD, int n_tail, Plan& out) {
             // Beyond the double-buffered TMEM plans. At ranks 122-164 the smem plan 9 measured
             // 2-4% faster on 1024^2 slabs (the split-K unit's exposed A1k fill weighs more there);
             // from rank ~180 on split-K wins: rank 246 29.2 vs 28.9 TF/s, cfg3's 328 32.0 vs 30.8.
-            case kPlanSplitK: ok = (force == kPlanSplitK || KD >= 44) && fits_splitk(KD, tmem_tail(n_tail)); ic = 64; break;
+            case kPlanSplitK: ok = (force == kPlanSplitK || KD >= 44) && fits_splitk(KD, n_tail); ic = 64; break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
         }
         if (ok) {
@@ -691,7 +691,8 @@ int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
         case kPlanTmem: return launch<TileWide, STORE, FUNC, true>(a, s);
         case kPlanTmem16: return launch<TileTmem16, STORE, FUNC, true>(a, s);
         case kPlanSplitK:
-            a.n_tail = tmem_tail(a.n_tail);
+            // No zero DFMA rank when R mod 4 == 0 (unlike the TMEM plans): the pair's halves then
+            // carry equal work, 0.8% at cfg3 and 1.6-2.4% at ranks 176-240.
             return launch_splitk(a, STORE, FUNC, s, ls::sm_count(), kernel_setup);
         case 0: return launch<TileWide, STORE, FUNC>(a, s);
         case 1: return launch<TileWide3, STORE, FUNC>(a, s);
@@ -726,7 +727,7 @@ extern "C" int ls_expand_plan_name(int R, char* out, int len) {
     const bool whole = plan_for(KD, n_tail, pl);
     if (!whole && !chunk_plan(pl)) return ls::fail(LS_EGUARD, "expand_plan_name: no tile plan");
     const int kd = pl.pad && n_tail == 2 ? KD + 1 : KD;
-    const int nt = pl.id == kPlanTmem || pl.id == kPlanTmem16 || pl.id == kPlanSplitK ? (pl.pad ? 1 : tmem_tail(n_tail)) : n_tail;
+    const int nt = pl.id == kPlanTmem || pl.id == kPlanTmem16 ? (pl.pad ? 1 : tmem_tail(n_tail)) : n_tail;
     const char* shape = pl.id == kPlanTmem     ? "expand_tmem_kernel, 8 warps x 2 CTAs/SM, A1k in TMEM"
                         : pl.id == kPlanTmem16 ? "expand_tmem_kernel, 16 warps x 1 CTA/SM, A1k in TMEM"
                         : pl.id == kPlanSplitK ? "expand_splitk_kernel, 16 warps x 1 CTA/SM, A1k halves in TMEM lane quarters"

@@ -407,7 +407,7 @@ int splitk_smem_bytes(int KD, int n_tail) {
 
 bool fits_splitk(int KD, int n_tail) {
     const int KH = (KD + 1) / 2;
-    return n_tail >= 1 && n_tail <= 2 && KD >= 2 && 8 * KH + 16 * n_tail <= 512 &&
+    return n_tail >= 0 && n_tail <= 2 && KD >= 2 && 8 * KH + 16 * n_tail <= 512 &&
            splitk_smem_bytes(KD, n_tail) + 1024 <= 227 * 1024;
 }
 
