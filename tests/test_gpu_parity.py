@@ -145,6 +145,26 @@ def test_assembly_bitwise_on_oracle_master(L, orc, periodic):
         assert got.rank == spec.charge_count() * rule.node_count()
 
 
+@pytest.mark.parametrize("Lc,n,M0,periodic", [(32, 64, 8, False), (32, 64, 8, True), (13, 64, 8, False),
+                                              (21, 16, 3, False), (256, 256, 1, True), (9, 8, 8, False)])
+def test_assembly_bitwise_at_config_scale(L, orc, Lc, n, M0, periodic):
+    """K2 at the BASELINE scales (cfg3: L = 32 with 8 charges; cfg4: periodic L = 256, n = 256)
+    and at L not a multiple of the box kernel's 8-shift blocks: bit-identical to the oracle's
+    ascending-k adds on the same master."""
+    rng = np.random.default_rng(100 + Lc + M0)
+    b = 10.0
+    h = b / n
+    ia = rng.integers(0, n + 1, size=(M0, 3))
+    charges = [(*(ia[c] * h - b / 2), float(c + 1)) for c in range(M0)]
+    spec, rule = cfg(L, Lc, n=n, b=b, charges=charges, M=20)
+    m, want, w = oracle_assembled(orc, spec, rule, "midpoint", periodic)
+    master = L.CanonicalTensor3(m, rule.weights, trusted=True)
+    got = (L.assembled_periodic_sum if periodic else L.assembled_box_sum)(spec, master)
+    for l in range(3):
+        assert np.array_equal(got.tensor.factor(l), want[l]), l
+    assert np.array_equal(got.tensor.weights(), w)
+
+
 def test_assembly_matches_golden_bitwise(L, golden):
     g = golden
     ch = g["mc_charges"]
