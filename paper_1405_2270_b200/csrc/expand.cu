@@ -35,7 +35,7 @@
 // persistent grid (CTAs per SM x SM count). Plans by rank (plan_for):
 //   * ranks <= 121: expand_tmem.cuh, A1k double-buffered in tensor memory (8 warps x 2 CTAs
 //     or 16 warps x 1 CTA per SM; instantiated in expand_tmem8.cu / expand_tmem16.cu);
-//   * ranks >= 176 (KD <= 120): expand_splitk.cu, A1k k-halves in different TMEM lane
+//   * ranks >= 164 (KD <= 120): expand_splitk.cu, A1k k-halves in different TMEM lane
 //     quarters with a pair reduction;
 //   * otherwise this file's expand_dmma_kernel with A1k in shared memory;
 // k3.cuh holds the definitions they share.
@@ -541,10 +541,11 @@ bool plan_for(int KD, int n_tail, Plan& out) {
                      fits_tmem16(KD + (n_tail == 2), n_tail == 2 ? 0 : n_tail);
                 ic = TileTmem16::IC;
                 break;
-            // Beyond the double-buffered TMEM plans. At ranks 122-164 the smem plan 9 measured
-            // 2-4% faster on 1024^2 slabs (the split-K unit's exposed A1k fill weighs more there);
-            // from rank ~180 on split-K wins: rank 246 29.2 vs 28.9 TF/s, cfg3's 328 32.0 vs 30.8.
-            case kPlanSplitK: ok = (force == kPlanSplitK || KD >= 44) && fits_splitk(KD, n_tail); ic = 64; break;
+            // Beyond the double-buffered TMEM plans. At ranks 122-160 the smem plan 9 and split-K
+            // trade places within 2% on 1024^2 x 256 slabs (the split-K unit's exposed A1k fill
+            // weighs more there); from rank 164 (KD 41) on split-K wins: 164-172 by 1-3%, rank 246
+            // 29.7 vs 28.9 TF/s, cfg3's 328 32.9 vs 30.8.
+            case kPlanSplitK: ok = (force == kPlanSplitK || KD >= 41) && fits_splitk(KD, n_tail); ic = 64; break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
         }
         if (ok) {
