@@ -317,14 +317,16 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         // j-chunk range of this unit (partial only for the first and last unit of a split tail)
         const int jc_lo = (kSplitTail && n == n_full) ? t0 % per_unit : 0;
         const int jc_hi = (kSplitTail && n >= n_full && n == my_units - 1) ? (t1 - 1) % per_unit + 1 : per_unit;
-        // Fill schedule for the next unit: tasks spread evenly over all of this unit's stages,
-        // offset by warp so the warps of an SM sub-partition do not fill in the same stage.
-        // Starting from the first stage rather than the third measured 1.7% faster at 256^3 (4
-        // stages per unit: fewer fill tasks share a stage) and 0.3% at cfg1; ending the fill a
-        // stage or two before the unit's last stage changed nothing.
+        // Fill schedule for the next unit: tasks spread evenly over this unit's stages, offset by
+        // warp so the warps of an SM sub-partition do not fill in the same stage. The 8-warp
+        // shape starts at the first stage: 1.7% faster at 256^3 (4 stages per unit, so fewer
+        // fill tasks share a stage) and 0.3% at cfg1. The 16-warp shape starts at the third
+        // (starting at the first measured -0.5 to -1.5% at ranks 73-113, +1.8% at 121). Ending
+        // the fill a stage or two before the unit's last stage changed nothing.
         const int n_here = jc_hi - jc_lo;
+        const int first_fill = (WARPS == 16 && n_here > 2) ? 2 : 0;
         auto fill_stage = [&](int task) {
-            return jc_lo + ((task * WARPS + warp) * n_here) / (WARPS * n_tasks);
+            return jc_lo + first_fill + ((task * WARPS + warp) * (n_here - first_fill)) / (WARPS * n_tasks);
         };
         const int buf = n & 1;
         const bool has_next = n + 1 < my_units;
