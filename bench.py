@@ -321,6 +321,26 @@ def _ev_ms(fn, reps=3, batch_ms=2.0):
     return best
 
 
+def _graph_ms(fn, reps=3, batch_ms=2.0):
+    """Device ms per call from back-to-back replays of a CUDA graph of `fn` (the host launch cost
+    of a short call is then outside the measurement); falls back to _ev_ms when the call cannot
+    be captured. Returns (ms, how)."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    try:
+        with torch.cuda.graph(g, stream=side, capture_error_mode="relaxed"):
+            fn()
+        torch.cuda.synchronize()
+    except Exception:  # noqa: BLE001 -- not capturable: eager timing
+        torch.cuda.synchronize()
+        return _ev_ms(fn, reps, batch_ms), "eager"
+    return _ev_ms(g.replay, reps, batch_ms), "graph"
+
+
 def run_other_configs(L, dev):
     """The other BASELINE configs, measured live on this GPU (device time, inputs in HBM):
     cfg0 full step; cfg2 (2048^3, 64 GiB) full step and energy on one GPU (its 8-way z-sharded

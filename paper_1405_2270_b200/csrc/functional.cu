@@ -67,37 +67,56 @@ __global__ void gram_reduce_kernel(const double* __restrict__ G0, const double* 
     out[0] = sum;
 }
 
-// One block per density f: 3R Gram entries <P_l[:,q], rho_l[:,f]> by warps into
-// shared memory, then thread 0 forms scale * sum_q ((w_q * 1) * G0) * G1 * G2.
+// One block per kFBatch densities f: the 3R Gram entries <P_l[:,q], rho_l[:,f]> of each f, by
+// warps into shared memory, then one thread per f forms scale * sum_q ((w_q * 1) * G0) * G1 * G2.
+// A warp computes an entry for the block's densities together, so each factor column is read
+// from L2 once per kFBatch densities (cfg4: 252 -> 63 MB of L2 reads; the density columns stay
+// in L1 across the R entries of an axis). Kernel 33.5 -> 29.0 us at cfg4 (F = 1024, ncu warm);
+// 2 densities per block measured the same, 8 and 16 slower (57.6 / 75.8 us: fewer blocks, the
+// per-warp entry loop is latency-bound). LS_FBATCH is a build-time lab knob.
+#ifndef LS_FBATCH
+#define LS_FBATCH 4
+#endif
+constexpr int kFBatch = LS_FBATCH;
 __global__ void functional_batch_kernel(const double* __restrict__ A, int64_t lda,
                                         const double* __restrict__ B, int64_t ldb,
                                         const double* __restrict__ C, int64_t ldc,
                                         const double* __restrict__ w, int R, int64_t n1,
                                         int64_t n2, int64_t n3, const double* __restrict__ X,
                                         int64_t ldx, const double* __restrict__ Y, int64_t ldy,
-                                        const double* __restrict__ Z, int64_t ldz, double scale,
+                                        const double* __restrict__ Z, int64_t ldz, int F, double scale,
                                         double* __restrict__ out) {
-    extern __shared__ double gsh[];  // [3][R]
-    const int f = blockIdx.x;
+    extern __shared__ double gsh[];  // [kFBatch][3][R]
+    const int f0 = blockIdx.x * kFBatch;
+    const int nf = F - f0 < kFBatch ? F - f0 : kFBatch;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     for (int e = warp; e < 3 * R; e += nwarps) {
         const int l = e / R, q = e % R;
-        double s;
-        if (l == 0)
-            s = warp_dot(A + lda * q, X + ldx * f, n1, lane);
-        else if (l == 1)
-            s = warp_dot(B + ldb * q, Y + ldy * f, n2, lane);
-        else
-            s = warp_dot(C + ldc * q, Z + ldz * f, n3, lane);
-        if (lane == 0) gsh[e] = s;
+        const double* x = l == 0 ? A + lda * q : l == 1 ? B + ldb * q : C + ldc * q;
+        const double* y = l == 0 ? X : l == 1 ? Y : Z;
+        const int64_t ld = l == 0 ? ldx : l == 1 ? ldy : ldz;
+        const int64_t n = l == 0 ? n1 : l == 1 ? n2 : n3;
+        double s[kFBatch] = {};
+        for (int64_t i = lane; i < n; i += 32) {
+            const double xv = x[i];
+#pragma unroll
+            for (int u = 0; u < kFBatch; ++u)
+                if (u < nf) s[u] = fma(xv, y[ld * (f0 + u) + i], s[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kFBatch; ++u) {
+            const double t = warp_sum(s[u]);
+            if (lane == 0) gsh[u * 3 * R + e] = t;
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < nf) {
+        const double* g = gsh + threadIdx.x * 3 * R;
         double sum = 0.0;
         for (int q = 0; q < R; ++q)
-            sum = rn_add(sum, rn_mul(rn_mul(rn_mul(rn_mul(w[q], 1.0), gsh[q]), gsh[R + q]), gsh[2 * R + q]));
-        out[f] = rn_mul(scale, sum);
+            sum = rn_add(sum, rn_mul(rn_mul(rn_mul(rn_mul(w[q], 1.0), g[q]), g[R + q]), g[2 * R + q]));
+        out[f0 + threadIdx.x] = rn_mul(scale, sum);
     }
 }
 
@@ -222,13 +241,13 @@ extern "C" int ls_functional_batch(const double* A_d, int64_t lda, const double*
         ldx < n1 || ldy < n2 || ldz < n3)
         return ls::fail(LS_EVALIDATION, "functional_batch: bad shape");
     if (F == 0) return LS_OK;
-    const size_t smem = sizeof(double) * 3 * static_cast<size_t>(R);
+    const size_t smem = sizeof(double) * 3 * static_cast<size_t>(R) * kFBatch;
     if (smem > 200 * 1024) return ls::fail(LS_EGUARD, "functional_batch: rank too large");
     auto kern = functional_batch_kernel;
     if (smem > 48 * 1024)
         LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<F, 256, smem, ls::as_stream(stream)>>>(A_d, lda, B_d, ldb, C_d, ldc, w_d, R, n1, n2, n3, X_d,
-                                                   ldx, Y_d, ldy, Z_d, ldz, scale, out_d);
+    kern<<<(F + kFBatch - 1) / kFBatch, 256, smem, ls::as_stream(stream)>>>(
+        A_d, lda, B_d, ldb, C_d, ldc, w_d, R, n1, n2, n3, X_d, ldx, Y_d, ldy, Z_d, ldz, F, scale, out_d);
     LS_LAUNCHED("functional_batch_kernel");
     return LS_OK;
 }
