@@ -407,7 +407,7 @@ def run_other_configs(L, dev):
     N = pipe.dims
     k1 = N[2] // 8
     shard = torch.empty((k1, N[1], N[0]), dtype=torch.float64, device=dev)
-    t_asm = _ev_ms(lambda: (pipe.generate(), pipe.assemble()))
+    t_asm, how_asm = _graph_ms(lambda: (pipe.generate(), pipe.assemble()))
     t_exp = _ev_ms(lambda: pipe.expand(shard, 0, k1))
     out["cfg3"] = {"grid": list(N), "rank": pipe.Rt, "generator_plus_assembly_ms": round(t_asm, 4),
                    "shard8_expand_ms": round(t_exp, 3),
@@ -420,7 +420,7 @@ def run_other_configs(L, dev):
     rule = L.sinc_quadrature(EPS, spec.unit.h, math.sqrt(3.0) * 256 * B, M_QUAD, C0)
     pipe = L.DevicePipeline(spec, rule, mode="erf", periodic=True, device=dev)
     grid = torch.empty(tuple(reversed(pipe.dims)), dtype=torch.float64, device=dev)
-    t_asm = _ev_ms(lambda: (pipe.generate(), pipe.assemble()))
+    t_asm, how_asm = _graph_ms(lambda: (pipe.generate(), pipe.assemble()))
     t_exp = _ev_ms(lambda: pipe.expand(grid))
     rng = np.random.default_rng(4)
     F = 1024
@@ -430,7 +430,7 @@ def run_other_configs(L, dev):
     mids = (np.arange(256) + 0.5 - 128) * spec.unit.h
     G = [torch.as_tensor(np.exp(-(mids[:, None] - centres[None, :, l]) ** 2 / (2 * sigma ** 2)), device=dev)
          for l in range(3)]
-    t_f = _ev_ms(lambda: L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w, G))
+    t_f, how_f = _graph_ms(lambda: L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w, G))
     # full-grid form: expansion + fused DMMA GEMM (2 * 256^3 * 1024 FLOP) + fixed-order reduction
     t_fg = _ev_ms(lambda: pipe.grid_functional_batch(G))
     fg_flop = 2.0 * float(np.prod(pipe.dims)) * F
@@ -442,7 +442,10 @@ def run_other_configs(L, dev):
                         "functionals_1024_full_grid_tflops": round(fg_flop / (t_fg * 1e-3) / 1e12, 2)}
     del grid
     torch.cuda.empty_cache()
-    out["timing"] = "CUDA events around back-to-back calls (batches >= 2 ms, best of 3); inputs in HBM"
+    out["timing"] = ("CUDA events around back-to-back calls (batches >= 2 ms, best of 3); inputs in HBM. "
+                     f"cfg3/cfg4 generator_plus_assembly and cfg4 functionals_1024 (short calls whose host "
+                     f"launch cost would dominate) time back-to-back replays of a CUDA graph of the call: "
+                     f"{how_asm}/{how_f}")
     return out
 
 

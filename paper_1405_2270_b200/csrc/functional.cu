@@ -67,6 +67,40 @@ __global__ void gram_reduce_kernel(const double* __restrict__ G0, const double* 
     out[0] = sum;
 }
 
+// Small batches (F below a few per SM): one block per density f: 3R Gram entries <P_l[:,q], rho_l[:,f]> by warps into
+// shared memory, then thread 0 forms scale * sum_q ((w_q * 1) * G0) * G1 * G2.
+__global__ void functional_batch_single_kernel(const double* __restrict__ A, int64_t lda,
+                                        const double* __restrict__ B, int64_t ldb,
+                                        const double* __restrict__ C, int64_t ldc,
+                                        const double* __restrict__ w, int R, int64_t n1,
+                                        int64_t n2, int64_t n3, const double* __restrict__ X,
+                                        int64_t ldx, const double* __restrict__ Y, int64_t ldy,
+                                        const double* __restrict__ Z, int64_t ldz, double scale,
+                                        double* __restrict__ out) {
+    extern __shared__ double gsh[];  // [3][R]
+    const int f = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    for (int e = warp; e < 3 * R; e += nwarps) {
+        const int l = e / R, q = e % R;
+        double s;
+        if (l == 0)
+            s = warp_dot(A + lda * q, X + ldx * f, n1, lane);
+        else if (l == 1)
+            s = warp_dot(B + ldb * q, Y + ldy * f, n2, lane);
+        else
+            s = warp_dot(C + ldc * q, Z + ldz * f, n3, lane);
+        if (lane == 0) gsh[e] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int q = 0; q < R; ++q)
+            sum = rn_add(sum, rn_mul(rn_mul(rn_mul(rn_mul(w[q], 1.0), gsh[q]), gsh[R + q]), gsh[2 * R + q]));
+        out[f] = rn_mul(scale, sum);
+    }
+}
+
 // One block per kFBatch densities f: the 3R Gram entries <P_l[:,q], rho_l[:,f]> of each f, by
 // warps into shared memory, then one thread per f forms scale * sum_q ((w_q * 1) * G0) * G1 * G2.
 // A warp computes an entry for the block's densities together, so each factor column is read
@@ -241,13 +275,26 @@ extern "C" int ls_functional_batch(const double* A_d, int64_t lda, const double*
         ldx < n1 || ldy < n2 || ldz < n3)
         return ls::fail(LS_EVALIDATION, "functional_batch: bad shape");
     if (F == 0) return LS_OK;
-    const size_t smem = sizeof(double) * 3 * static_cast<size_t>(R) * kFBatch;
+    // Batches too small to fill the GPU with kFBatch densities per block take one per block
+    // with the single-density kernel (cfg2's one energy density).
+    const int fb = F >= kFBatch * ls::sm_count() ? kFBatch : 1;
+    const size_t smem = sizeof(double) * 3 * static_cast<size_t>(R) * fb;
     if (smem > 200 * 1024) return ls::fail(LS_EGUARD, "functional_batch: rank too large");
+    const cudaStream_t s = ls::as_stream(stream);
+    if (fb == 1) {
+        auto kern = functional_batch_single_kernel;
+        if (smem > 48 * 1024)
+            LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<F, 256, smem, s>>>(A_d, lda, B_d, ldb, C_d, ldc, w_d, R, n1, n2, n3, X_d, ldx, Y_d, ldy, Z_d, ldz,
+                                  scale, out_d);
+        LS_LAUNCHED("functional_batch_single_kernel");
+        return LS_OK;
+    }
     auto kern = functional_batch_kernel;
     if (smem > 48 * 1024)
         LS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(F + kFBatch - 1) / kFBatch, 256, smem, ls::as_stream(stream)>>>(
-        A_d, lda, B_d, ldb, C_d, ldc, w_d, R, n1, n2, n3, X_d, ldx, Y_d, ldy, Z_d, ldz, F, scale, out_d);
+    kern<<<(F + fb - 1) / fb, 256, smem, s>>>(A_d, lda, B_d, ldb, C_d, ldc, w_d, R, n1, n2, n3, X_d, ldx, Y_d, ldy,
+                                              Z_d, ldz, F, scale, out_d);
     LS_LAUNCHED("functional_batch_kernel");
     return LS_OK;
 }
