@@ -66,6 +66,14 @@ int ls_sinc_quadrature(double eps, double a_min, double a_max, int M, double C0,
 int ls_gen_master(int mode, const double* tau_d, int R, int64_t len, double h, double* out_d,
                   int64_t ld, void* stream);
 
+/* Device instantiation of the generator's libm routines (csrc/glibc_math.cuh):
+ * y_d[i] = erf(x_d[i]) (fn LS_LIBM_ERF) or exp(x_d[i]) (fn LS_LIBM_EXP), bit-identical to
+ * glibc 2.39's x86-64 erf and FMA exp, which std::erf / std::exp resolve to in the reference
+ * (newton.hpp:34, :50). Exposed so the parity tests can sweep arguments beyond the masters. */
+#define LS_LIBM_ERF 0
+#define LS_LIBM_EXP 1
+int ls_libm_eval(int fn, const double* x_d, double* y_d, int64_t n, void* stream);
+
 /* ---- K2: assembled lattice summation ----------------------------------
  * Replaces detail::assembled_axis_columns (lattice.hpp:220-274) for one
  * axis: column c = nu*R + q of out_d (out_len x M0*R, leading dim ld_out) is

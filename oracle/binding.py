@@ -70,6 +70,7 @@ class _Lib:
             f("potential_matrix", C.c_int, [C.c_int64, C.c_double, C.c_int, _dp, C.c_int, _dp, _dp, _dp, _dp, C.c_int, _dp])
             f("grid_functional", C.c_double, [C.c_int64] * 3 + [C.c_int] + [_dp] * 7 + [C.c_int64] * 2)
             f("quadrature_value", C.c_double, [_dp, _dp, C.c_int, C.c_double])
+            f("libm_eval", C.c_int, [C.c_int, _dp, _dp, C.c_int64])
 
     def _f(self, name, res, args):
         fn = getattr(self.lib, self.p + name)
@@ -117,6 +118,13 @@ class _Lib:
             rc = self._lattice_master(mode, L.ctypes.data_as(_i64p), n, b, _ptr(tau), R, _ptr(f[0]), _ptr(f[1]), _ptr(f[2]))
         self._check(rc, "lattice_master")
         return f
+
+    def libm_eval(self, fn, x):
+        """Host libm erf (fn 0) / exp (fn 1) of every element of x."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        self._check(self._libm_eval(fn, _ptr(x), _ptr(y), x.size), "libm_eval")
+        return y
 
     # ---- tensors ----
     def densify_slabs(self, A, B, Cf, w, k0=0, k1=None):

@@ -102,6 +102,13 @@ int orc_gaussian_moment_vector(double b, int64_t n, double t, int doubled, doubl
     return 0;
 }
 
+/* newton.hpp:34 and :50 call std::erf / std::exp: the host libm, element by element. */
+int orc_libm_eval(int fn, const double* x, double* y, int64_t n) {
+    if (fn != 0 && fn != 1) return 2;
+    for (int64_t i = 0; i < n; ++i) y[i] = fn == 0 ? erf(x[i]) : exp(x[i]);
+    return 0;
+}
+
 /* lattice.hpp:109-113 -> newton.hpp:57-75 (mode 0) or the erf master (mode 1). Axes with
  * equal length share the factor (newton.hpp:60-69), which here just recomputes bit-equal data. */
 int orc_lattice_master(int mode, const int64_t L[3], int64_t n, double b, const double* tau, int R,

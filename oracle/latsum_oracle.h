@@ -31,6 +31,9 @@ double orc_quadrature_value(const double* exponents, const double* weights, int 
 int orc_gaussian_sample_vector(int64_t len, double h, double t, double* out);
 /* newton.hpp:21-37 (erf-difference cell integrals); grid = (b, n) */
 int orc_gaussian_moment_vector(double b, int64_t n, double t, int doubled, double* out);
+/* y[i] = erf(x[i]) (fn 0) or exp(x[i]) (fn 1) from the host libm: the calls std::erf / std::exp
+ * make in gaussian_moment_vector / gaussian_sample_vector (newton.hpp:34, :50). */
+int orc_libm_eval(int fn, const double* x, double* y, int64_t n);
 /* mode 0: build_lattice_master (lattice.hpp:109-113 -> newton.hpp:57-75, midpoint)
  * mode 1: erf master, column q = gaussian_moment_vector(GridSpec(L_l*b, L_l*n), tau_q, true)
  * f[l] receives 2*L[l]*n x R. */

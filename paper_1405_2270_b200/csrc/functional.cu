@@ -6,6 +6,7 @@
 // (canonical.hpp:304-314). Dot products use a fixed lane-strided order and a
 // fixed xor tree, so every result is bitwise reproducible run to run.
 #include "common.cuh"
+#include "glibc_math.cuh"
 
 namespace {
 
@@ -198,7 +199,8 @@ __global__ void probe_error_kernel(const double* __restrict__ tau, const double*
         for (int q = 0; q < R; ++q) {
             const double t = tau[q];
             const double xi = rn_mul(t, mi), xj = rn_mul(t, mj), xk = rn_mul(t, mk);
-            const double fi = exp(-rn_mul(xi, xi)), fj = exp(-rn_mul(xj, xj)), fk = exp(-rn_mul(xk, xk));
+            const double fi = ls::gm::exp(-rn_mul(xi, xi)), fj = ls::gm::exp(-rn_mul(xj, xj)),
+                         fk = ls::gm::exp(-rn_mul(xk, xk));
             sum = rn_add(sum, rn_mul(rn_mul(rn_mul(w[q], fi), fj), fk));
         }
         worst = fmax(worst, fabs(rn_sub(rn_mul(sum, r[p]), 1.0)));

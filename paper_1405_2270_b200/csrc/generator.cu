@@ -9,6 +9,7 @@
 // erf(t*x_{i+1}) and erf(t*x_i) separately as the reference does, and only the
 // lower half of each (exactly even) column is evaluated.
 #include "common.cuh"
+#include "glibc_math.cuh"
 
 namespace {
 
@@ -33,7 +34,7 @@ __global__ void gen_midpoint_kernel(const double* __restrict__ tau, int64_t len,
          i += (int64_t)gridDim.x * blockDim.x) {
         const double mid = rn_mul(rn_sub(rn_add(static_cast<double>(i), 0.5), half_len), h);
         const double x = rn_mul(t, mid);
-        const double v = exp(-rn_mul(x, x));
+        const double v = ls::gm::exp(-rn_mul(x, x));  // glibc exp, bit for bit
         col[i] = v;
         col[len - 1 - i] = v;
     }
@@ -58,18 +59,33 @@ __global__ void gen_erf_kernel(const double* __restrict__ tau, int64_t len, doub
     }
     for (int v = threadIdx.x; v <= kGenThreads; v += kGenThreads) {
         const int64_t vi = i0 + v;
-        if (vi <= half) ev[v] = erf(rn_mul(t, rn_mul(static_cast<double>(vi - half), h)));
+        if (vi <= half) ev[v] = ls::gm::erf(rn_mul(t, rn_mul(static_cast<double>(vi - half), h)));
     }
     __syncthreads();
     if (i < half) {
-        const double scale = sqrt(CUDART_PI) / rn_mul(2.0, t);
+        const double scale = __ddiv_rn(sqrt(CUDART_PI), rn_mul(2.0, t));
         const double v = rn_mul(scale, rn_sub(ev[threadIdx.x + 1], ev[threadIdx.x]));
         col[i] = v;
         col[len - 1 - i] = v;
     }
 }
 
+__global__ void libm_eval_kernel(int fn, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = fn == LS_LIBM_ERF ? ls::gm::erf(x[i]) : ls::gm::exp(x[i]);
+}
+
 }  // namespace
+
+extern "C" int ls_libm_eval(int fn, const double* x_d, double* y_d, int64_t n, void* stream) {
+    if (fn != LS_LIBM_ERF && fn != LS_LIBM_EXP) return ls::fail(LS_EVALIDATION, "libm_eval: unknown function");
+    if (n < 0) return ls::fail(LS_EVALIDATION, "libm_eval: negative length");
+    if (n == 0) return LS_OK;
+    const int blocks = (int)std::min<int64_t>(ls::ceil_div(n, 256), 148 * 16);
+    libm_eval_kernel<<<blocks, 256, 0, ls::as_stream(stream)>>>(fn, x_d, y_d, n);
+    LS_LAUNCHED("libm_eval_kernel");
+    return LS_OK;
+}
 
 extern "C" int ls_gen_master(int mode, const double* tau_d, int R, int64_t len, double h,
                              double* out_d, int64_t ld, void* stream) {
