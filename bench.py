@@ -184,6 +184,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     lib = L.load_library()
     lib.ls_set_device(dev_idx)
+    if lib.ls_dev_knobs_enabled():
+        raise SystemExit("bench.py: liblatsum_cuda.so is a dev build (-DLS_DEV_KNOBS); rebuild the product library")
     N1, N2, N3 = spec.target_dims()
     shard = ShardedPotential(spec, rule, mode="erf", device=dev)
     pipe, k0, k1 = shard.pipe, shard.k0, shard.k1
@@ -377,7 +379,8 @@ def run_other_configs(L, dev):
     else:
         out["cfg2_1gpu"] = {"skipped": "less than 68 GiB of free HBM"}
     x2 = [(np.arange(N2d[l]) + 0.5 - N2d[l] / 2.0) * spec2.unit.h for l in range(3)]
-    r2 = [np.exp(-x * x / 2.0) for x in x2]  # as run_energy: rho = exp(-|x|^2/2), box centre
+    sig2 = energy_sigma(spec2)
+    r2 = [np.exp(-x * x / (2.0 * sig2 * sig2)) for x in x2]  # as run_energy: sigma = L*b/4, box centre
     rho2 = [torch.as_tensor(r, device=dev) for r in r2]
     X2 = [torch.as_tensor(r.reshape(-1, 1), device=dev) for r in r2]
     one_d = lambda: L.DevicePipeline.functional_batch_device([pipe2.factor(l).T for l in range(3)], pipe2.w, X2)  # noqa: E731
@@ -430,7 +433,7 @@ def run_other_configs(L, dev):
     mids = (np.arange(256) + 0.5 - 128) * spec.unit.h
     G = [torch.as_tensor(np.exp(-(mids[:, None] - centres[None, :, l]) ** 2 / (2 * sigma ** 2)), device=dev)
          for l in range(3)]
-    t_f, how_f = _graph_ms(lambda: L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w, G))
+    t_f, how_f = _graph_ms(lambda: L.DevicePipeline.functional_batch_device([pipe.factor(l).T for l in range(3)], pipe.w, G))
     # full-grid form: expansion + fused DMMA GEMM (2 * 256^3 * 1024 FLOP) + fixed-order reduction
     t_fg = _ev_ms(lambda: pipe.grid_functional_batch(G))
     fg_flop = 2.0 * float(np.prod(pipe.dims)) * F
@@ -449,14 +452,21 @@ def run_other_configs(L, dev):
     return out
 
 
+def energy_sigma(spec) -> float:
+    """Width of the energy density: a quarter of the box edge, so the density is >= e^-2 of its
+    peak on every box face and the fused functional epilogue weighs every grid point."""
+    return max(spec.L) * spec.unit.b / 4.0
+
+
 def run_energy(L, shard, spec, world, dev):
     import torch
     N = spec.target_dims()
     h = spec.unit.h
     rho_np = []
+    sigma = energy_sigma(spec)
     for l in range(3):
         x = (np.arange(N[l]) + 0.5 - N[l] / 2.0) * h
-        rho_np.append(np.exp(-x * x / 2.0))  # rank-1 Gaussian density, centre = box centre, sigma = 1 bohr
+        rho_np.append(np.exp(-x * x / (2.0 * sigma * sigma)))  # rank-1 Gaussian, centre = box centre
     rho = [torch.as_tensor(r, device=dev) for r in rho_np]
     shard.energy(rho)  # warm-up
     torch.cuda.synchronize()
@@ -480,7 +490,8 @@ def run_energy(L, shard, spec, world, dev):
     e1d = float(L.DevicePipeline.functional_batch_device([pipe.factor(l).T for l in range(3)], pipe.w, X)[0])
     return {"value": e, "one_d_value": e1d, "rel_diff_vs_1d": abs(e - e1d) / abs(e1d), "ms": round(ms, 3),
             "wall_ms": round(wall_ms, 3),
-            "density": "rho(x)=exp(-|x|^2/2) separable, centre = box centre",
+            "density": f"rho(x)=exp(-|x|^2/(2 sigma^2)) separable, centre = box centre, sigma = L*b/4 = {sigma} bohr "
+                       "(rho >= e^-2 of its peak at every box face, so every grid point carries weight)",
             "path": "fused expansion-reduction over own z-slabs + scalar all_reduce (NCCL)"}
 
 

@@ -47,6 +47,14 @@ int ls_abi_version(void);
 const char* ls_last_error(void);
 /* Sets the CUDA device used by the host-level calls of this thread. */
 int ls_set_device(int device);
+/* Kernel watchdog: 1 if a kernel on the current device abandoned an mbarrier wait after
+ * 20 s (its results are garbage; the kernel drained and exited, the context is intact), else
+ * 0; reset != 0 clears the flag. The host-level ls_h_* calls check it themselves and return
+ * LS_ECUDA. */
+int ls_fault_status(int reset);
+/* 1 if this build reads the development A/B knobs (LS_EXPAND_PLAN, LS_EXPAND_DEBUG, ...) from
+ * the environment (-DLS_DEV_KNOBS); the product build returns 0 and ignores them. */
+int ls_dev_knobs_enabled(void);
 /* Number of kernel launches this library issued since load (all threads). */
 int64_t ls_launch_count(void);
 

@@ -42,6 +42,8 @@ SIGNATURES = {
     "ls_sinc_quadrature": (_i, [_d, _d, _d, _i, _d, _vp, _vp, _vp, _dp]),
     "ls_gen_master": (_i, [_i, _vp, _i, _i64, _d, _vp, _i64, _vp]),
     "ls_libm_eval": (_i, [_i, _vp, _vp, _i64, _vp]),
+    "ls_fault_status": (_i, [_i]),
+    "ls_dev_knobs_enabled": (_i, []),
     "ls_assemble_axis": (_i, [_vp, _i64, _i, _i, _vp, _i64, _i64, _i, _vp, _i64, _vp]),
     "ls_expand": (_i, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i, _i64, _i64, _vp, _i64, _i64,
                        _vp, _vp, _vp, _vp, _vp]),

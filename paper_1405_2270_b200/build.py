@@ -21,6 +21,12 @@ OBJ = ROOT / "build" / "obj"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}", "-Xptxas", "-v"]
+# `--dev` (or LS_BUILD_DEV=1) compiles in the development A/B knobs (LS_EXPAND_PLAN, ...) that
+# the lab scripts under tools/ use; the product build ignores the environment.
+DEV = "--dev" in sys.argv or os.environ.get("LS_BUILD_DEV") == "1"
+if DEV:
+    FLAGS.append("-DLS_DEV_KNOBS")
+    OBJ = ROOT / "build" / "obj_dev"
 
 
 def sources():
@@ -47,6 +53,9 @@ def _compile(src: Path) -> tuple[Path, str]:
 
 def build(verbose: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
+    marker = OUT.with_suffix(".dev")
+    if OUT.exists() and marker.exists() != DEV:
+        OUT.unlink()  # switching between the product and the dev build: relink from this OBJ dir
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         results = list(ex.map(_compile, sources()))
     objs = [o for o, _ in results]
@@ -61,6 +70,10 @@ def build(verbose: bool = False) -> Path:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         tmp.replace(OUT)
+        if DEV:
+            marker.touch()
+        elif marker.exists():
+            marker.unlink()
     return OUT
 
 

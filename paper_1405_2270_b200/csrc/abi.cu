@@ -38,6 +38,31 @@ int sm_count() {
     return cache[dev];
 }
 
+unsigned* fault_flag() {
+    static std::mutex mu;
+    static std::vector<unsigned*> flags;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= static_cast<int>(flags.size())) flags.resize(dev + 1, nullptr);
+    if (flags[dev] == nullptr) {
+        unsigned* f = nullptr;
+        if (cudaMalloc(&f, sizeof(unsigned)) != cudaSuccess) return nullptr;
+        if (cudaMemset(f, 0, sizeof(unsigned)) != cudaSuccess) return nullptr;
+        flags[dev] = f;
+    }
+    return flags[dev];
+}
+
+bool take_fault() {
+    unsigned* f = fault_flag();
+    if (f == nullptr) return false;
+    unsigned v = 0;
+    if (cudaMemcpy(&v, f, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    if (v != 0) cudaMemset(f, 0, sizeof(unsigned));
+    return v != 0;
+}
+
 void ensure_pool() {
     static std::mutex mu;
     static std::vector<char> done;
@@ -169,6 +194,7 @@ int expand_to_host(const double* A, const double* B, const double* C, const doub
     if (rc != LS_OK) return rc;
     if (e1 != cudaSuccess) return cuda_fail(e1, "copy stream");
     if (e2 != cudaSuccess) return cuda_fail(e2, "compute stream");
+    if (take_fault()) return fail(LS_ECUDA, "kernel watchdog: an mbarrier wait timed out (results discarded)");
     return LS_OK;
 }
 
@@ -183,6 +209,23 @@ extern "C" {
 int ls_abi_version(void) { return 1; }
 
 const char* ls_last_error(void) { return ls::last_error().c_str(); }
+
+int ls_fault_status(int reset) {
+    unsigned* f = ls::fault_flag();
+    if (f == nullptr) return ls::fail(LS_ECUDA, "fault_status: no CUDA device");
+    unsigned v = 0;
+    LS_CUDA(cudaMemcpy(&v, f, sizeof(v), cudaMemcpyDeviceToHost));
+    if (v != 0 && reset) LS_CUDA(cudaMemset(f, 0, sizeof(unsigned)));
+    return v != 0 ? 1 : 0;
+}
+
+int ls_dev_knobs_enabled(void) {
+#ifdef LS_DEV_KNOBS
+    return 1;
+#else
+    return 0;
+#endif
+}
 
 int ls_set_device(int device) {
     LS_CUDA(cudaSetDevice(device));
@@ -308,7 +351,7 @@ int ls_h_calibrate_quadrature(double b, int64_t n, double eps, double a_min, dou
             LS_TRY(ls_probe_error(dtau.d(), dw.d(), R, n, h, didx.i(), drad.d(), P, derr.d() + d, s));
         }
         LS_CUDA(cudaMemcpyAsync(errs, derr.p, sizeof(errs), cudaMemcpyDeviceToHost, s));
-        LS_CUDA(cudaStreamSynchronize(s));
+        LS_SYNC(s);
         int pick = 0;
         for (int d = 0; d < 4; ++d) {
             if (trace_len && n_trace < trace_cap) {
@@ -343,7 +386,7 @@ int ls_h_gen_column(int mode, double t, int64_t len, double h, double* out_h) {
     LS_TRY(out.alloc(sizeof(double) * static_cast<size_t>(std::max<int64_t>(len, 1)), st->compute));
     LS_TRY(ls_gen_master(mode, tau.d(), 1, len, h, out.d(), len, st->compute));
     LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double) * len, cudaMemcpyDeviceToHost, st->compute));
-    LS_CUDA(cudaStreamSynchronize(st->compute));
+    LS_SYNC(st->compute);
     return LS_OK;
 }
 
@@ -368,7 +411,7 @@ int ls_h_newton_master(int mode, const int64_t lens[3], double h, const double* 
         for (int m = 0; m < l; ++m)
             if (lens[m] == lens[l]) same = m;
         if (same >= 0) {
-            LS_CUDA(cudaStreamSynchronize(st->compute));
+            LS_SYNC(st->compute);
             std::memcpy(outs[l], outs[same], sizeof(double) * static_cast<size_t>(lens[l] * R));
             continue;
         }
@@ -376,7 +419,7 @@ int ls_h_newton_master(int mode, const int64_t lens[3], double h, const double* 
         LS_TRY(f.alloc(sizeof(double) * static_cast<size_t>(lens[l] * R), st->compute));
         LS_TRY(ls_gen_master(mode, tau.d(), R, lens[l], h, f.d(), lens[l], st->compute));
         LS_CUDA(cudaMemcpyAsync(outs[l], f.p, sizeof(double) * lens[l] * R, cudaMemcpyDeviceToHost, st->compute));
-        LS_CUDA(cudaStreamSynchronize(st->compute));
+        LS_SYNC(st->compute);
     }
     return LS_OK;
 }
@@ -403,7 +446,7 @@ int ls_h_functional_batch(const int64_t dims[3], int R, const double* A_h, const
     LS_TRY(ls_functional_batch(A.d(), dims[0], B.d(), dims[1], C.d(), dims[2], w.d(), R, dims[0], dims[1], dims[2],
                                X.d(), dims[0], Y.d(), dims[1], Z.d(), dims[2], F, scale, out.d(), st->compute));
     LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double) * F, cudaMemcpyDeviceToHost, st->compute));
-    LS_CUDA(cudaStreamSynchronize(st->compute));
+    LS_SYNC(st->compute);
     return LS_OK;
 }
 
@@ -424,8 +467,8 @@ int ls_h_max_norm_diff(const int64_t dims[3], int Ra, const double* A0_h, const 
         LS_TRY(ls::upload(fa[l], ah[l], sizeof(double) * dims[l] * Ra, s));
         LS_TRY(ls::upload(fb[l], bh[l], sizeof(double) * dims[l] * Rb, s));
     }
-    LS_TRY(ls::upload(wa, wa_h, sizeof(double) * std::max(Ra, 1), s));
-    LS_TRY(ls::upload(wb, wb_h, sizeof(double) * std::max(Rb, 1), s));
+    LS_TRY(ls::upload(wa, wa_h, sizeof(double) * Ra, s));
+    LS_TRY(ls::upload(wb, wb_h, sizeof(double) * Rb, s));
     // Both tensors expanded chunk by chunk on the device; the grids never leave HBM
     // (max_norm_diff_canonical, canonical.hpp:282-301).
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(dims[2], (256ll << 20) / (slab * 8)));
@@ -444,7 +487,7 @@ int ls_h_max_norm_diff(const int64_t dims[3], int Ra, const double* A0_h, const 
     }
     std::vector<double> hp(2 * static_cast<size_t>(nblocks));
     LS_CUDA(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, s));
-    LS_CUDA(cudaStreamSynchronize(s));
+    LS_SYNC(s);
     for (int b = 0; b < nblocks; ++b) {
         *max_diff_h = std::max(*max_diff_h, hp[2 * b]);
         *max_abs_b_h = std::max(*max_abs_b_h, hp[2 * b + 1]);
@@ -474,7 +517,7 @@ int ls_h_lattice_master(int mode, const int64_t L[3], int64_t n, double b, const
         for (int m = 0; m < l; ++m)
             if (L[m] == L[l]) same = m;
         if (same >= 0) {
-            LS_CUDA(cudaStreamSynchronize(st->compute));
+            LS_SYNC(st->compute);
             std::memcpy(outs[l], outs[same], sizeof(double) * static_cast<size_t>(len * R));
             continue;
         }
@@ -482,7 +525,7 @@ int ls_h_lattice_master(int mode, const int64_t L[3], int64_t n, double b, const
         LS_TRY(f.alloc(sizeof(double) * static_cast<size_t>(len * R), st->compute));
         LS_TRY(ls_gen_master(mode, tau.d(), R, len, h, f.d(), len, st->compute));
         LS_CUDA(cudaMemcpyAsync(outs[l], f.p, sizeof(double) * len * R, cudaMemcpyDeviceToHost, st->compute));
-        LS_CUDA(cudaStreamSynchronize(st->compute));
+        LS_SYNC(st->compute);
     }
     return LS_OK;
 }
@@ -500,7 +543,7 @@ int ls_h_assemble_axis(const double* master_h, int64_t master_len, int R, int M0
     LS_TRY(out.alloc(sizeof(double) * out_len * M0 * R, st->compute));
     LS_TRY(ls_assemble_axis(m.d(), master_len, R, M0, ia.i(), n, L, periodic, out.d(), out_len, st->compute));
     LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double) * out_len * M0 * R, cudaMemcpyDeviceToHost, st->compute));
-    LS_CUDA(cudaStreamSynchronize(st->compute));
+    LS_SYNC(st->compute);
     return LS_OK;
 }
 
@@ -535,7 +578,7 @@ int ls_h_eval_points(const int64_t dims[3], int R, const double* A_h, const doub
     LS_TRY(out.alloc(sizeof(double) * P, st->compute));
     LS_TRY(ls_eval_points(A.d(), dims[0], B.d(), dims[1], C.d(), dims[2], w.d(), R, idx.i(), P, out.d(), st->compute));
     LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double) * P, cudaMemcpyDeviceToHost, st->compute));
-    LS_CUDA(cudaStreamSynchronize(st->compute));
+    LS_SYNC(st->compute);
     return LS_OK;
 }
 
@@ -562,7 +605,7 @@ int ls_h_scalar_product(const int64_t dims[3], int Ra, const double* A0_h, const
     LS_TRY(out.alloc(sizeof(double), st->compute));
     LS_TRY(ls_gram_reduce(G[0].d(), G[1].d(), G[2].d(), wa.d(), Ra, wb.d(), Rb, out.d(), st->compute));
     LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double), cudaMemcpyDeviceToHost, st->compute));
-    LS_CUDA(cudaStreamSynchronize(st->compute));
+    LS_SYNC(st->compute);
     return LS_OK;
 }
 
@@ -577,7 +620,7 @@ int ls_h_grid_functional(const int64_t dims[3], int R, const double* A_h, const 
     LS_TRY(ls::upload(A, A_h, sizeof(double) * dims[0] * R, st->compute));
     LS_TRY(ls::upload(B, B_h, sizeof(double) * dims[1] * R, st->compute));
     LS_TRY(ls::upload(C, C_h, sizeof(double) * dims[2] * R, st->compute));
-    LS_TRY(ls::upload(w, w_h, sizeof(double) * std::max(R, 1), st->compute));
+    LS_TRY(ls::upload(w, w_h, sizeof(double) * R, st->compute));
     LS_TRY(ls::upload(r1, r1_h, sizeof(double) * dims[0], st->compute));
     LS_TRY(ls::upload(r2, r2_h, sizeof(double) * dims[1], st->compute));
     LS_TRY(ls::upload(r3, r3_h, sizeof(double) * dims[2], st->compute));
@@ -590,7 +633,7 @@ int ls_h_grid_functional(const int64_t dims[3], int R, const double* A_h, const 
                      k0, k1, nullptr, 0, 0, r1.d(), r2.d(), r3.d(), part.d(), st->compute));
     LS_TRY(ls_sum_partials(part.d(), np, out.d(), st->compute));
     LS_CUDA(cudaMemcpyAsync(out_h, out.p, sizeof(double), cudaMemcpyDeviceToHost, st->compute));
-    LS_CUDA(cudaStreamSynchronize(st->compute));
+    LS_SYNC(st->compute);
     return LS_OK;
 }
 
@@ -654,7 +697,7 @@ int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, co
     if (grid_h) {
         LS_TRY(ls::expand_to_host(fptr[0], fptr[1], fptr[2], wd.d(), d, Rt, k0, k1, grid_h, *st));
     } else {
-        LS_CUDA(cudaStreamSynchronize(s));
+        LS_SYNC(s);
     }
     return LS_OK;
 }

@@ -6,6 +6,7 @@
 #include <math_constants.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 #include <string>
 #include <utility>
@@ -40,6 +41,32 @@ inline int cuda_fail(cudaError_t e, const char* where) {
         if (_e != cudaSuccess) return ::ls::cuda_fail(_e, name);        \
     } while (0)
 
+// Kernel watchdog: a device word per device that a timed-out mbarrier wait sets (k3.cuh
+// mbar_wait); every other wait then returns at once, so the kernel drains and exits normally
+// (TMEM released, context intact) and the host reports LS_ECUDA instead of hanging or
+// trapping. fault_flag() is the current device's word; take_fault() reads and clears it.
+unsigned* fault_flag();
+bool take_fault();
+
+#define LS_SYNC(stream)                                                                   \
+    do {                                                                                  \
+        LS_CUDA(cudaStreamSynchronize(stream));                                           \
+        if (::ls::take_fault())                                                           \
+            return ::ls::fail(LS_ECUDA, "kernel watchdog: an mbarrier wait timed out (results discarded)"); \
+    } while (0)
+
+// Development A/B knobs (forced plans, debug modes, verbose plan print) are read from the
+// environment only in a build with -DLS_DEV_KNOBS (python -m paper_1405_2270_b200.build --dev);
+// the product library never changes its work based on the environment.
+inline const char* dev_knob(const char* name) {
+#ifdef LS_DEV_KNOBS
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -56,6 +83,22 @@ struct DeviceGuard {
     }
     DeviceGuard(const DeviceGuard&) = delete;
     DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// Stream-ordered scratch from the device pool, released on every exit path (early error
+// returns included) with cudaFreeAsync on the stream it was allocated on.
+struct AsyncScratch {
+    void* p = nullptr;
+    cudaStream_t s;
+    explicit AsyncScratch(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, s); }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    ~AsyncScratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    AsyncScratch(const AsyncScratch&) = delete;
+    AsyncScratch& operator=(const AsyncScratch&) = delete;
 };
 
 // Number of SMs of the current device (cached per device).

@@ -237,7 +237,7 @@ expand_dmma_kernel(const ExpandArgs p) {
             compute_scale(unit + gridDim.x, scale + (parity ^ 1) * rpad);  // read after the unit barrier
 
         const int slot = st % kNS;
-        mbar_wait(full + slot, static_cast<unsigned>((st / kNS) & 1));
+        mbar_wait(full + slot, static_cast<unsigned>((st / kNS) & 1), p.fault);
         const double* stage = ring + slot * stage_elems;
         if (kc == 0) {
 #pragma unroll
@@ -450,7 +450,7 @@ struct TmemShape {
 };
 inline TmemShape tmem_shape() {
     TmemShape sh{4, 1};
-    if (const char* e = std::getenv("LS_EXPAND_TMEM")) {
+    if (const char* e = ls::dev_knob("LS_EXPAND_TMEM")) {
         const int v = std::atoi(e);
         sh = {v / 10, v % 10};
     }
@@ -477,7 +477,7 @@ bool fits_tmem_shape(int KD, int n_tail, TmemShape sh) {
 }
 // Ring depth 4 where it fits (ranks up to 45), else 3 (up to 57); LS_EXPAND_TMEM overrides.
 TmemShape tmem_shape_for(int KD, int n_tail) {
-    if (std::getenv("LS_EXPAND_TMEM")) return tmem_shape();
+    if (ls::dev_knob("LS_EXPAND_TMEM")) return tmem_shape();
     return fits_tmem_shape(KD, n_tail, {4, 1}) ? TmemShape{4, 1} : TmemShape{3, 1};
 }
 bool fits_tmem(int KD, int n_tail) { return fits_tmem_shape(KD, n_tail, tmem_shape_for(KD, n_tail)); }
@@ -503,7 +503,7 @@ bool fits(int KD, int KC, int n_tail) {
 
 bool plan_for(int KD, int n_tail, Plan& out) {
     int force = -1;
-    if (const char* e = std::getenv("LS_EXPAND_PLAN")) force = std::atoi(e);  // development A/B knob
+    if (const char* e = ls::dev_knob("LS_EXPAND_PLAN")) force = std::atoi(e);  // development A/B knob
     struct Cand {
         int id, KC;
     };
@@ -551,7 +551,7 @@ bool plan_for(int KD, int n_tail, Plan& out) {
         if (ok) {
             const int pad = c.id == kPlanTmem16 && n_tail == 2;
             out = {c.id, c.id == kPlanTmem16 ? tmem16_stage_ks(KD + pad, pad ? 0 : n_tail) : KC + pad, ic, pad};
-            if (const char* e = std::getenv("LS_EXPAND_KC")) out.KC = std::max(1, std::min(KD, std::atoi(e)));
+            if (const char* e = ls::dev_knob("LS_EXPAND_KC")) out.KC = std::max(1, std::min(KD, std::atoi(e)));
             return true;
         }
     }
@@ -605,23 +605,24 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     a.n_jc = ls::ceil_div(a.N2, JC);
     a.n_jt = a.n_jc * JT;
     a.n_kc = static_cast<int>(ls::ceil_div(a.KD, a.KC));
-    // Pack A2 once per call (stream-ordered scratch from the pool).
-    double* bp = nullptr;
+    // 32-bit counters inside the kernel
+    if (a.n_units * a.n_jc * a.n_kc >= (int64_t(1) << 31) || a.N1 + T::IC >= (int64_t(1) << 31) ||
+        a.N2 + JC >= (int64_t(1) << 31))
+        return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
+    // Pack A2 once per call (stream-ordered scratch from the pool, freed on every exit path).
     const size_t stage_elems = static_cast<size_t>(JT) * a.KC * 32 + static_cast<size_t>(JT) * 8 * a.n_tail;
     const size_t bp_elems = static_cast<size_t>(a.n_kc) * a.n_jc * stage_elems;
     const size_t s_elems = TMEM ? static_cast<size_t>(a.k1) * a.R : 0;
     ls::ensure_pool();
-    LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bp), (bp_elems + s_elems) * sizeof(double), s));
+    ls::AsyncScratch scratch(s);
+    LS_CUDA(scratch.alloc((bp_elems + s_elems) * sizeof(double)));
+    double* bp = scratch.as<double>();
     a.S = TMEM ? bp + bp_elems : nullptr;
     const int64_t pb = std::min<int64_t>(ls::ceil_div(static_cast<int64_t>(bp_elems + s_elems), 256), 4096);
     LS_CUDA(ls::launch_pdl(pack_b_kernel, dim3((unsigned)pb), dim3(256), 0, s, a.B, a.ldb, a.N2, a.R, a.KD,
                            a.n_tail, a.KC, a.n_kc, JT, a.n_jc, bp, a.w, a.C, a.ldc, a.k1, const_cast<double*>(a.S)));
     LS_LAUNCHED("pack_b_kernel");
     a.Bp = bp;
-    // 32-bit counters inside the kernel
-    if (a.n_units * a.n_jc * a.n_kc >= (int64_t(1) << 31) || a.N1 + T::IC >= (int64_t(1) << 31) ||
-        a.N2 + JC >= (int64_t(1) << 31))
-        return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
     const size_t smem =
         TMEM ? sizeof(double) * (32 + tmem_stg_elems(T::WARPS) + sh.ns * stage_elems) : smem_bytes<T>(a.KD, a.KC, a.n_tail);
     void (*kern)(ExpandArgs) = nullptr;
@@ -661,7 +662,7 @@ int launch(ExpandArgs& a, cudaStream_t s) {
             grid = std::min<int64_t>(a.n_units * a.n_jc, G);
         }
     }
-    if (std::getenv("LS_EXPAND_VERBOSE"))
+    if (ls::dev_knob("LS_EXPAND_VERBOSE"))
         std::fprintf(stderr, "ls_expand: tile %dx%d warps, IC %d, KC %d/%d, smem %zu B, %d CTA/SM, grid %lld, %s\n",
                      T::WARPS, T::WI, T::IC, a.KC, a.KD, smem, per_sm, static_cast<long long>(grid),
                      TMEM ? "A1k in TMEM" : "A1k in smem");
@@ -669,7 +670,6 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         LS_CUDA(ls::launch_pdl(kern, dim3((unsigned)grid), dim3(T::WARPS * 32), smem, s, a));
         LS_LAUNCHED("expand_dmma_kernel");
     }
-    LS_CUDA(cudaFreeAsync(bp, s));
     return LS_OK;
 }
 
@@ -778,7 +778,9 @@ extern "C" int ls_expand(const double* A_d, int64_t lda, const double* B_d, int6
     a.out = out_d; a.ldy = ldy; a.ldz = ldz;
     a.vec_store = (ldy % 2 == 0 && ldz % 2 == 0 && (reinterpret_cast<uintptr_t>(out_d) & 15) == 0) ? 1 : 0;
     a.rho1 = rho1_d; a.rho2 = rho2_d; a.rho3 = rho3_d; a.partial = partial_d;
-    if (const char* dbg = std::getenv("LS_EXPAND_DEBUG")) a.debug = std::atoi(dbg);
+    if (const char* dbg = ls::dev_knob("LS_EXPAND_DEBUG")) a.debug = std::atoi(dbg);
+    a.fault = ls::fault_flag();
+    if (a.fault == nullptr) return ls::fail(LS_ECUDA, "expand: no CUDA device");
     const bool store = out_d != nullptr;
     Plan pl;
     if (plan_for(a.KD, a.n_tail, pl)) {

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
         for (int w = 0; w < per_unit; ++w, ++st) {
             const int jc = w / n_kc, kc = w % n_kc;
             const int slot = st % kSkNS;
-            mbar_wait(full + slot, static_cast<unsigned>((st / kSkNS) & 1));
+            mbar_wait(full + slot, static_cast<unsigned>((st / kSkNS) & 1), p.fault);
             const double* stage = ring + slot * stage_elems;
             const int jt0 = wj * kTM;
             if (kc == 0) {
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
                 if (lane == 0) mbar_arrive(ready + pair);
                 continue;
             }
-            mbar_wait(ready + pair, phase);
+            mbar_wait(ready + pair, phase, p.fault);
             // half 0 + half 1, in that order whichever warp reduces
 #pragma unroll
             for (int m = 0; m < kTM; ++m)
@@ -427,9 +427,10 @@ int launch_splitk(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_c
     const size_t stage_elems = static_cast<size_t>(2 * kSkJT * kSkKC * 32 + kSkJT * 8 * a.n_tail);
     const size_t bp_elems = static_cast<size_t>(n_kc) * a.n_jc * stage_elems;
     const size_t s_elems = static_cast<size_t>(a.k1) * a.R;
-    double* bp = nullptr;
     ls::ensure_pool();
-    LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bp), (bp_elems + s_elems) * sizeof(double), s));
+    ls::AsyncScratch scratch(s);  // freed on every exit path
+    LS_CUDA(scratch.alloc((bp_elems + s_elems) * sizeof(double)));
+    double* bp = scratch.as<double>();
     a.S = bp + bp_elems;
     const int64_t pb = std::min<int64_t>(ls::ceil_div(static_cast<int64_t>(bp_elems + s_elems), 256), 4096);
     LS_CUDA(ls::launch_pdl(pack_splitk_kernel, dim3((unsigned)pb), dim3(256), 0, s, a.B, a.ldb, a.N2, a.R, a.KD, KH,
@@ -447,7 +448,6 @@ int launch_splitk(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_c
         LS_CUDA(ls::launch_pdl(kern, dim3((unsigned)grid), dim3(kSkWarps * 32), smem, s, a));
         LS_LAUNCHED("expand_splitk_kernel");
     }
-    LS_CUDA(cudaFreeAsync(bp, s));
     return LS_OK;
 }
 

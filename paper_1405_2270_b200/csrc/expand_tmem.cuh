@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         const bool has_next = n + 1 < my_units;
         const int ib = (unit % n_ichunks) * IC;
         const int64_t kk = unit / n_ichunks;
-        mbar_wait(as_full + buf, static_cast<unsigned>((n >> 1) & 1));
+        mbar_wait(as_full + buf, static_cast<unsigned>((n >> 1) & 1), p.fault);
         tmem::fence_after();
         const uint32_t tb = tq + static_cast<uint32_t>(buf * CB);
         // rho1 of this lane's eight i columns, held for the whole unit (zero beyond N1, where the
@@ -359,10 +359,10 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 while (target < n_tasks && fill_stage(target) <= w) ++target;
             const bool fill_now = target > next_task;
             if (fill_now && next_task == 0 && n >= 1)  // buffer buf^1 was read by unit n-1
-                mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1));
+                mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1), p.fault);
 
             const int slot = st % kNS;
-            mbar_wait(full + slot, static_cast<unsigned>((st / kNS) & 1));
+            mbar_wait(full + slot, static_cast<unsigned>((st / kNS) & 1), p.fault);
             const double* stage = ring + slot * stage_elems;
 #pragma unroll 1
             for (int h = 0; h < JPS; ++h) {
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         if (has_next && n_tasks == 0) publish(buf ^ 1);  // no fill share (KD = 1, wj = 1): still arrive
         if (has_next && next_task < n_tasks) {  // tiny units: finish the fill now
             if (next_task == 0 && n >= 1)
-                mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1));
+                mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1), p.fault);
             for (; next_task < n_tasks; ++next_task) run_task(n + 1, next_task, buf ^ 1);
             publish(buf ^ 1);
         }

@@ -155,6 +155,21 @@ __global__ void functional_batch_kernel(const double* __restrict__ A, int64_t ld
     }
 }
 
+// Ranks whose Gram entries do not fit in shared memory: G_l (R x Fc, from gram_kernel, the same
+// warp_dot as above) comes from global scratch, and one thread per density forms the same
+// rank-ordered sum, so the result is bit-identical to the shared-memory kernels.
+__global__ void functional_reduce_kernel(const double* __restrict__ G0, const double* __restrict__ G1,
+                                         const double* __restrict__ G2, const double* __restrict__ w, int R,
+                                         int Fc, double scale, double* __restrict__ out) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= Fc) return;
+    const int64_t c = static_cast<int64_t>(R) * f;
+    double sum = 0.0;
+    for (int q = 0; q < R; ++q)
+        sum = rn_add(sum, rn_mul(rn_mul(rn_mul(rn_mul(w[q], 1.0), G0[c + q]), G1[c + q]), G2[c + q]));
+    out[f] = rn_mul(scale, sum);
+}
+
 // Block-partial max |a - b| and max |b| over n entries (max is order-independent: exact).
 __global__ void maxdiff_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
                                double* __restrict__ part) {
@@ -278,11 +293,40 @@ extern "C" int ls_functional_batch(const double* A_d, int64_t lda, const double*
         return ls::fail(LS_EVALIDATION, "functional_batch: bad shape");
     if (F == 0) return LS_OK;
     // Batches too small to fill the GPU with kFBatch densities per block take one per block
-    // with the single-density kernel (cfg2's one energy density).
-    const int fb = F >= kFBatch * ls::sm_count() ? kFBatch : 1;
-    const size_t smem = sizeof(double) * 3 * static_cast<size_t>(R) * fb;
-    if (smem > 200 * 1024) return ls::fail(LS_EGUARD, "functional_batch: rank too large");
+    // with the single-density kernel (cfg2's one energy density); either kernel keeps its 3R
+    // Gram entries per density in shared memory, and ranks beyond that take the global-scratch
+    // path (bit-identical results).
+    constexpr size_t kSmemCap = 200 * 1024;
+    const size_t per_f = sizeof(double) * 3 * static_cast<size_t>(R);
+    const int fb = (F >= kFBatch * ls::sm_count() && per_f * kFBatch <= kSmemCap) ? kFBatch : 1;
+    const size_t smem = per_f * fb;
     const cudaStream_t s = ls::as_stream(stream);
+    if (smem > kSmemCap) {
+        // F chunked so the three R x Fc Gram blocks stay within 256 MiB of scratch.
+        const int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, (int64_t(32) << 20) / (3 * (int64_t)R)));
+        ls::ensure_pool();
+        ls::AsyncScratch scratch(s);
+        LS_CUDA(scratch.alloc(sizeof(double) * 3 * static_cast<size_t>(R) * Fc));
+        double* G = scratch.as<double>();
+        for (int64_t f0 = 0; f0 < F; f0 += Fc) {
+            const int fc = static_cast<int>(std::min<int64_t>(Fc, F - f0));
+            const double* fac[3] = {A_d, B_d, C_d};
+            const int64_t ldf[3] = {lda, ldb, ldc};
+            const double* rho[3] = {X_d, Y_d, Z_d};
+            const int64_t ldr[3] = {ldx, ldy, ldz};
+            const int64_t nl[3] = {n1, n2, n3};
+            for (int l = 0; l < 3; ++l) {
+                const int64_t blocks = ls::ceil_div((int64_t)R * fc * 32, 256);
+                gram_kernel<<<(unsigned)blocks, 256, 0, s>>>(fac[l], ldf[l], R, rho[l] + ldr[l] * f0, ldr[l], fc,
+                                                             nl[l], G + (int64_t)l * R * Fc);
+                LS_LAUNCHED("gram_kernel");
+            }
+            functional_reduce_kernel<<<(unsigned)ls::ceil_div(fc, 128), 128, 0, s>>>(
+                G, G + (int64_t)R * Fc, G + 2 * (int64_t)R * Fc, w_d, R, fc, scale, out_d + f0);
+            LS_LAUNCHED("functional_reduce_kernel");
+        }
+        return LS_OK;
+    }
     if (fb == 1) {
         auto kern = functional_batch_single_kernel;
         if (smem > 48 * 1024)

@@ -58,6 +58,7 @@ struct GridBatchArgs {
     int F;
     int64_t M;  // N2 * N3
     double* part;  // [n_mtiles][F]
+    unsigned* fault;  // watchdog word of the device (ls::fault_flag)
 };
 
 // Epilogue shared by both feeds: weight by Y(j,f) * Z(k,f), sum this lane's rows (mi ascending),
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 
     for (int kc = 0; kc < n_kc; ++kc) {
         const int st = kc % kTmaNS;
-        ls_k3::mbar_wait(full + st, (kc / kTmaNS) & 1);
+        ls_k3::mbar_wait(full + st, (kc / kTmaNS) & 1, p.fault);
         const uint8_t* sa = gbase + st * kTmaStage + arow;
         const uint8_t* sb = gbase + st * kTmaStage + brow;
 #pragma unroll
@@ -383,16 +384,17 @@ extern "C" int ls_grid_functional_batch(const double* V_d, int64_t N1, int64_t N
     const int64_t n_mtiles = ls::ceil_div(M, BM);
     if (n_mtiles > 65535) return ls::fail(LS_EGUARD, "grid_functional_batch: more than 65535*128 rows (split k)");
     ls::ensure_pool();
-    double* part = nullptr;
-    LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * n_mtiles * F, s));
-    GridBatchArgs a{V_d, N1, N2, N3, ldy, ldz, X_d, ldx, Y_d, ldyy, Z_d, ldzz, F, M, part};
+    ls::AsyncScratch scratch(s);  // freed on every exit path
+    LS_CUDA(scratch.alloc(sizeof(double) * n_mtiles * F));
+    double* part = scratch.as<double>();
+    GridBatchArgs a{V_d, N1, N2, N3, ldy, ldz, X_d, ldx, Y_d, ldyy, Z_d, ldzz, F, M, part, ls::fault_flag()};
     const bool vec = (reinterpret_cast<uintptr_t>(V_d) % 16 == 0) && (reinterpret_cast<uintptr_t>(X_d) % 16 == 0) &&
                      N1 % 2 == 0 && ldy % 2 == 0 && ldz % 2 == 0 && ldx % 2 == 0;
     const dim3 grid(static_cast<unsigned>(ls::ceil_div(F, BN)), static_cast<unsigned>(n_mtiles));
     // tensor-map feed when the rows have one stride (and within TMA's limits), else cp.async
     CUtensorMap tv, tx;
     const bool tma = vec && ldz == ldy * N2 && M <= INT32_MAX && ldy < (int64_t(1) << 36) &&
-                     ldx < (int64_t(1) << 36) && std::getenv("LS_GRID_BATCH_CPASYNC") == nullptr &&
+                     ldx < (int64_t(1) << 36) && ls::dev_knob("LS_GRID_BATCH_CPASYNC") == nullptr &&
                      make_map(&tv, V_d, N1, M, ldy, BM) && make_map(&tx, X_d, N1, F, ldx, BN);
     if (tma) {
         LS_CUDA(cudaFuncSetAttribute(grid_batch_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -409,6 +411,5 @@ extern "C" int ls_grid_functional_batch(const double* V_d, int64_t N1, int64_t N
     grid_batch_reduce_kernel<<<static_cast<unsigned>(ls::ceil_div(F, 32)), 32 * kRedWarps, 0, s>>>(
         part, n_mtiles, F, scale, accumulate, out_d);
     LS_LAUNCHED("grid_batch_reduce_kernel");
-    LS_CUDA(cudaFreeAsync(part, s));
     return LS_OK;
 }

@@ -38,6 +38,7 @@ struct ExpandArgs {
     int accumulate;   // add into out / partial instead of overwriting (rank-chunked expansions)
     const double* S;  // per-slab scales S(k, q) = w_q * A3(k, q), [k][q] (TMEM variant)
     int split_tail;   // TMEM store-only: split the last round of units at stage granularity
+    unsigned* fault;  // watchdog word of the device (ls::fault_flag)
 };
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -76,13 +77,20 @@ __device__ __forceinline__ uint64_t global_ns() {
     return t;
 }
 // Waits for the phase with the given parity. A wait that has not completed after 20 s (no stage
-// of any plan takes more than milliseconds) traps: a protocol error surfaces as a launch
-// failure instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+// of any plan takes more than milliseconds) sets the device's fault word (ls::fault_flag) and
+// returns; once the word is set every other wait returns at once too, so the kernel drains,
+// releases its TMEM and exits, and the host-level call reports LS_ECUDA (ls_fault_status for
+// device-level callers) instead of hanging the GPU or trapping the context.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity, unsigned* fault) {
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = global_ns();
-    while (!mbar_try_wait(bar, parity))
-        if (global_ns() - t0 > 20000000000ull) __trap();
+    while (!mbar_try_wait(bar, parity)) {
+        if (*reinterpret_cast<volatile unsigned*>(fault) != 0) return;
+        if (global_ns() - t0 > 20000000000ull) {
+            atomicExch(fault, 1u);
+            return;
+        }
+    }
 }
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile(

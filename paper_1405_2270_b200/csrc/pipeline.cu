@@ -204,7 +204,7 @@ int ls_pipeline_energy(ls_pipeline* p, const double* r1_d, const double* r2_d, c
     const int64_t np = ls_expand_partial_count(p->dims[0], p->dims[1], p->Rt, k0, k1);
     if (np < 0) return ls::fail(LS_EGUARD, "energy: no tile plan for this rank");
     if (np > p->partial_cap) {
-        LS_CUDA(cudaStreamSynchronize(ls::as_stream(stream)));
+        LS_SYNC(ls::as_stream(stream));
         cudaFree(p->partial);
         p->partial = nullptr;
         LS_CUDA(cudaMalloc(&p->partial, sizeof(double) * std::max<int64_t>(np, 1)));
@@ -229,12 +229,12 @@ int ls_device_free(void* p_d) {
 
 int ls_memcpy(void* dst, const void* src, size_t bytes, void* stream) {
     LS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ls::as_stream(stream)));
-    LS_CUDA(cudaStreamSynchronize(ls::as_stream(stream)));
+    LS_SYNC(ls::as_stream(stream));
     return LS_OK;
 }
 
 int ls_synchronize(void* stream) {
-    LS_CUDA(cudaStreamSynchronize(ls::as_stream(stream)));
+    LS_SYNC(ls::as_stream(stream));
     return LS_OK;
 }
 

@@ -35,6 +35,35 @@ def _f64(a, order="F"):
     return np.require(np.asarray(a, dtype=np.float64), requirements=[order, "A"])
 
 
+def _check_host_out(out, shape, what):
+    """A caller-supplied host grid goes to native code as a raw pointer: it must be exactly the
+    Fortran-ordered float64 (n1, n2, k1 - k0) block the call writes."""
+    shape = tuple(int(x) for x in shape)
+    if not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.shape != shape \
+            or not out.flags["F_CONTIGUOUS"] or not out.flags["WRITEABLE"]:
+        got = (getattr(out, "shape", None), getattr(out, "dtype", None))
+        raise ValidationError(f"{what}: out must be a writeable Fortran-ordered float64 array of shape {shape}, "
+                              f"got shape/dtype {got}")
+
+
+def _check_lengths(vecs, dims, what):
+    if len(vecs) != 3:
+        raise ValidationError(f"{what}: need three density factors")
+    for l in range(3):
+        if vecs[l].shape[0] != dims[l]:
+            raise ValidationError(f"{what}: density factor {l} has length {vecs[l].shape[0]}, grid axis has {dims[l]}")
+
+
+def _check_device_tensor(x, shape, dev, what):
+    """A caller-supplied device tensor: float64, contiguous, on the pipeline's device, exact shape."""
+    import torch
+    shape = tuple(int(v) for v in shape)
+    if not isinstance(x, torch.Tensor) or x.dtype != torch.float64 or tuple(x.shape) != shape \
+            or not x.is_contiguous() or x.device != dev:
+        got = (tuple(getattr(x, "shape", ())), getattr(x, "dtype", None), getattr(x, "device", None))
+        raise ValidationError(f"{what}: need a contiguous float64 tensor of shape {shape} on {dev}, got {got}")
+
+
 # --------------------------------------------------------------------- grid.hpp
 @dataclass(frozen=True)
 class GridSpec:
@@ -146,9 +175,11 @@ def densify(t: CanonicalTensor3, guard: int = DEFAULT_DENSIFY_GUARD) -> np.ndarr
 def expand_slabs(t: CanonicalTensor3, k0: int, k1: int, out: np.ndarray | None = None) -> np.ndarray:
     """densify_slab over slabs [k0, k1) (canonical.hpp:241-246) into host memory (no guard)."""
     d = t.dims()
+    if not (0 <= k0 <= k1 <= d[2]):
+        raise ValidationError("expand: slab range outside [0, N3]")
     if out is None:
         out = np.empty((d[0], d[1], k1 - k0), order="F")
-    assert out.flags["F_CONTIGUOUS"] and out.dtype == np.float64
+    _check_host_out(out, (d[0], d[1], k1 - k0), "expand_slabs")
     call("ls_h_expand", _p(_dims_arr(t)), t.rank(), _p(t.factor(0)), _p(t.factor(1)), _p(t.factor(2)),
          _p(t.weights()), k0, k1, _p(out))
     return out
@@ -181,6 +212,7 @@ def grid_functional(t: CanonicalTensor3, rho: Sequence[np.ndarray], k0: int = 0,
     """Full-grid sum_{ijk} V(i,j,k) rho1(i) rho2(j) rho3(k) over slabs [k0, k1), V never stored."""
     k1 = t.dim(2) if k1 is None else k1
     r = [_f64(x).ravel() for x in rho]
+    _check_lengths(r, t.dims(), "grid_functional")
     out = np.zeros(1)
     call("ls_h_grid_functional", _p(_dims_arr(t)), t.rank(), _p(t.factor(0)), _p(t.factor(1)), _p(t.factor(2)),
          _p(t.weights()), _p(r[0]), _p(r[1]), _p(r[2]), k0, k1, _p(out))
@@ -444,8 +476,11 @@ def lattice_potential(spec: LatticeSpec, rule: QuadratureRule, mode: str = "erf"
     n = spec.unit.n
     dims = (n, n, n) if periodic else spec.target_dims()
     k1 = dims[2] if k1 is None else k1
+    if not (0 <= k0 <= k1 <= dims[2]):
+        raise ValidationError("lattice_potential: slab range outside [0, N3]")
     if out is None:
         out = np.empty((dims[0], dims[1], k1 - k0), order="F")
+    _check_host_out(out, (dims[0], dims[1], k1 - k0), "lattice_potential")
     M0, R = spec.charge_count(), rule.node_count()
     ch = np.array([[*c.pos, c.Z] for c in spec.charges], dtype=np.float64)
     L = np.array(spec.L, dtype=np.int64)
@@ -562,6 +597,7 @@ class DevicePipeline:
         self.torch = torch
         self.spec, self.rule, self.mode, self.periodic = spec, rule, mode, periodic
         self.dev = torch.device("cuda") if device is None else torch.device(device)
+        self._devc = torch.device("cuda", self.dev.index if self.dev.index is not None else torch.cuda.current_device())
         self._lib = _abi.load()
         L = np.array(spec.L, dtype=np.int64)
         ch = np.array([[*c.pos, c.Z] for c in spec.charges], dtype=np.float64)
@@ -607,14 +643,21 @@ class DevicePipeline:
     def assemble(self, stream=None):
         call("ls_pipeline_assemble", self._h, self._stream(stream))
 
+    def _check_out(self, out, k0, k1):
+        if not (0 <= k0 <= k1 <= self.dims[2]):
+            raise ValidationError("expand: slab range outside [0, N3]")
+        _check_device_tensor(out, (k1 - k0, self.dims[1], self.dims[0]), self._devc, "expand")
+
     def expand(self, out, k0=0, k1=None, stream=None):
         """Writes slabs [k0, k1) into `out` (a contiguous (k1-k0, N2, N1) float64 tensor)."""
         k1 = self.dims[2] if k1 is None else k1
+        self._check_out(out, k0, k1)
         call("ls_pipeline_expand", self._h, k0, k1, self._ptr(out), self._stream(stream))
 
     def step(self, out, k0=0, k1=None, stream=None):
         """One pass of the hot path: generate, assemble, expand into `out`."""
         k1 = self.dims[2] if k1 is None else k1
+        self._check_out(out, k0, k1)
         call("ls_pipeline_step", self._h, k0, k1, self._ptr(out), self._stream(stream))
 
     def partial_count(self, k0=0, k1=None):
@@ -625,8 +668,14 @@ class DevicePipeline:
         """sum V*rho over slabs [k0, k1) fused into the expansion (V not stored); returns a
         1-element device tensor."""
         k1 = self.dims[2] if k1 is None else k1
-        out = self.torch.zeros(1, dtype=self.torch.float64, device=self.dev)
+        if not (0 <= k0 <= k1 <= self.dims[2]):
+            raise ValidationError("grid_functional: slab range outside [0, N3]")
         r = [x.contiguous() for x in rho]
+        for l in range(3):
+            _check_device_tensor(r[l], (self.dims[l],), self._devc, f"grid_functional: density factor {l}")
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.dev)
+        with self.torch.cuda.stream(s):
+            out = self.torch.zeros(1, dtype=self.torch.float64, device=self.dev)
         call("ls_pipeline_energy", self._h, self._ptr(r[0]), self._ptr(r[1]), self._ptr(r[2]), k0, k1,
              self._ptr(out), self._stream(stream))
         return out
@@ -662,14 +711,21 @@ class DevicePipeline:
 
     @staticmethod
     def functional_batch_device(factors, w, rho, scale=1.0, stream=None):
-        """scale * scalar_product(P, rho_f) for every column f of rho = (X, Y, Z) (device tensors,
-        X is (n1, F) column-major i.e. a (F, n1) row-major tensor or a Fortran-ordered view)."""
+        """scale * scalar_product(P, rho_f) for every column f of rho = (X, Y, Z).
+
+        Every matrix is given in its logical (Eigen) shape, whatever its memory layout:
+        factors[l] is (n_l, R) (e.g. ``pipe.factor(l).T``), rho[l] is (n_l, F); the rank-major
+        and density-major buffers the kernel reads are built here with ``.T.contiguous()``."""
         import torch
         X, Y, Z = rho
-        F = X.shape[1]
-        Xt, Yt, Zt = (r.T.contiguous() for r in (X, Y, Z))  # (F, n) rows = columns
-        ft = [f.T.contiguous() if f.shape[0] != w.shape[0] else f for f in factors]  # (R, n)
         R = w.shape[0]
+        F = X.shape[1]
+        if len(factors) != 3 or any(f.dim() != 2 or f.shape[1] != R for f in factors):
+            raise ValidationError(f"functional_batch: factors must be three (n_l, R={R}) matrices")
+        if any(r.dim() != 2 or r.shape[1] != F or r.shape[0] != f.shape[0] for r, f in zip(rho, factors)):
+            raise ValidationError("functional_batch: rho[l] must be (n_l, F) with the factor's n_l")
+        Xt, Yt, Zt = (r.T.contiguous() for r in (X, Y, Z))  # (F, n) rows = columns
+        ft = [f.T.contiguous() for f in factors]  # (R, n) rows = rank columns
         n = [ft[l].shape[1] for l in range(3)]
         out = torch.zeros(F, dtype=torch.float64, device=w.device)
         s = stream if stream is not None else torch.cuda.current_stream(w.device)

@@ -411,6 +411,18 @@ TEST(StreamingDiff, MatchesDenseDifference) {  // test_canonical.cpp:276-285
     EXPECT_NEAR(d.max_abs_b, max_abs(db), 1e-13);
 }
 
+TEST(StreamingDiff, ZeroRankSideExpandsToZero) {  // canonical.hpp:282-301 with a rank-0 tensor
+    std::mt19937 gen(62);
+    CanonicalTensor3 b = random_tensor(gen, {9, 8, 7}, 3), z(Dims3{9, 8, 7});
+    DenseTensor3 db = scalar_oracle(b);
+    StreamDiff d = max_norm_diff_canonical(z, b);
+    EXPECT_NEAR(d.max_diff, max_abs(db), 1e-13);
+    EXPECT_NEAR(d.max_abs_b, max_abs(db), 1e-13);
+    StreamDiff e = max_norm_diff_canonical(b, z);
+    EXPECT_NEAR(e.max_diff, max_abs(db), 1e-13);
+    EXPECT_EQ(e.max_abs_b, 0.0);
+}
+
 // ------------------------------------------------------------------ lattice (GPU assembly)
 TEST(Window, ValidatesBoundsAndExtracts) {  // test_lattice.cpp:62-82
     EXPECT_NO_THROW(WindowOp(4, 8, 4));

@@ -138,7 +138,7 @@ def cfg2(emit):
     t_e = ev_time(lambda: holder.__setitem__("e", pipe.grid_functional(rho)), reps=2, warm=1)
     X = [r1.reshape(-1, 1)] * 3
     t_1d = ev_time(lambda: holder.__setitem__("e1", L.DevicePipeline.functional_batch_device(
-        [pipe.factor(l) for l in range(3)], pipe.w, X)))
+        [pipe.factor(l).T for l in range(3)], pipe.w, X)))
     e, e1 = float(holder["e"][0]), float(holder["e1"][0])
     line.update({"energy_full_grid": e, "energy_1d": e1, "energy_rel_diff": abs(e - e1) / abs(e1),
                  "energy_full_grid_ms": t_e, "energy_1d_ms": t_1d})
@@ -183,7 +183,7 @@ def cfg4(emit):
              for l in range(3)]
         holder = {}
         t_b = ev_time(lambda: holder.__setitem__("v", L.DevicePipeline.functional_batch_device(
-            [pipe.factor(l) for l in range(3)], pipe.w, G)))
+            [pipe.factor(l).T for l in range(3)], pipe.w, G)))
         # full-grid form for a sample of 16 test functions (fused expansion-reduction each)
         t_f = ev_time(lambda: [pipe.grid_functional([G[0][:, f].contiguous(), G[1][:, f].contiguous(),
                                                       G[2][:, f].contiguous()]) for f in range(16)], reps=2, warm=1)

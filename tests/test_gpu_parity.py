@@ -371,7 +371,7 @@ def test_cfg3_multi_atom_rank_328(L, orc):
     assert rel(out[0].cpu().numpy().T, want[:, :, 0]) <= 1e-12
 
 
-@pytest.mark.parametrize("Lc", [64, 256])
+@pytest.mark.parametrize("Lc", [64, 128, 256])
 def test_cfg4_periodic_and_functional_batch(L, orc, Lc):
     import torch
     spec, rule = cfg(L, Lc, n=256)
@@ -467,7 +467,7 @@ def test_cfg4_grid_functional_batch_matches_1d_form(L):
     G = [torch.as_tensor(np.exp(-(mids[:, None] - centres[None, :, l]) ** 2 / (2 * sigma ** 2)), device="cuda")
          for l in range(3)]
     full = pipe.grid_functional_batch(G).cpu().numpy()
-    one_d = L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w, G).cpu().numpy()
+    one_d = L.DevicePipeline.functional_batch_device([pipe.factor(l).T for l in range(3)], pipe.w, G).cpu().numpy()
     assert np.max(np.abs(full - one_d) / np.abs(one_d)) <= 1e-12
     again = pipe.grid_functional_batch(G).cpu().numpy()
     assert np.array_equal(full, again)  # fixed-order reductions: bitwise run to run
@@ -491,7 +491,7 @@ def test_fused_energy_matches_1d_form_multi_charge(L, charges, periodic):
         x = (np.arange(N[l]) + 0.5 - N[l] / 2) * spec.unit.h
         rho.append(torch.as_tensor(np.exp(-x * x / (2.0 + l)), device="cuda"))
     e = float(pipe.grid_functional(rho).cpu())
-    one_d = L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w,
+    one_d = L.DevicePipeline.functional_batch_device([pipe.factor(l).T for l in range(3)], pipe.w,
                                                     [r.reshape(-1, 1) for r in rho]).cpu().numpy()[0]
     assert abs(e - one_d) <= 1e-12 * abs(one_d)
     # and the stored grid contracted on the host agrees
@@ -635,7 +635,7 @@ def test_cfg2_sharded_energy_matches_whole(L):
     parts = [float(pipe.grid_functional(rho, *slab_range(N[2], r, 8))[0]) for r in range(8)]
     assert abs(sum(parts) - whole) <= 1e-13 * abs(whole)
     X = [r1.reshape(-1, 1)] * 3
-    one_d = float(L.DevicePipeline.functional_batch_device([pipe.factor(l) for l in range(3)], pipe.w, X)[0])
+    one_d = float(L.DevicePipeline.functional_batch_device([pipe.factor(l).T for l in range(3)], pipe.w, X)[0])
     assert abs(whole - one_d) <= 1e-12 * abs(one_d)
 
 
@@ -682,3 +682,76 @@ def test_calibration_matches_reference(L, ref):
     c0 = C.c_double(0)
     M = ref.lib.ref_calibrate_for_lattice(Lx.ctypes.data_as(C.POINTER(C.c_int64)), 8, 2.0, 1e-4, C.byref(c0))
     assert (rule.M, rule.C0) == (M, c0.value)
+
+
+# ------------------------------------------------------------ large ranks / caller buffers
+@pytest.mark.parametrize("R,F", [(2200, 600), (9000, 40), (3, 700)])
+def test_functional_batch_any_rank(L, orc, R, F):
+    """functional_batch beyond the shared-memory Gram kernels: F >= 4 * SMs with R > 2133 used
+    to be refused; now the 4-density kernel falls back to the single one, and
+    ranks beyond that take the global-scratch Gram path, with the same rank-ordered sum."""
+    rng = np.random.default_rng(R + F)
+    dims = (12, 10, 9)
+    fac = [np.asfortranarray(rng.uniform(0.1, 1.0, (dims[l], R))) for l in range(3)]
+    w = rng.uniform(0.5, 1.5, R)
+    G = [np.asfortranarray(rng.uniform(0.1, 1.0, (dims[l], F))) for l in range(3)]
+    got = L.functional_batch(L.CanonicalTensor3(fac, w, trusted=True), G)
+    for f in rng.integers(0, F, 6):
+        want = orc.scalar_product(fac, w, [np.asfortranarray(G[l][:, [f]]) for l in range(3)], np.ones(1))
+        assert abs(got[f] - want) <= 1e-12 * abs(want), (R, F, f)
+
+
+def test_functional_batch_paths_agree_bitwise(L):
+    """The same density through the 4-density kernel (large batch) and the single-density
+    kernel (small batch) gives bit-identical results."""
+    rng = np.random.default_rng(5)
+    dims = (16, 8, 8)
+    R = 100
+    fac = [np.asfortranarray(rng.uniform(0.1, 1.0, (dims[l], R))) for l in range(3)]
+    w = rng.uniform(0.5, 1.5, R)
+    t = L.CanonicalTensor3(fac, w, trusted=True)
+    G = [np.asfortranarray(rng.uniform(0.1, 1.0, (dims[l], 700))) for l in range(3)]
+    big = L.functional_batch(t, G)      # F >= 4 * SMs: four densities per block
+    small = L.functional_batch(t, [np.asfortranarray(g[:, :3]) for g in G])
+    assert np.array_equal(big[:3], small)
+
+
+def test_caller_buffers_are_validated(L):
+    import torch
+    spec, rule = cfg(L, 2, n=8)
+    pipe = L.DevicePipeline(spec, rule)
+    N = pipe.dims
+    with pytest.raises(L.ValidationError):
+        pipe.expand(torch.empty((N[2], N[1], N[0] - 1), dtype=torch.float64, device="cuda"))
+    with pytest.raises(L.ValidationError):
+        pipe.expand(torch.empty((N[2], N[1], N[0]), dtype=torch.float32, device="cuda"))
+    with pytest.raises(L.ValidationError):
+        pipe.step(torch.empty((N[0], N[1], N[2]), dtype=torch.float64, device="cuda").transpose(0, 2))
+    with pytest.raises(L.ValidationError):
+        pipe.grid_functional([torch.ones(N[0] + 1, dtype=torch.float64, device="cuda")] * 3)
+    with pytest.raises(L.ValidationError):
+        L.lattice_potential(spec, rule, out=np.empty((N[0], N[1], N[2])))  # C order
+    with pytest.raises(L.ValidationError):
+        L.lattice_potential(spec, rule, out=np.empty((N[0], N[1], N[2] - 1), order="F"))
+    t = L.CanonicalTensor3([np.ones((N[l], 1)) for l in range(3)], np.ones(1))
+    with pytest.raises(L.ValidationError):
+        L.grid_functional(t, [np.ones(N[0]), np.ones(N[1]), np.ones(N[2] - 1)])
+    with pytest.raises(L.ValidationError):
+        L.expand_slabs(t, 0, 2, out=np.empty((N[0], N[1], 3), order="F"))
+    # square factors (n_l == R) keep their meaning: no shape-based transposition
+    R = 6
+    rng = np.random.default_rng(9)
+    fac = [np.asfortranarray(rng.uniform(0.1, 1.0, (R, R))) for _ in range(3)]
+    w = rng.uniform(0.5, 1.5, R)
+    X = [np.asfortranarray(rng.uniform(0.1, 1.0, (R, 2))) for _ in range(3)]
+    got = L.functional_batch(L.CanonicalTensor3(fac, w, trusted=True), X)
+    want = np.einsum("q,iq,jq,kq,i,j,k->", w, *fac, X[0][:, 0], X[1][:, 0], X[2][:, 0])
+    assert abs(got[0] - want) <= 1e-13 * abs(want)
+
+
+def test_watchdog_clear_and_product_build(L):
+    lib = L._abi.load()
+    assert lib.ls_dev_knobs_enabled() == 0
+    spec, rule = cfg(L, 2, n=8)
+    L.lattice_potential(spec, rule)
+    assert lib.ls_fault_status(0) == 0

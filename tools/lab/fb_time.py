@@ -10,5 +10,5 @@ p4.generate(); p4.assemble()
 rng = np.random.default_rng(4)
 G = [torch.as_tensor(rng.uniform(size=(256, 1024)), device=dev) for _ in range(3)]
 for _ in range(5):
-    L.DevicePipeline.functional_batch_device([p4.factor(l) for l in range(3)], p4.w, G)
+    L.DevicePipeline.functional_batch_device([p4.factor(l).T for l in range(3)], p4.w, G)
 torch.cuda.synchronize()

@@ -32,7 +32,7 @@ rule4 = L.sinc_quadrature(1e-6, spec4.unit.h, math.sqrt(3.0) * 256 * B, 20, 1.0)
 p4 = L.DevicePipeline(spec4, rule4, mode="erf", periodic=True, device=dev)
 rng = np.random.default_rng(4)
 G = [torch.as_tensor(rng.uniform(size=(256, 1024)), device=dev) for _ in range(3)]
-fb = lambda: L.DevicePipeline.functional_batch_device([p4.factor(l) for l in range(3)], p4.w, G)  # noqa: E731
+fb = lambda: L.DevicePipeline.functional_batch_device([p4.factor(l).T for l in range(3)], p4.w, G)  # noqa: E731
 p4.generate(); p4.assemble()
 want = fb().clone()
 for name, fn in [("cfg4 gen+asm", lambda: (p4.generate(), p4.assemble())), ("functionals 1D", fb),

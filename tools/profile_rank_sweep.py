@@ -1,7 +1,8 @@
 """Times ls_expand over a rank sweep on random factors (plan selection study).
 
   python tools/profile_rank_sweep.py [--n 1024] [--slabs 64] [--ranks 60,82,164,328]
-Set LS_EXPAND_PLAN / LS_EXPAND_KC in the environment to force a plan.
+Set LS_EXPAND_PLAN / LS_EXPAND_KC in the environment to force a plan (needs the dev build:
+`python -m paper_1405_2270_b200.build --dev`; the product library ignores them).
 """
 import argparse
 import os
