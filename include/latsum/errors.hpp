@@ -38,6 +38,15 @@ inline void check(int status, const char* call) {
     if (status == LS_EGUARD) throw resource_guard_error(msg);
     throw device_error(msg);
 }
+// Same, with the library's message alone: the host validation entry points
+// (ls_validate_*) already word it exactly like the reference's exceptions.
+inline void check_bare(int status) {
+    if (status == LS_OK) return;
+    const std::string msg = ls_last_error();
+    if (status == LS_EVALIDATION) throw validation_error(msg);
+    if (status == LS_EGUARD) throw resource_guard_error(msg);
+    throw device_error(msg);
+}
 }  // namespace cuda
 
 }  // namespace latsum

@@ -65,6 +65,17 @@ int64_t ls_launch_count(void);
 int ls_sinc_quadrature(double eps, double a_min, double a_max, int M, double C0, double* nodes_h,
                        double* exponents_h, double* weights_h, double* step);
 
+/* ---- host-side validation (no device work) -------------------------------
+ * The single implementation of GridSpec::validate (grid.hpp:21-27), LatticeSpec::validate
+ * and charge_grid_index (lattice.hpp:33-68), with the reference's messages; the drop-in
+ * headers, the host-level calls, the pipeline and the Python mirror all call these.
+ * charges_h is M0 x {x, y, z, Z} row-major; ia_out (optional) receives the vertex index of
+ * charge nu on axis l at [l * M0 + nu]. */
+int ls_validate_grid(double b, int64_t n);
+int ls_charge_grid_index(double b, int64_t n, double p, int axis, int nu, int64_t* out);
+int ls_validate_lattice(const int64_t L[3], int64_t n, double b, const double* charges_h, int M0,
+                        int64_t* ia_out);
+
 /* ---- K1: rank-R Newton-kernel generator --------------------------------
  * Replaces the column loop of build_newton_master (newton.hpp:57-75) with
  * gaussian_sample_vector (mode LS_GEN_MIDPOINT, newton.hpp:43-52) or

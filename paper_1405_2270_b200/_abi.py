@@ -43,6 +43,9 @@ SIGNATURES = {
     "ls_gen_master": (_i, [_i, _vp, _i, _i64, _d, _vp, _i64, _vp]),
     "ls_libm_eval": (_i, [_i, _vp, _vp, _i64, _vp]),
     "ls_fault_status": (_i, [_i]),
+    "ls_validate_grid": (_i, [_d, _i64]),
+    "ls_charge_grid_index": (_i, [_d, _i64, _d, _i, _i, _vp]),
+    "ls_validate_lattice": (_i, [_vp, _i64, _d, _vp, _i, _vp]),
     "ls_dev_knobs_enabled": (_i, []),
     "ls_assemble_axis": (_i, [_vp, _i64, _i, _i, _vp, _i64, _i64, _i, _vp, _i64, _vp]),
     "ls_expand": (_i, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i, _i64, _i64, _vp, _i64, _i64,

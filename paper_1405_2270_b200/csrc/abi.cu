@@ -139,17 +139,6 @@ int upload(DevBuf& b, const void* host, size_t bytes, cudaStream_t s) {
     return LS_OK;
 }
 
-// lattice.hpp:57-68: grid-point index of coordinate p on the unit cell (b, n).
-int charge_grid_index(double b, int64_t n, double p, int64_t& out) {
-    const double h = b / static_cast<double>(n);
-    const double x = (p + b / 2.0) / h;
-    const double r = std::round(x);
-    if (std::abs(x - r) > 1e-9 * static_cast<double>(n) || r < 0.0 || r > static_cast<double>(n))
-        return fail(LS_EVALIDATION, "lattice: charge coordinate " + std::to_string(p) +
-                                        " does not lie on a grid point of the unit cell");
-    out = static_cast<int64_t>(r);
-    return LS_OK;
-}
 
 // Expands slabs [k0, k1) of a device-resident tensor into host memory: the
 // compute stream fills chunk buffers, the copy stream drains them, and two
@@ -209,6 +198,49 @@ extern "C" {
 int ls_abi_version(void) { return 1; }
 
 const char* ls_last_error(void) { return ls::last_error().c_str(); }
+
+// grid.hpp:21-27 (GridSpec::validate) and lattice.hpp:33-68 (LatticeSpec::validate,
+// charge_grid_index): the one host implementation of these checks, with the reference's
+// messages, called by the drop-in headers, the host-level calls, the pipeline and the
+// Python mirror.
+int ls_charge_grid_index(double b, int64_t n, double p, int axis, int nu, int64_t* out) {
+    const double h = b / static_cast<double>(n);
+    const double x = (p + b / 2.0) / h;
+    const double rounded = std::round(x);
+    if (std::abs(x - rounded) > 1e-9 * static_cast<double>(n) || rounded < 0.0 ||
+        rounded > static_cast<double>(n))
+        return ls::fail(LS_EVALIDATION, "lattice: charge " + std::to_string(nu) + " coordinate " + std::to_string(p) +
+                                            " on axis " + std::to_string(axis) +
+                                            " does not lie on a grid point of the unit cell");
+    if (out) *out = static_cast<int64_t>(rounded);
+    return LS_OK;
+}
+
+int ls_validate_grid(double b, int64_t n) {
+    if (!(b > 0.0) || !std::isfinite(b))
+        return ls::fail(LS_EVALIDATION, "grid: box edge must be positive, got " + std::to_string(b));
+    if (n < 2 || n % 2 != 0)
+        return ls::fail(LS_EVALIDATION, "grid: n must be even and at least 2, got " + std::to_string(n));
+    return LS_OK;
+}
+
+int ls_validate_lattice(const int64_t L[3], int64_t n, double b, const double* charges_h, int M0, int64_t* ia_out) {
+    if (const int rc = ls_validate_grid(b, n)) return rc;
+    for (int l = 0; l < 3; ++l)
+        if (L[l] < 1) return ls::fail(LS_EVALIDATION, "lattice: cell count on axis " + std::to_string(l) + " must be >= 1");
+    if (M0 < 1) return ls::fail(LS_EVALIDATION, "lattice: at least one charge required");
+    for (int nu = 0; nu < M0; ++nu) {
+        const double Z = charges_h[4 * nu + 3];
+        if (!(Z > 0.0) || !std::isfinite(Z))
+            return ls::fail(LS_EVALIDATION, "lattice: charge " + std::to_string(nu) + " must have positive finite Z");
+        for (int l = 0; l < 3; ++l) {
+            int64_t i = 0;
+            if (const int rc = ls_charge_grid_index(b, n, charges_h[4 * nu + l], l, nu, &i)) return rc;
+            if (ia_out) ia_out[static_cast<size_t>(l) * M0 + nu] = i;
+        }
+    }
+    return LS_OK;
+}
 
 int ls_fault_status(int reset) {
     unsigned* f = ls::fault_flag();
@@ -641,23 +673,14 @@ int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, co
                            const double* w_h, int R, const double* charges_h, int M0, int periodic,
                            int64_t k0, int64_t k1, double* grid_h, double* f0_h, double* f1_h,
                            double* f2_h, double* wout_h) {
-    if (n < 2 || n % 2 != 0 || !(b > 0.0) || !std::isfinite(b))
-        return ls::fail(LS_EVALIDATION, "grid: need b > 0 and even n >= 2");
-    if (M0 < 1) return ls::fail(LS_EVALIDATION, "lattice: at least one charge required");
+    // LatticeSpec::validate + charge snapping (lattice.hpp:33-68), then weights Z_nu * w_q
+    // (lattice.hpp:284-287), on the host.
+    std::vector<int64_t> ia(static_cast<size_t>(3 * std::max(M0, 0)));
+    LS_TRY(ls_validate_lattice(L, n, b, charges_h, M0, ia.data()));
     if (R < 1) return ls::fail(LS_EVALIDATION, "lattice: master tensor has rank 0");
-    for (int l = 0; l < 3; ++l)
-        if (L[l] < 1) return ls::fail(LS_EVALIDATION, "lattice: cell counts must be >= 1");
-    // Charge snapping and weights Z_nu * w_q (lattice.hpp:57-68, :284-287) on the host.
-    std::vector<int64_t> ia(static_cast<size_t>(3 * M0));
     std::vector<double> wt(static_cast<size_t>(M0) * R);
-    for (int nu = 0; nu < M0; ++nu) {
-        const double Z = charges_h[4 * nu + 3];
-        if (!(Z > 0.0) || !std::isfinite(Z))
-            return ls::fail(LS_EVALIDATION, "lattice: charge must have positive finite Z");
-        for (int l = 0; l < 3; ++l)
-            LS_TRY(ls::charge_grid_index(b, n, charges_h[4 * nu + l], ia[static_cast<size_t>(l * M0 + nu)]));
-        for (int q = 0; q < R; ++q) wt[static_cast<size_t>(nu) * R + q] = Z * w_h[q];
-    }
+    for (int nu = 0; nu < M0; ++nu)
+        for (int q = 0; q < R; ++q) wt[static_cast<size_t>(nu) * R + q] = charges_h[4 * nu + 3] * w_h[q];
     Streams* st;
     LS_TRY(ls::get_streams(st));
     const cudaStream_t s = st->compute;

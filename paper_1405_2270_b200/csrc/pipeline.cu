@@ -35,17 +35,6 @@ struct ls_pipeline {
 
 namespace {
 
-int charge_index(double b, int64_t n, double p, int64_t& out) {
-    const double h = b / static_cast<double>(n);
-    const double x = (p + b / 2.0) / h;
-    const double r = std::round(x);
-    if (std::abs(x - r) > 1e-9 * static_cast<double>(n) || r < 0.0 || r > static_cast<double>(n))
-        return ls::fail(LS_EVALIDATION, "lattice: charge coordinate " + std::to_string(p) +
-                                            " does not lie on a grid point of the unit cell");
-    out = static_cast<int64_t>(r);
-    return LS_OK;
-}
-
 void release(ls_pipeline* p) {
     if (!p) return;
     cudaFree(p->tau);
@@ -69,27 +58,16 @@ int ls_pipeline_create(int mode, const int64_t L[3], int64_t n, double b, const 
                        int R, const double* charges_h, int M0, int periodic, ls_pipeline** out) {
     *out = nullptr;
     if (mode != LS_GEN_MIDPOINT && mode != LS_GEN_ERF) return ls::fail(LS_EVALIDATION, "pipeline: unknown mode");
-    if (n < 2 || n % 2 != 0 || !(b > 0.0) || !std::isfinite(b))
-        return ls::fail(LS_EVALIDATION, "grid: need b > 0 and even n >= 2");
-    if (M0 < 1) return ls::fail(LS_EVALIDATION, "lattice: at least one charge required");
+    std::vector<int64_t> ia(static_cast<size_t>(3 * std::max(M0, 0)));
+    if (const int rc = ls_validate_lattice(L, n, b, charges_h, M0, ia.data())) return rc;
     if (R < 1) return ls::fail(LS_EVALIDATION, "lattice: master tensor has rank 0");
-    for (int l = 0; l < 3; ++l)
-        if (L[l] < 1) return ls::fail(LS_EVALIDATION, "lattice: cell counts must be >= 1");
     for (int q = 0; q < R; ++q)
         if (!(tau_h[q] >= 0.0) || !std::isfinite(tau_h[q]))
             return ls::fail(LS_EVALIDATION, "generator: exponents must be finite and >= 0");
-    std::vector<int64_t> ia(static_cast<size_t>(3 * M0));
     std::vector<double> wt(static_cast<size_t>(M0) * R);
-    for (int nu = 0; nu < M0; ++nu) {
-        const double Z = charges_h[4 * nu + 3];
-        if (!(Z > 0.0) || !std::isfinite(Z))
-            return ls::fail(LS_EVALIDATION, "lattice: charge must have positive finite Z");
-        for (int l = 0; l < 3; ++l) {
-            const int rc = charge_index(b, n, charges_h[4 * nu + l], ia[static_cast<size_t>(l * M0 + nu)]);
-            if (rc) return rc;
-        }
-        for (int q = 0; q < R; ++q) wt[static_cast<size_t>(nu) * R + q] = Z * w_h[q];  // lattice.hpp:284-287
-    }
+    for (int nu = 0; nu < M0; ++nu)
+        for (int q = 0; q < R; ++q)
+            wt[static_cast<size_t>(nu) * R + q] = charges_h[4 * nu + 3] * w_h[q];  // lattice.hpp:284-287
     int device = 0;
     LS_CUDA(cudaGetDevice(&device));
     ls_pipeline* p = new ls_pipeline;

@@ -72,10 +72,8 @@ class GridSpec:
     n: int
 
     def __post_init__(self):
-        if not (self.b > 0.0) or not math.isfinite(self.b):
-            raise ValidationError(f"grid: box edge must be positive, got {self.b}")
-        if self.n < 2 or self.n % 2 != 0:
-            raise ValidationError(f"grid: n must be even and at least 2, got {self.n}")
+        # grid.hpp:21-27 through the library's one implementation (ls_validate_grid)
+        _abi.check(_abi.load().ls_validate_grid(float(self.b), int(self.n)))
 
     @property
     def h(self) -> float:
@@ -344,16 +342,11 @@ class LatticeSpec:
     charges: list[Charge] = field(default_factory=list)
 
     def validate(self) -> None:
-        for l in range(3):
-            if self.L[l] < 1:
-                raise ValidationError(f"lattice: cell count on axis {l} must be >= 1")
-        if not self.charges:
-            raise ValidationError("lattice: at least one charge required")
-        for nu, c in enumerate(self.charges):
-            if not (c.Z > 0.0) or not math.isfinite(c.Z):
-                raise ValidationError(f"lattice: charge {nu} must have positive finite Z")
-            for l in range(3):
-                self.charge_grid_index(l, nu)
+        """lattice.hpp:33-45 through the library's one implementation (ls_validate_lattice)."""
+        L = np.array(self.L, dtype=np.int64)
+        ch = np.array([[*c.pos, c.Z] for c in self.charges], dtype=np.float64).reshape(-1, 4)
+        _abi.check(_abi.load().ls_validate_lattice(_p(L), int(self.unit.n), float(self.unit.b), _p(ch),
+                                                   len(self.charges), None))
 
     def target_cells(self, axis: int) -> int:
         return self.L[axis] * self.unit.n
@@ -368,14 +361,12 @@ class LatticeSpec:
         return self.L[0] * self.L[1] * self.L[2]
 
     def charge_grid_index(self, axis: int, nu: int) -> int:
-        h = self.unit.h
-        p = self.charges[nu].pos[axis]
-        x = (p + self.unit.b / 2.0) / h
-        r = float(np.round(x))  # half-away vs half-even only differs off-grid (rejected below)
-        if abs(x - r) > 1e-9 * self.unit.n or r < 0.0 or r > self.unit.n:
-            raise ValidationError(f"lattice: charge {nu} coordinate {p} on axis {axis} does not lie on a grid "
-                                  "point of the unit cell")
-        return int(r)
+        """lattice.hpp:57-68 (ls_charge_grid_index): off-grid positions are rejected."""
+        out = C.c_int64(0)
+        _abi.check(_abi.load().ls_charge_grid_index(float(self.unit.b), int(self.unit.n),
+                                                    float(self.charges[nu].pos[axis]), int(axis), int(nu),
+                                                    C.byref(out)))
+        return int(out.value)
 
 
 def calibrate_for_lattice(spec: "LatticeSpec", eps: float, trace: list | None = None) -> QuadratureRule:
