@@ -57,6 +57,8 @@ public:
 
     Dims3 dims() const { return dims_; }
     Index rank() const { return rank_; }
+    // The native pipeline object, for C-ABI calls that take it (e.g. ls_pipeline_energy_allreduce).
+    ls_pipeline* handle() const { return h_; }
 
     // Stages on `stream` (a cudaStream_t; nullptr = default stream), asynchronous.
     void generate(void* stream = nullptr) { cuda::check(ls_pipeline_generate(h_, stream), "generate"); }

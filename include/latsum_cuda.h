@@ -55,6 +55,10 @@ int ls_fault_status(int reset);
 /* 1 if this build reads the development A/B knobs (LS_EXPAND_PLAN, LS_EXPAND_DEBUG, ...) from
  * the environment (-DLS_DEV_KNOBS); the product build returns 0 and ignores them. */
 int ls_dev_knobs_enabled(void);
+/* Host threads the host-level calls use to move grid data out of their bounded pinned
+ * staging ring into a pageable destination (0 = min(8, hardware threads)). One process per
+ * GPU on a shared host: give each rank its share of the cores. */
+int ls_set_host_threads(int n);
 /* Number of kernel launches this library issued since load (all threads). */
 int64_t ls_launch_count(void);
 
@@ -212,6 +216,28 @@ int ls_pipeline_step(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void
 /* out_d[0] = sum over slabs [k0,k1) of V * rho1(i) rho2(j) rho3(k) (fused, V never stored). */
 int ls_pipeline_energy(ls_pipeline* p, const double* r1_d, const double* r2_d, const double* r3_d, int64_t k0,
                        int64_t k1, double* out_d, void* stream);
+
+/* ---- multi-GPU: the scalar all-reduce of the sharded path ------
+ * One process per GPU; each owns a contiguous z-slab range of the grid (the reference's
+ * k-slab parallel_for, canonical.hpp:251-266, spread over GPUs) and recomputes the
+ * generator and assembly, so the only collective is the all-reduce of functional partials.
+ * Rank 0 creates an id with ls_comm_unique_id and the caller hands its LS_COMM_ID_BYTES
+ * bytes to every rank (file, socket, MPI ...); each rank then calls ls_comm_init on its own
+ * device. NCCL (libnccl.so.2) is loaded with dlopen on first use. */
+#define LS_COMM_ID_BYTES 128
+#define LS_REDUCE_SUM 0
+#define LS_REDUCE_MAX 1
+typedef struct ls_comm ls_comm;
+int ls_comm_unique_id(void* id_out, int bytes);
+int ls_comm_init(int world, int rank, const void* id, int bytes, ls_comm** out);
+int ls_comm_destroy(ls_comm* c);
+int ls_comm_info(const ls_comm* c, int* world, int* rank);
+/* In-place all-reduce (sum or max) of n doubles in device memory, on `stream`. */
+int ls_comm_allreduce_f64(ls_comm* c, double* buf_d, int64_t n, int op, void* stream);
+/* ls_pipeline_energy over this rank's slabs [k0, k1), then the sum over all ranks: every
+ * rank's out_d[0] receives the whole-grid energy. */
+int ls_pipeline_energy_allreduce(ls_pipeline* p, const double* r1_d, const double* r2_d, const double* r3_d,
+                                 int64_t k0, int64_t k1, double* out_d, ls_comm* c, void* stream);
 
 /* Small runtime helpers for callers without the CUDA headers: device memory
  * on the current device, a synchronous copy in any direction (cudaMemcpyDefault

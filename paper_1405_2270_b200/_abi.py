@@ -47,6 +47,13 @@ SIGNATURES = {
     "ls_charge_grid_index": (_i, [_d, _i64, _d, _i, _i, _vp]),
     "ls_validate_lattice": (_i, [_vp, _i64, _d, _vp, _i, _vp]),
     "ls_dev_knobs_enabled": (_i, []),
+    "ls_set_host_threads": (_i, [_i]),
+    "ls_comm_unique_id": (_i, [_vp, _i]),
+    "ls_comm_init": (_i, [_i, _i, _vp, _i, _vp]),
+    "ls_comm_destroy": (_i, [_vp]),
+    "ls_comm_info": (_i, [_vp, _vp, _vp]),
+    "ls_comm_allreduce_f64": (_i, [_vp, _vp, _i64, _i, _vp]),
+    "ls_pipeline_energy_allreduce": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "ls_assemble_axis": (_i, [_vp, _i64, _i, _i, _vp, _i64, _i64, _i, _vp, _i64, _vp]),
     "ls_expand": (_i, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i, _i64, _i64, _vp, _i64, _i64,
                        _vp, _vp, _vp, _vp, _vp]),

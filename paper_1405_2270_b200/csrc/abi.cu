@@ -6,7 +6,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <condition_variable>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -140,14 +143,134 @@ int upload(DevBuf& b, const void* host, size_t bytes, cudaStream_t s) {
 }
 
 
-// Expands slabs [k0, k1) of a device-resident tensor into host memory: the
-// compute stream fills chunk buffers, the copy stream drains them, and two
-// chunk buffers alternate so compute of chunk c+1 overlaps the copy of c.
+// Host threads the pageable copy-out uses (ls_set_host_threads); 0 = min(8, hardware).
+std::atomic<int>& host_threads() {
+    static std::atomic<int> n{0};
+    return n;
+}
+
+// Pinned staging for pageable destinations: a bounded ring of page-locked pieces per thread
+// and device (kRingSlots x kPieceBytes = 256 MiB), so a caller's ordinary (numpy, std::vector)
+// buffer receives the grid at near link speed without pinning gigabytes of host memory.
+constexpr int kRingSlots = 8;
+constexpr int64_t kPieceBytes = 32ll << 20;
+
+struct PinnedRing {
+    int device = -1;
+    void* slot[kRingSlots] = {};
+    cudaEvent_t ready[kRingSlots] = {};
+    ~PinnedRing() {
+        for (int r = 0; r < kRingSlots; ++r) {
+            if (slot[r]) cudaFreeHost(slot[r]);
+            if (ready[r]) cudaEventDestroy(ready[r]);
+        }
+    }
+};
+
+int get_ring(PinnedRing*& out) {
+    thread_local PinnedRing ring;
+    int dev = 0;
+    LS_CUDA(cudaGetDevice(&dev));
+    if (ring.device != dev) {
+        for (int r = 0; r < kRingSlots; ++r) {
+            if (ring.slot[r]) cudaFreeHost(ring.slot[r]);
+            ring.slot[r] = nullptr;
+            LS_CUDA(cudaMallocHost(&ring.slot[r], static_cast<size_t>(kPieceBytes)));
+            if (!ring.ready[r]) LS_CUDA(cudaEventCreateWithFlags(&ring.ready[r], cudaEventDisableTiming));
+        }
+        ring.device = dev;
+    }
+    out = &ring;
+    return LS_OK;
+}
+
+// Copy-out workers: each job waits for its piece's D2H event, then memcpy's the pinned piece
+// into the caller's buffer. Jobs run in submission order per worker (round robin), and a
+// slot is reused only after its previous job has finished (done[r]).
+class CopyOut {
+public:
+    explicit CopyOut(int n) : queues_(static_cast<size_t>(n)) {
+        for (int t = 0; t < n; ++t) workers_.emplace_back([this, t] { run(t); });
+    }
+    ~CopyOut() { finish(); }
+    void submit(int slot, cudaEvent_t ev, void* dst, const void* src, size_t bytes) {
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            busy_[slot] = true;
+            queues_[static_cast<size_t>(next_)].push_back({slot, ev, dst, src, bytes});
+            next_ = (next_ + 1) % static_cast<int>(workers_.size());
+        }
+        cv_.notify_all();
+    }
+    // Blocks until the last job that used `slot` has finished copying out of it.
+    void wait_slot(int slot) {
+        std::unique_lock<std::mutex> lock(mu_);
+        done_cv_.wait(lock, [&] { return !busy_[slot]; });
+    }
+    void finish() {
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            if (stop_) return;
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    bool failed() const { return failed_.load(); }
+
+private:
+    struct Job {
+        int slot;
+        cudaEvent_t ev;
+        void* dst;
+        const void* src;
+        size_t bytes;
+    };
+    void run(int t) {
+        for (;;) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> lock(mu_);
+                cv_.wait(lock, [&] { return stop_ || !queues_[static_cast<size_t>(t)].empty(); });
+                if (queues_[static_cast<size_t>(t)].empty()) return;  // stop_ and drained
+                j = queues_[static_cast<size_t>(t)].front();
+                queues_[static_cast<size_t>(t)].erase(queues_[static_cast<size_t>(t)].begin());
+            }
+            if (cudaEventSynchronize(j.ev) != cudaSuccess) failed_ = true;
+            else std::memcpy(j.dst, j.src, j.bytes);
+            {
+                std::lock_guard<std::mutex> lock(mu_);
+                busy_[j.slot] = false;
+            }
+            done_cv_.notify_all();
+        }
+    }
+    std::vector<std::vector<Job>> queues_;
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    bool busy_[kRingSlots] = {};
+    bool stop_ = false;
+    int next_ = 0;
+    std::atomic<bool> failed_{false};
+};
+
+// Expands slabs [k0, k1) of a device-resident tensor into host memory. The compute stream
+// fills ~1 GiB chunk buffers (two alternate, so the expansion of chunk c+1 overlaps the copy of
+// chunk c); the copy stream drains them. A page-locked destination (cudaMallocHost /
+// cudaHostRegister, e.g. a pinned torch tensor) receives the D2H copies directly; a pageable
+// one goes through the bounded pinned ring above, piece by piece, with host threads moving
+// each piece into place while the link carries the next.
 int expand_to_host(const double* A, const double* B, const double* C, const double* w,
                    const int64_t d[3], int R, int64_t k0, int64_t k1, double* out_h, Streams& st) {
     const int64_t slab = d[0] * d[1];
     if (k1 <= k0 || slab == 0) return LS_OK;
     const int64_t slab_bytes = slab * static_cast<int64_t>(sizeof(double));
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, out_h) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // an unregistered pointer is not an error here
+    PinnedRing* ring = nullptr;
+    if (!pinned) LS_TRY(get_ring(ring));
     // ~1 GiB chunks: enough work units per launch to fill the GPU; two buffers in flight.
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, (1ll << 30) / slab_bytes));
     DevBuf buf[2];
@@ -157,8 +280,12 @@ int expand_to_host(const double* A, const double* B, const double* C, const doub
         LS_CUDA(cudaEventCreateWithFlags(&done_compute[b], cudaEventDisableTiming));
         LS_CUDA(cudaEventCreateWithFlags(&done_copy[b], cudaEventDisableTiming));
     }
+    int nt = host_threads().load();
+    if (nt <= 0) nt = static_cast<int>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())));
+    std::unique_ptr<CopyOut> copier;
+    if (!pinned) copier.reset(new CopyOut(std::min(nt, kRingSlots)));
     int rc = LS_OK;
-    int64_t c = 0;
+    int64_t c = 0, piece = 0;
     for (int64_t ks = k0; ks < k1 && rc == LS_OK; ks += chunk, ++c) {
         const int b = static_cast<int>(c & 1);
         const int64_t ke = std::min(k1, ks + chunk);
@@ -168,11 +295,31 @@ int expand_to_host(const double* A, const double* B, const double* C, const doub
         if (rc != LS_OK) break;
         cudaEventRecord(done_compute[b], st.compute);
         cudaStreamWaitEvent(st.copy, done_compute[b], 0);
-        cudaError_t e = cudaMemcpyAsync(out_h + (ks - k0) * slab, buf[b].p,
-                                        static_cast<size_t>((ke - ks) * slab_bytes),
-                                        cudaMemcpyDeviceToHost, st.copy);
-        if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync D2H");
+        const int64_t bytes = (ke - ks) * slab_bytes;
+        char* dst = reinterpret_cast<char*>(out_h + (ks - k0) * slab);
+        const char* src = static_cast<const char*>(buf[b].p);
+        if (pinned) {
+            cudaError_t e = cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost, st.copy);
+            if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync D2H");
+        } else {
+            for (int64_t off = 0; off < bytes && rc == LS_OK; off += kPieceBytes, ++piece) {
+                const int r = static_cast<int>(piece % kRingSlots);
+                const size_t n = static_cast<size_t>(std::min(kPieceBytes, bytes - off));
+                copier->wait_slot(r);  // the slot's previous piece has left it
+                cudaError_t e = cudaMemcpyAsync(ring->slot[r], src + off, n, cudaMemcpyDeviceToHost, st.copy);
+                if (e != cudaSuccess) {
+                    rc = cuda_fail(e, "cudaMemcpyAsync D2H (pinned ring)");
+                    break;
+                }
+                cudaEventRecord(ring->ready[r], st.copy);
+                copier->submit(r, ring->ready[r], dst + off, ring->slot[r], n);
+            }
+        }
         cudaEventRecord(done_copy[b], st.copy);
+    }
+    if (copier) {
+        copier->finish();
+        if (copier->failed() && rc == LS_OK) rc = fail(LS_ECUDA, "expand_to_host: D2H piece failed");
     }
     cudaError_t e1 = cudaStreamSynchronize(st.copy);
     cudaError_t e2 = cudaStreamSynchronize(st.compute);
@@ -249,6 +396,12 @@ int ls_fault_status(int reset) {
     LS_CUDA(cudaMemcpy(&v, f, sizeof(v), cudaMemcpyDeviceToHost));
     if (v != 0 && reset) LS_CUDA(cudaMemset(f, 0, sizeof(unsigned)));
     return v != 0 ? 1 : 0;
+}
+
+int ls_set_host_threads(int n) {
+    if (n < 0) return ls::fail(LS_EVALIDATION, "set_host_threads: negative count");
+    ls::host_threads() = n;
+    return LS_OK;
 }
 
 int ls_dev_knobs_enabled(void) {

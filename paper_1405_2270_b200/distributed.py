@@ -68,3 +68,40 @@ class ShardedPotential:
         scalar all_reduce."""
         local = self.pipe.grid_functional(rho, self.k0, self.k1, stream)
         return all_reduce_sum(local, self.group)
+
+
+# ------------------------------------------------------------- the C++ runner
+def runner_path():
+    """The C++ multi-GPU runner (paper_1405_2270_b200/bin/latsum_shard_runner, built by
+    ``python -m paper_1405_2270_b200.build``): one process per GPU, DevicePotential +
+    Communicator (include/latsum/sharded.hpp), NCCL all-reduce through the C ABI."""
+    from pathlib import Path
+    p = Path(__file__).resolve().parent / "bin" / "latsum_shard_runner"
+    if not p.exists():
+        raise FileNotFoundError(f"{p} not built (python -m paper_1405_2270_b200.build)")
+    return p
+
+
+def nccl_id_hex() -> str:
+    """A fresh NCCL unique id (rank 0), as the runner's --id-hex argument."""
+    import subprocess
+    r = subprocess.run([str(runner_path()), "--print-id"], capture_output=True, text=True, check=True)
+    return r.stdout.strip()
+
+
+def run_runner(args: Sequence[str], env: dict | None = None, timeout: float = 1800.0) -> dict | None:
+    """Runs one rank of the C++ runner; returns its JSON line (rank 0) or None (other ranks).
+    The runner's stderr (NCCL INFO lines included) passes through."""
+    import json
+    import os
+    import subprocess
+    import sys
+    e = dict(os.environ)
+    if env:
+        e.update(env)
+    r = subprocess.run([str(runner_path()), *map(str, args)], stdout=subprocess.PIPE, stderr=sys.stderr,
+                       text=True, env=e, timeout=timeout)
+    if r.returncode != 0:
+        raise RuntimeError(f"latsum_shard_runner exited with {r.returncode}: {r.stdout[-2000:]}")
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return json.loads(lines[-1]) if lines else None
