@@ -687,12 +687,18 @@ def run_sharded(args, rank, world, local_rank):
     does all device work, takes every timing as the max over ranks (NCCL all-reduce) and rank
     0's Python composes the JSON line."""
     import torch.distributed as dist
-    from paper_1405_2270_b200.distributed import nccl_id_hex, run_runner, weak_scaling_lattice
+    import secrets
+    from paper_1405_2270_b200.distributed import run_runner, weak_scaling_lattice
     import paper_1405_2270_b200 as L
     L.load_library()  # the product library is mapped in this process too (the runner links it)
     dist.init_process_group("gloo")
-    box = [nccl_id_hex() if rank == 0 else None]
-    dist.broadcast_object_list(box, src=0)
+
+    def id_file():
+        # rank 0's runner creates the NCCL id (its bootstrap root lives in that process) and
+        # writes it to this fresh path; the other ranks' runners wait for the file
+        box = [f"/tmp/latsum_nccl_{secrets.token_hex(8)}.id" if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        return box[0]
     ncores = os.cpu_count() or 1
     common = ["--n", n_CELL, "--b", B, "--M", M_QUAD, "--eps", EPS, "--world", world, "--rank", rank,
               "--device", local_rank, "--host-threads", max(1, ncores // world)]
@@ -700,16 +706,14 @@ def run_sharded(args, rank, world, local_rank):
     with ClockSampler(None if rank == 0 else -1) as clk:
         dist.barrier()
         clk.mark()
-        res = run_runner(["--L", CFG2_L, "--id-hex", box[0], "--steps", args.steps, "--warmup", args.warmup,
+        res = run_runner(["--L", CFG2_L, "--id-file", id_file(), "--steps", args.steps, "--warmup", args.warmup,
                           "--energy", "--e2e-steps", 0 if args.step_only else max(1, min(args.e2e_steps, 2)),
                           *common], env)
         clocks = clk.summary()
     weak = None
     if not args.step_only:
-        box = [nccl_id_hex() if rank == 0 else None]
-        dist.broadcast_object_list(box, src=0)
         Lw = weak_scaling_lattice(world)
-        weak = run_runner(["--L", ",".join(map(str, Lw)), "--id-hex", box[0], "--steps", max(3, args.steps // 4),
+        weak = run_runner(["--L", ",".join(map(str, Lw)), "--id-file", id_file(), "--steps", max(3, args.steps // 4),
                            "--warmup", 3, *common], env)
     dist.barrier()
     dist.destroy_process_group()

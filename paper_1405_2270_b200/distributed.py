@@ -82,13 +82,6 @@ def runner_path():
     return p
 
 
-def nccl_id_hex() -> str:
-    """A fresh NCCL unique id (rank 0), as the runner's --id-hex argument."""
-    import subprocess
-    r = subprocess.run([str(runner_path()), "--print-id"], capture_output=True, text=True, check=True)
-    return r.stdout.strip()
-
-
 def run_runner(args: Sequence[str], env: dict | None = None, timeout: float = 1800.0) -> dict | None:
     """Runs one rank of the C++ runner; returns its JSON line (rank 0) or None (other ranks).
     The runner's stderr (NCCL INFO lines included) passes through."""

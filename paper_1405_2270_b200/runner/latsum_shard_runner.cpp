@@ -10,11 +10,13 @@
 //
 //   latsum_shard_runner --L 32 --n 64 --b 10 --M 20 [--charges cell.csv] [--periodic]
 //                       [--world W --rank R --device D] (default: $WORLD_SIZE $RANK $LOCAL_RANK)
-//                       [--id-hex HEX | --id-file PATH | --print-id]
+//                       [--id-hex HEX | --id-file PATH]
 //                       [--steps K] [--warmup W] [--energy] [--e2e-steps E] [--host-threads T]
 //
-// bench.py drives it under torchrun for --gpus N > 1 (the NCCL id travels over the launcher's
-// gloo group); without an id and with world = 1 it makes its own.
+// bench.py drives it under torchrun for --gpus N > 1: rank 0's runner creates the NCCL id and
+// writes it to a fresh --id-file path the launcher's gloo group agreed on (the id's bootstrap
+// root lives in the process that created it, so rank 0 must be a runner that stays up). With
+// --id-hex the caller moved the id of a living rank 0 itself; world = 1 needs neither.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -45,7 +47,6 @@ struct Args {
     bool periodic = false;
     int world = -1, rank = -1, device = -1;
     std::string id_hex, id_file;
-    bool print_id = false;
     int steps = 20, warmup = 3, e2e_steps = 0, host_threads = 0;
     bool energy = false;
     bool midpoint = false;
@@ -84,7 +85,6 @@ Args parse(int argc, char** argv) {
         else if (k == "--device") a.device = std::atoi(val().c_str());
         else if (k == "--id-hex") a.id_hex = val();
         else if (k == "--id-file") a.id_file = val();
-        else if (k == "--print-id") a.print_id = true;
         else if (k == "--steps") a.steps = std::atoi(val().c_str());
         else if (k == "--warmup") a.warmup = std::atoi(val().c_str());
         else if (k == "--e2e-steps") a.e2e_steps = std::atoi(val().c_str());
@@ -97,16 +97,6 @@ Args parse(int argc, char** argv) {
     if (a.device < 0) a.device = env_int("LOCAL_RANK", a.rank);
     if (a.steps < 1 || a.warmup < 0) usage("need --steps >= 1 and --warmup >= 0");
     return a;
-}
-
-std::string to_hex(const latsum::CommId& id) {
-    static const char* d = "0123456789abcdef";
-    std::string s;
-    for (unsigned char c : id) {
-        s += d[c >> 4];
-        s += d[c & 15];
-    }
-    return s;
 }
 
 latsum::CommId from_hex(const std::string& s) {
@@ -159,10 +149,6 @@ double wall_s() {
 
 int main(int argc, char** argv) try {
     const Args a = parse(argc, argv);
-    if (a.print_id) {  // rank 0 of a launcher that moves the id itself
-        std::printf("%s\n", to_hex(latsum::Communicator::unique_id()).c_str());
-        return 0;
-    }
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     const int dev = a.device % std::max(ndev, 1);
