@@ -473,7 +473,7 @@ bool fits_tmem_shape(int KD, int n_tail, TmemShape sh) {
     if (n_tail > 2 || 2 * (8 * KD + 16 * n_tail) > tmem_cols(8)) return false;
     const size_t jt = static_cast<size_t>(TileWide::JT) * sh.jps;
     const size_t stage = jt * KD * 32 + jt * 8 * n_tail;
-    return 2 * (sizeof(double) * (32 + tmem_stg_elems(8) + sh.ns * stage) + 1024) <= kSmemPerSM;
+    return 2 * (sizeof(double) * (kTmemHdr + tmem_stg_elems(8) + sh.ns * stage) + 1024) <= kSmemPerSM;
 }
 // Ring depth 4 where it fits (ranks up to 45), else 3 (up to 57); LS_EXPAND_TMEM overrides.
 TmemShape tmem_shape_for(int KD, int n_tail) {
@@ -489,7 +489,7 @@ int tmem16_stage_ks(int KD, int n_tail) {
     const size_t jt = TileTmem16::JT;
     for (int kc : {KD, (KD + 1) / 2}) {
         const size_t stage = jt * kc * 32 + jt * 8 * n_tail;
-        if (sizeof(double) * (32 + tmem_stg_elems(16) + TileTmem16::NS * stage) + 1024 <= kSmemPerSM) return kc;
+        if (sizeof(double) * (kTmemHdr + tmem_stg_elems(16) + TileTmem16::NS * stage) + 1024 <= kSmemPerSM) return kc;
         if (KD > 30) break;  // chunked instantiations exist for KD 24..30 only
     }
     return 0;
@@ -624,7 +624,7 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     LS_LAUNCHED("pack_b_kernel");
     a.Bp = bp;
     const size_t smem =
-        TMEM ? sizeof(double) * (32 + tmem_stg_elems(T::WARPS) + sh.ns * stage_elems) : smem_bytes<T>(a.KD, a.KC, a.n_tail);
+        TMEM ? sizeof(double) * (kTmemHdr + tmem_stg_elems(T::WARPS) + sh.ns * stage_elems) : smem_bytes<T>(a.KD, a.KC, a.n_tail);
     void (*kern)(ExpandArgs) = nullptr;
     if constexpr (!TMEM) {
         kern = expand_dmma_kernel<T, STORE, FUNC>;
@@ -657,7 +657,8 @@ int launch(ExpandArgs& a, cudaStream_t s) {
         const int64_t full = a.n_units / G, tail = a.n_units - full * G;
         const int64_t whole = ls::ceil_div(a.n_units, G) * a.n_jc;
         const int64_t split = full * a.n_jc + ls::ceil_div(tail * a.n_jc, G);
-        if (tail > 0 && split + 2 <= whole && a.n_kc == 1) {
+        const bool force = ls::dev_knob("LS_SPLIT_ALL") != nullptr;  // lab A/B
+        if (tail > 0 && (split + 2 <= whole || force) && a.n_kc == 1) {
             a.split_tail = 1;
             grid = std::min<int64_t>(a.n_units * a.n_jc, G);
         }
@@ -672,6 +673,16 @@ int launch(ExpandArgs& a, cudaStream_t s) {
     }
     return LS_OK;
 }
+
+#ifdef LS_TIMELINE
+// Lab builds only: the event log of the last instrumented launch (see k3.cuh).
+constexpr size_t kLabTimelineBytes = size_t(148) * 2 * 16 * 128 * sizeof(unsigned long long);
+unsigned long long* lab_timeline() {
+    static unsigned long long* p = nullptr;
+    if (!p) cudaMalloc(&p, kLabTimelineBytes);
+    return p;
+}
+#endif
 
 constexpr int kRankChunk = 256;
 
@@ -707,6 +718,14 @@ int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+#ifdef LS_TIMELINE
+extern "C" int ls_lab_timeline(unsigned long long* host, int64_t n) {
+    const size_t bytes = std::min<size_t>(kLabTimelineBytes, size_t(n) * sizeof(unsigned long long));
+    LS_CUDA(cudaMemcpy(host, lab_timeline(), bytes, cudaMemcpyDeviceToHost));
+    return LS_OK;
+}
+#endif
 
 extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_t k0, int64_t k1) {
     (void)N2;
@@ -781,6 +800,12 @@ extern "C" int ls_expand(const double* A_d, int64_t lda, const double* B_d, int6
     if (const char* dbg = ls::dev_knob("LS_EXPAND_DEBUG")) a.debug = std::atoi(dbg);
     a.fault = ls::fault_flag();
     if (a.fault == nullptr) return ls::fail(LS_ECUDA, "expand: no CUDA device");
+#ifdef LS_TIMELINE
+    if (ls::dev_knob("LS_TIMELINE")) {
+        LS_CUDA(cudaMemsetAsync(lab_timeline(), 0, kLabTimelineBytes, s));
+        a.timeline = lab_timeline();
+    }
+#endif
     const bool store = out_d != nullptr;
     Plan pl;
     if (plan_for(a.KD, a.n_tail, pl)) {

@@ -104,16 +104,20 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     const int per_unit = static_cast<int>(p.n_jc) * n_kc;
     const unsigned stage_bytes = static_cast<unsigned>(stage_elems * sizeof(double));
 
-    // Shared-memory header (256 bytes): 16 mbarrier slots, then the slot counters and the TMEM
-    // base address; the A2 ring follows.
-    static_assert(kNS + 4 <= 16 && kNS <= 12, "header holds up to 12 ring slots");
+    // Shared-memory header (kTmemHdr doubles): ring mbarriers, then the A1k hand-over
+    // mbarriers per buffer and TMEM lane quarter, the ring release counters and the TMEM base
+    // address; the fill staging and the A2 ring follow.
+    static_assert(kNS <= 12, "header holds up to 12 ring slots");
     extern __shared__ __align__(128) double smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // [kNS] A2 stage landed
-    uint64_t* as_full = full + kNS;                            // [2] A1k buffer written by every warp
-    uint64_t* as_empty = as_full + 2;                          // [2] A1k buffer released by every warp
-    int* released = reinterpret_cast<int*>(smem + 16);         // [kNS] warps done with a ring slot
-    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 24);
-    double* ring = smem + 32 + tmem_stg_elems(WARPS);          // [kNS][stage_elems]
+    // A1k buffer b, lane quarter q is written and read only by the WJ warps of that quarter
+    // (warp & 3 == q), so the hand-over is per quarter: a quarter's warps never wait for the
+    // other quarters' skew at unit boundaries.
+    uint64_t* as_full = full + 12;                             // [2][4] quarter's A1k written by its WJ warps
+    uint64_t* as_empty = full + 20;                            // [2][4] quarter's A1k released by its WJ warps
+    int* released = reinterpret_cast<int*>(smem + 28);         // [kNS] warps done with a ring slot
+    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 34);
+    double* ring = smem + kTmemHdr + tmem_stg_elems(WARPS);    // [kNS][stage_elems]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -166,9 +170,9 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
             mbar_init(full + b, 1);
             released[b] = 0;
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(as_full + b, WARPS);
-            mbar_init(as_empty + b, WARPS);
+        for (int b = 0; b < 8; ++b) {
+            mbar_init(as_full + b, WJ);
+            mbar_init(as_empty + b, WJ);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -178,75 +182,99 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     // TMEM allocation and barrier set-up overlap the tail of the preceding (prep) launch; the
     // packed A2, the scale table and the factors are read only after it completes.
     pdl_wait();
+    LS_TL_INIT();
+    LS_TL(1);  // set-up done
     const uint32_t tq = *tmem_base_s + (static_cast<uint32_t>(32 * wi) << 16);  // this warp's lane quarter
-    double* stg = smem + 32 + warp * (kFillSlots * 32) + lane;  // this lane's fill staging slots (stride 32)
+    double* stg = smem + kTmemHdr + warp * (kFillSlots * 32) + lane;  // this lane's fill staging (stride 32)
 
     // Fill tasks of one unit for this warp: fragment k-steps ks = wj, wj+WJ, ... (4 values each),
-    // then (warp wj == 0 only) the tail ranks (8 values each).
+    // then (warp wj == 0 only) the tail ranks, each as two half tasks of 4 values (so every
+    // task stages 4 A1 values + 1 scale).
     const int n_frag_tasks = (KD - wj + WJ - 1) / WJ;
-    const int n_tasks = n_frag_tasks + (wj == 0 ? n_tail : 0);
-    // A fill task's operands are copied global->shared asynchronously one task ahead (the copy
-    // for the following task is issued right after a task is consumed), so the L2 latency of the
-    // A1/S reads is off the warp's critical path.
-    auto task_issue = [&](int u, int task) {
+    const int n_tasks = n_frag_tasks + (wj == 0 ? 2 * n_tail : 0);
+#ifdef LS_DEV_KNOBS
+    const bool lab_nofill = (p.debug & 2) != 0;   // lab A/B: later units reuse the first A1k
+    const bool lab_nostore = (p.debug & 1) != 0;  // lab A/B: epilogue without stores
+#else
+    constexpr bool lab_nofill = false, lab_nostore = false;
+#endif
+    // A fill task's operands are copied global->shared asynchronously TWO tasks ahead, through two
+    // staging slots: the copy for task e + 2 is issued right after task e is consumed, so even
+    // when a stage consumes two tasks back to back (short units: 4 stages per unit at 256^3)
+    // the L2 latency of the A1/S reads stays off the warp's critical path. Tasks form one
+    // sequence per warp over the units after the first: e = (nu - 1) * n_tasks + task.
+    auto task_issue = [&](int u, int task, double* sg) {
         const int ib = (u % n_ichunks) * IC;
         const int64_t k = p.k0 + u / n_ichunks;
         if (task < n_frag_tasks) {
             const int ks = wj + WJ * task;
             const int q = 4 * ks + t;
-            cp_async8(stg + 8 * 32, p.S + k * p.R + (q < p.R ? q : 0), q < p.R);
+            cp_async8(sg + 4 * 32, p.S + k * p.R + (q < p.R ? q : 0), q < p.R);
 #pragma unroll
             for (int it = 0; it < 4; ++it) {
                 const int i = ib + 8 * (4 * wi + it) + g;
                 const bool ok = i < p.N1 && q < p.R;
-                cp_async8(stg + it * 32, ok ? p.A + i + p.lda * q : p.A, ok);
+                cp_async8(sg + it * 32, ok ? p.A + i + p.lda * q : p.A, ok);
             }
         } else {
-            const int q = 4 * KD + (task - n_frag_tasks);  // q >= R: the zero rank (see below)
-            cp_async8(stg + 8 * 32, q < p.R ? p.S + k * p.R + q : p.S, q < p.R);
+            const int ht = task - n_frag_tasks;           // half task: tail rank ht / 2, half ht % 2
+            const int q = 4 * KD + (ht >> 1);              // q >= R: the zero rank (see below)
+            cp_async8(sg + 4 * 32, q < p.R ? p.S + k * p.R + q : p.S, q < p.R);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e4 = 0; e4 < 4; ++e4) {
+                const int e = 4 * (ht & 1) + e4;
                 const int i = ib + 32 * wi + 8 * (e >> 1) + 2 * t + (e & 1);
                 const bool ok = i < p.N1 && q < p.R;
-                cp_async8(stg + e * 32, ok ? p.A + i + p.lda * q : p.A, ok);
+                cp_async8(sg + e4 * 32, ok ? p.A + i + p.lda * q : p.A, ok);
             }
         }
         cp_async_commit();
     };
-    auto task_consume = [&](int buf, int task) {
-        cp_async_wait_all();
-        const double sv = stg[8 * 32];
+    const int n_seq = (my_units - 1) * n_tasks;  // fill tasks after the prologue's unit
+    int n_issued = 0;                             // cp.async groups committed (one per task)
+    auto seq_issue = [&](int e) {
+        if (e >= n_seq) return;
+#ifdef LS_DEV_KNOBS
+        if (p.debug & 32) return;  // lab A/B: no fill loads (stale staging)
+#endif
+        task_issue(unit_of(1 + e / n_tasks), e % n_tasks, stg + (e & 1) * (kTaskSlots * 32));
+        ++n_issued;
+    };
+    auto task_consume = [&](int buf, int task, int e) {
+        // the group of task e is complete once at most n_issued - e - 1 (0 or 1) groups are pending
+        if (n_issued - e - 1 >= 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else cp_async_wait_all();
+        const double* sg = stg + (e & 1) * (kTaskSlots * 32);
+        const double sv = sg[4 * 32];
         const uint32_t col = static_cast<uint32_t>(buf * CB);
+        double v[4];
+#pragma unroll
+        for (int it = 0; it < 4; ++it) v[it] = rn_mul(sg[it * 32], sv);  // Eigen's A1 * scale.asDiagonal()
+#ifdef LS_DEV_KNOBS
+        if (p.debug & 64)
+#pragma unroll
+            for (int it = 0; it < 4; ++it) v[it] = sg[it * 32];  // lab A/B: no DMUL
+        if (p.debug & 16) return;                               // lab A/B: no TMEM store
+#endif
         if (task < n_frag_tasks) {
-            const int ks = wj + WJ * task;
-            double v[4];
-#pragma unroll
-            for (int it = 0; it < 4; ++it) v[it] = rn_mul(stg[it * 32], sv);  // Eigen's A1 * scale.asDiagonal()
-            tmem::st_x8(tq + col + 8 * ks, v);
+            tmem::st_x8(tq + col + 8 * (wj + WJ * task), v);
         } else {
-            const int qt = task - n_frag_tasks;
-            double v0[4], v1[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                v0[e] = rn_mul(stg[e * 32], sv);
-                v1[e] = rn_mul(stg[(4 + e) * 32], sv);
-            }
-            tmem::st_x8(tq + col + 8 * KD + 16 * qt, v0);
-            tmem::st_x8(tq + col + 8 * KD + 16 * qt + 8, v1);
+            const int ht = task - n_frag_tasks;
+            tmem::st_x8(tq + col + 8 * KD + 16 * (ht >> 1) + 8 * (ht & 1), v);
         }
     };
-    // Consume task `task` of this CTA's unit number nu into buffer buf, then start the copy for
-    // the task after it (the next unit's first task after the last one).
+    // Consume task `task` of this CTA's unit number nu into buffer buf, then start the copy two
+    // tasks further down the sequence.
     auto run_task = [&](int nu, int task, int buf) {
-        task_consume(buf, task);
-        if (task + 1 < n_tasks) task_issue(unit_of(nu), task + 1);
-        else if (nu + 1 < my_units) task_issue(unit_of(nu + 1), 0);
+        const int e = (nu - 1) * n_tasks + task;
+        task_consume(buf, task, e);
+        seq_issue(e + 2);
     };
     auto publish = [&](int buf) {
         tmem::wait_st();
         tmem::fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(as_full + buf);
+        if (lane == 0) mbar_arrive(as_full + 4 * buf + wi);
     };
 
     // The first ring stages load while the warps build the first unit's A1k.
@@ -260,7 +288,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         const int ib = (u % n_ichunks) * IC;
         const int64_t k = p.k0 + u / n_ichunks;
         for (int t0 = 0; t0 < n_tasks; t0 += 4) {
-            double av[4][8], sv[4];
+            double av[4][4], sv[4];
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
                 const int task = t0 + b;
@@ -274,12 +302,14 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                         av[b][it] = (i < p.N1 && q < p.R) ? __ldg(p.A + i + p.lda * q) : 0.0;
                     }
                 } else {
-                    const int q = 4 * KD + (task - n_frag_tasks);
+                    const int ht = task - n_frag_tasks;
+                    const int q = 4 * KD + (ht >> 1);
                     sv[b] = q < p.R ? __ldg(p.S + k * p.R + q) : 0.0;
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
+                    for (int e4 = 0; e4 < 4; ++e4) {
+                        const int e = 4 * (ht & 1) + e4;
                         const int i = ib + 32 * wi + 8 * (e >> 1) + 2 * t + (e & 1);
-                        av[b][e] = (i < p.N1 && q < p.R) ? __ldg(p.A + i + p.lda * q) : 0.0;
+                        av[b][e4] = (i < p.N1 && q < p.R) ? __ldg(p.A + i + p.lda * q) : 0.0;
                     }
                 }
             }
@@ -287,27 +317,22 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
             for (int b = 0; b < 4; ++b) {
                 const int task = t0 + b;
                 if (task >= n_tasks) break;
-                if (task < n_frag_tasks) {
-                    double v[4];
+                double v[4];
 #pragma unroll
-                    for (int it = 0; it < 4; ++it) v[it] = rn_mul(av[b][it], sv[b]);
+                for (int it = 0; it < 4; ++it) v[it] = rn_mul(av[b][it], sv[b]);
+                if (task < n_frag_tasks) {
                     tmem::st_x8(tq + 8 * (wj + WJ * task), v);
                 } else {
-                    const int qt = task - n_frag_tasks;
-                    double v0[4], v1[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        v0[e] = rn_mul(av[b][e], sv[b]);
-                        v1[e] = rn_mul(av[b][4 + e], sv[b]);
-                    }
-                    tmem::st_x8(tq + 8 * KD + 16 * qt, v0);
-                    tmem::st_x8(tq + 8 * KD + 16 * qt + 8, v1);
+                    const int ht = task - n_frag_tasks;
+                    tmem::st_x8(tq + 8 * KD + 16 * (ht >> 1) + 8 * (ht & 1), v);
                 }
             }
         }
-        if (my_units > 1) task_issue(unit_of(1), 0);
+        seq_issue(0);
+        seq_issue(1);
         publish(0);
     }
+    LS_TL(2);  // prologue fill published
 
     double acc[kTM][kTN][2];
     double fsum = 0.0;
@@ -317,23 +342,26 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         // j-chunk range of this unit (partial only for the first and last unit of a split tail)
         const int jc_lo = (kSplitTail && n == n_full) ? t0 % per_unit : 0;
         const int jc_hi = (kSplitTail && n >= n_full && n == my_units - 1) ? (t1 - 1) % per_unit + 1 : per_unit;
-        // Fill schedule for the next unit: tasks spread evenly over this unit's stages, offset by
-        // warp so the warps of an SM sub-partition do not fill in the same stage. The 8-warp
-        // shape starts at the first stage: 1.7% faster at 256^3 (4 stages per unit, so fewer
-        // fill tasks share a stage) and 0.3% at cfg1. The 16-warp shape starts at the third
-        // (starting at the first measured -0.5 to -1.5% at ranks 73-113, +1.8% at 121). Ending
-        // the fill a stage or two before the unit's last stage changed nothing.
+        // Fill schedule for the next unit. 8-warp shape: the whole fill right after the first
+        // stage's DMMAs, so the rest of the unit is pure DMMA issue and the next unit's A1k is
+        // ready long before any warp of the quarter reaches it (with the per-quarter hand-over
+        // and two-ahead copies: 676 -> 660 us at 1024^2 x 256 slabs, 55.8 -> 54.1 us at 256^3,
+        // against tasks spread evenly over the unit's stages). 16-warp shape: spread over the
+        // stages from the third on, offset by warp (starting at the first measured -0.5 to
+        // -1.5% at ranks 73-113, +1.8% at 121).
         const int n_here = jc_hi - jc_lo;
         const int first_fill = (WARPS == 16 && n_here > 2) ? 2 : 0;
         auto fill_stage = [&](int task) {
+            if (WARPS == 8) return jc_lo;
             return jc_lo + first_fill + ((task * WARPS + warp) * (n_here - first_fill)) / (WARPS * n_tasks);
         };
         const int buf = n & 1;
         const bool has_next = n + 1 < my_units;
         const int ib = (unit % n_ichunks) * IC;
         const int64_t kk = unit / n_ichunks;
-        mbar_wait(as_full + buf, static_cast<unsigned>((n >> 1) & 1), p.fault);
+        mbar_wait(as_full + 4 * buf + wi, static_cast<unsigned>((n >> 1) & 1), p.fault);
         tmem::fence_after();
+        LS_TL(3);  // unit's A1k ready
         const uint32_t tb = tq + static_cast<uint32_t>(buf * CB);
         // rho1 of this lane's eight i columns, held for the whole unit (zero beyond N1, where the
         // accumulators are zero too).
@@ -351,18 +379,20 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         int next_task = 0;
 
         for (int w = jc_lo; w < jc_hi; ++w, ++st) {
+            LS_TL(7);  // stage loop top (previous epilogue done)
             const int jc = kChunked ? w / n_kc : w;  // j-chunk of this stage
             const int kc = kChunked ? w % n_kc : 0;  // k-chunk of this stage
             // Fill task(s) for the next unit: loads now, product + TMEM store after the DMMAs.
             int target = next_task;
-            if (has_next)
+            if (has_next && !lab_nofill)
                 while (target < n_tasks && fill_stage(target) <= w) ++target;
             const bool fill_now = target > next_task;
-            if (fill_now && next_task == 0 && n >= 1)  // buffer buf^1 was read by unit n-1
-                mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1), p.fault);
+            if (fill_now && next_task == 0 && n >= 1)  // this quarter of buffer buf^1 was read by unit n-1
+                mbar_wait(as_empty + 4 * (buf ^ 1) + wi, static_cast<unsigned>(((n - 1) >> 1) & 1), p.fault);
 
             const int slot = st % kNS;
             mbar_wait(full + slot, static_cast<unsigned>((st / kNS) & 1), p.fault);
+            LS_TL(4);  // stage landed
             const double* stage = ring + slot * stage_elems;
 #pragma unroll 1
             for (int h = 0; h < JPS; ++h) {
@@ -428,6 +458,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                         for (int ks = 0; ks < KD; ++ks) kstep(ks);
                     }
                 }
+                LS_TL(5);  // DMMAs issued
                 if (h == JPS - 1) {
                     // Release the ring slot; the last warp refills it with stage st + kNS.
                     __syncwarp();
@@ -448,6 +479,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                     }
                 }
 
+                LS_TL(6);  // slot released, fill tasks done
                 if (kChunked && kc != n_kc - 1) continue;  // the tile continues in the next stage
                 // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
                 const int jb = (jc * JPS + h) * JC + wj * (8 * kTM);
@@ -459,6 +491,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                                         : nullptr;
 #pragma unroll
                     for (int m = 0; m < kTM; ++m) {
+                        if (lab_nostore) break;
                         if (FUNC) {
                             double sm = 0.0;
 #pragma unroll
@@ -514,11 +547,11 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         // This warp is done reading A1k buffer buf.
         tmem::fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(as_empty + buf);
-        if (has_next && n_tasks == 0) publish(buf ^ 1);  // no fill share (KD = 1, wj = 1): still arrive
-        if (has_next && next_task < n_tasks) {  // tiny units: finish the fill now
+        if (lane == 0) mbar_arrive(as_empty + 4 * buf + wi);
+        if (has_next && (n_tasks == 0 || lab_nofill)) publish(buf ^ 1);  // no fill share (KD = 1, wj = 1): still arrive
+        else if (has_next && next_task < n_tasks) {  // tiny units: finish the fill now
             if (next_task == 0 && n >= 1)
-                mbar_wait(as_empty + (buf ^ 1), static_cast<unsigned>(((n - 1) >> 1) & 1), p.fault);
+                mbar_wait(as_empty + 4 * (buf ^ 1) + wi, static_cast<unsigned>(((n - 1) >> 1) & 1), p.fault);
             for (; next_task < n_tasks; ++next_task) run_task(n + 1, next_task, buf ^ 1);
             publish(buf ^ 1);
         }
@@ -533,6 +566,8 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
             }
         }
     }
+    LS_TL(8);  // all units done
+    LS_TL_END();
     tmem::fence_before();
     __syncthreads();
     if (warp == 0)

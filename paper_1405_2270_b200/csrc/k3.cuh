@@ -39,7 +39,36 @@ struct ExpandArgs {
     const double* S;  // per-slab scales S(k, q) = w_q * A3(k, q), [k][q] (TMEM variant)
     int split_tail;   // TMEM store-only: split the last round of units at stage granularity
     unsigned* fault;  // watchdog word of the device (ls::fault_flag)
+    unsigned long long* timeline;  // lab builds with -DLS_TIMELINE only: per-warp event log (else null)
 };
+
+// Lab instrumentation (-DLS_TIMELINE builds only; compiled out of the product): lane 0 of each
+// warp logs (clock64 << 8 | event) into 128 slots per warp, slot 0 holding the count and the
+// SM id, so tools/lab/timeline.py can attribute a CTA's time to waits, DMMA issue, fills and
+// epilogues.
+#ifdef LS_TIMELINE
+#define LS_TL_INIT()                                                                         \
+    int tl_n_ = 1;                                                                           \
+    unsigned long long* tl_ = p.timeline ? p.timeline + (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 128 : nullptr
+#define LS_TL(ev)                                                                            \
+    do {                                                                                     \
+        if (tl_ && (threadIdx.x & 31) == 0 && tl_n_ < 128) {                                 \
+            tl_[tl_n_++] = (static_cast<unsigned long long>(clock64()) << 8) | (ev);         \
+        }                                                                                    \
+    } while (0)
+#define LS_TL_END()                                                                          \
+    do {                                                                                     \
+        if (tl_ && (threadIdx.x & 31) == 0) {                                                \
+            unsigned smid;                                                                   \
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                                \
+            tl_[0] = (static_cast<unsigned long long>(smid) << 32) | static_cast<unsigned>(tl_n_); \
+        }                                                                                    \
+    } while (0)
+#else
+#define LS_TL_INIT() (void)0
+#define LS_TL(ev) (void)0
+#define LS_TL_END() (void)0
+#endif
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -102,8 +131,14 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
 
 // TMEM columns per CTA: 8-warp CTAs run two per SM (256 columns each), 16-warp CTAs one (512).
 __host__ __device__ constexpr int tmem_cols(int warps) { return warps == 8 ? 256 : 512; }
-constexpr int kFillSlots = 9;   // per lane: up to 8 A1 values + the slab scale of one fill task
+// Fill staging per lane: two tasks in flight (cp.async two tasks ahead), each 4 A1 values + the
+// slab scale.
+constexpr int kTaskSlots = 5;
+constexpr int kFillSlots = 2 * kTaskSlots;
 __host__ __device__ constexpr int tmem_stg_elems(int warps) { return warps * kFillSlots * 32; }  // per CTA
+// Shared-memory header of the TMEM kernels (doubles): ring mbarriers, per-lane-quarter A1k
+// hand-over mbarriers, ring release counters and the TMEM base address.
+constexpr int kTmemHdr = 48;
 
 using KernelFn = void (*)(ExpandArgs);
 
