@@ -443,7 +443,7 @@ struct Plan {
     int pad = 0;  // 1: run a 2-rank remainder as one zero-padded k-step (TMEM plans have a 1-rank tail)
 };
 
-constexpr int kPlanTmem = 20, kPlanTmem16 = 21, kPlanSplitK = 22;
+constexpr int kPlanTmem = 20, kPlanTmem16 = 21, kPlanSplitK = 22, kPlanTmem16S = 23;
 // TMEM variant shape (ring depth, j-chunks per stage); LS_EXPAND_TMEM=<ns><jps> overrides.
 struct TmemShape {
     int ns, jps;
@@ -495,6 +495,15 @@ int tmem16_stage_ks(int KD, int n_tail) {
     return 0;
 }
 bool fits_tmem16(int KD, int n_tail) { return tmem16_stage_ks(KD, n_tail) > 0; }
+// Single-buffer 16-warp TMEM plan (expand_tmem16s.cuh): KD 31..62 with one DFMA rank; one A1k
+// buffer of 8 KD + 16 <= 512 columns, NKC stages of KC k-steps per tile in a 2-deep ring.
+bool fits_tmem16s(int KD, int n_tail) {
+    if (tmem_tail(n_tail) != 1 || KD < 31 || KD > 62) return false;
+    const size_t jt = TileTmem16::JT, kc = static_cast<size_t>(tmem16s_kc(KD));
+    const size_t stage = jt * kc * 32 + jt * 8;
+    return sizeof(double) * (kTmemHdr + tmem_stg_elems(16) + TileTmem16::NS * stage) + 1024 <= kSmemPerSM &&
+           8 * KD + 16 <= tmem_cols(16);
+}
 
 template <class T>
 bool fits(int KD, int KC, int n_tail) {
@@ -514,8 +523,8 @@ bool plan_for(int KD, int n_tail, Plan& out) {
     // with a 64-row i-chunk (29.0) or 16-row warp tiles (no fit) were slower).
     // Up to KD 14 the 2-CTA TileWide with 8-k-step stages beats the 16-warp plan 9 (rank 46:
     // 27.1 vs 22.0 TF/s); beyond it plan 9 wins (rank 123: 26.4 vs 24.2).
-    const Cand small_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {kPlanSplitK, 0}, {0, 0}, {0, 8}, {9, 4}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
-    const Cand large_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {kPlanSplitK, 0}, {0, 0}, {9, 4}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
+    const Cand small_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {kPlanTmem16S, 0}, {kPlanSplitK, 0}, {0, 0}, {0, 8}, {9, 4}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
+    const Cand large_r[] = {{kPlanTmem, 0}, {kPlanTmem16, 0}, {kPlanTmem16S, 0}, {kPlanSplitK, 0}, {0, 0}, {9, 4}, {0, 8}, {8, 8}, {6, 5}, {7, 4}, {2, 4}, {3, 4}, {3, 2}, {1, 0}};
     for (const Cand& c : KD <= 14 ? small_r : large_r) {
         if (force >= 0 && c.id != force) continue;
         const int KC = c.KC == 0 ? KD : std::min(KD, c.KC);
@@ -545,12 +554,22 @@ bool plan_for(int KD, int n_tail, Plan& out) {
             // trade places within 2% on 1024^2 x 256 slabs (the split-K unit's exposed A1k fill
             // weighs more there); from rank 164 (KD 41) on split-K wins: 164-172 by 1-3%, rank 246
             // 29.7 vs 28.9 TF/s, cfg3's 328 32.9 vs 30.8.
+            // Ranks 122..249 (KD 31..62): the single-buffer 16-warp TMEM plan (31.9-33.7 TF/s at 1024^2 x
+            // 512 slabs against 26.0-29.8 for split-K and the smem plan 9 it replaces).
+            case kPlanTmem16S:
+                ok = fits_tmem16s(KD + (n_tail == 2), n_tail == 2 ? 0 : n_tail);
+                ic = TileTmem16::IC;
+                break;
             case kPlanSplitK: ok = (force == kPlanSplitK || KD >= 41) && fits_splitk(KD, n_tail); ic = 64; break;
             default: ok = fits<TileNarrow>(KD, KC, n_tail); ic = TileNarrow::IC; break;
         }
         if (ok) {
-            const int pad = c.id == kPlanTmem16 && n_tail == 2;
-            out = {c.id, c.id == kPlanTmem16 ? tmem16_stage_ks(KD + pad, pad ? 0 : n_tail) : KC + pad, ic, pad};
+            const int pad = (c.id == kPlanTmem16 || c.id == kPlanTmem16S) && n_tail == 2;
+            out = {c.id,
+                   c.id == kPlanTmem16    ? tmem16_stage_ks(KD + pad, pad ? 0 : n_tail)
+                   : c.id == kPlanTmem16S ? tmem16s_kc(KD + pad)
+                                          : KC + pad,
+                   ic, pad};
             if (const char* e = ls::dev_knob("LS_EXPAND_KC")) out.KC = std::max(1, std::min(KD, std::atoi(e)));
             return true;
         }
@@ -634,7 +653,8 @@ int launch(ExpandArgs& a, cudaStream_t s) {
             return ls::fail(LS_EVALIDATION, "expand: TMEM plan needs one DFMA rank (two with 8 warps)");
         if constexpr (T::WARPS == 16) {
             static_assert(T::NS == 2, "the 16-warp TMEM kernels are built with a 2-deep ring");
-            kern = tmem16_kernel(STORE, FUNC, a.KD, a.KC);
+            kern = a.KD >= 31 ? tmem16s_kernel(STORE, FUNC, a.KD) : tmem16_kernel(STORE, FUNC, a.KD, a.KC);
+            if (!kern) return ls::fail(LS_EVALIDATION, "expand: unsupported 16-warp TMEM shape");
         } else {
             kern = tmem8_kernel(STORE, FUNC, code, a.KD, a.n_tail);
             if (!kern) return ls::fail(LS_EVALIDATION, "expand: unsupported TMEM shape");
@@ -701,7 +721,8 @@ int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
     a.KC = std::min(pl.KC, a.KD);
     switch (pl.id) {
         case kPlanTmem: return launch<TileWide, STORE, FUNC, true>(a, s);
-        case kPlanTmem16: return launch<TileTmem16, STORE, FUNC, true>(a, s);
+        case kPlanTmem16:
+        case kPlanTmem16S: return launch<TileTmem16, STORE, FUNC, true>(a, s);
         case kPlanSplitK:
             // No zero DFMA rank when R mod 4 == 0 (unlike the TMEM plans): the pair's halves then
             // carry equal work, 0.8% at cfg3 and 1.6-2.4% at ranks 176-240.
@@ -736,7 +757,7 @@ extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_
     if (!plan_for(KD, n_tail, pl) && !chunk_plan(pl)) return -1;
     const int64_t IC = pl.ic;
     // the TMEM variant writes one partial per warp (no CTA barrier per unit)
-    return ls::ceil_div(N1, IC) * (k1 - k0) * (pl.id == kPlanTmem ? 8 : pl.id == kPlanTmem16 || pl.id == kPlanSplitK ? 16 : 1);
+    return ls::ceil_div(N1, IC) * (k1 - k0) * (pl.id == kPlanTmem ? 8 : pl.id == kPlanTmem16 || pl.id == kPlanTmem16S || pl.id == kPlanSplitK ? 16 : 1);
 }
 
 extern "C" int ls_expand_plan_name(int R, char* out, int len) {
@@ -747,16 +768,20 @@ extern "C" int ls_expand_plan_name(int R, char* out, int len) {
     const bool whole = plan_for(KD, n_tail, pl);
     if (!whole && !chunk_plan(pl)) return ls::fail(LS_EGUARD, "expand_plan_name: no tile plan");
     const int kd = pl.pad && n_tail == 2 ? KD + 1 : KD;
-    const int nt = pl.id == kPlanTmem || pl.id == kPlanTmem16 ? (pl.pad ? 1 : tmem_tail(n_tail)) : n_tail;
+    const int nt = pl.id == kPlanTmem || pl.id == kPlanTmem16 || pl.id == kPlanTmem16S ? (pl.pad ? 1 : tmem_tail(n_tail))
+                                                                                    : n_tail;
     const char* shape = pl.id == kPlanTmem     ? "expand_tmem_kernel, 8 warps x 2 CTAs/SM, A1k in TMEM"
                         : pl.id == kPlanTmem16 ? "expand_tmem_kernel, 16 warps x 1 CTA/SM, A1k in TMEM"
+                        : pl.id == kPlanTmem16S ? "expand_tmem_kernel, 16 warps x 1 CTA/SM, single A1k buffer in TMEM"
                         : pl.id == kPlanSplitK ? "expand_splitk_kernel, 16 warps x 1 CTA/SM, A1k halves in TMEM lane quarters"
                         : pl.id == 9           ? "expand_dmma_kernel TileLR16, 16 warps x 1 CTA/SM, A1k in smem"
                                                : "expand_dmma_kernel, A1k in smem";
     std::snprintf(out, static_cast<size_t>(len), "%s; plan %d, KD %d (%s), %d DFMA rank(s)%s", shape, pl.id, kd,
                   (pl.id == kPlanTmem && kd <= 14) || (pl.id == kPlanTmem16 && kd >= 14 && kd <= 23)
                       ? "compiled"
-                      : (pl.id == kPlanTmem16 && kd >= 24 && kd <= 30 ? "compiled, two stages per tile" : "runtime"),
+                      : (pl.id == kPlanTmem16 && kd >= 24 && kd <= 30 ? "compiled, two stages per tile"
+                         : pl.id == kPlanTmem16S                        ? "compiled, k-chunked stages"
+                                                                        : "runtime"),
                   nt, whole ? "" : ", 256-rank chunks");
     return LS_OK;
 }

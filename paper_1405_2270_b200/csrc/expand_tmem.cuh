@@ -84,7 +84,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // KC_ > 0 (16-warp shape, compile-time KD_ only): stages of KC_ k-steps, two per j-chunk, for
 // ranks whose whole-rank stage no longer fits the shared-memory ring (KD 24..30); the
 // accumulators persist across the two stages of a tile.
-template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8, int KD_ = 0, int NT_ = 1, int KC_ = 0>
+// NKC_ (with KC_ > 0): k-chunk stages per tile (the last one may be shorter).
+// SINGLE_ (16-warp shape, ranks beyond two A1k buffers: KD 31..62): ONE A1k buffer of up to 512
+// columns. The next unit's A1k is written at the unit boundary, each lane quarter as soon as its
+// own WJ warps are done with the unit, with all of the quarter's fill loads in flight at once;
+// the A2 ring keeps streaming the next unit's stages meanwhile.
+template <bool STORE, bool FUNC, int NS, int JPS, int WARPS_ = 8, int KD_ = 0, int NT_ = 1, int KC_ = 0,
+          int NKC_ = 2, bool SINGLE_ = false>
 __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_kernel(const ExpandArgs p) {
     constexpr int WARPS = WARPS_, WI = 4, WJ = WARPS / WI, kTM = 4, kTN = 4, IC = 128, JT = kTM * WJ * JPS,
                   JC = 8 * kTM * WJ, kNS = NS;
@@ -94,9 +100,12 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     constexpr int n_tail = NT_;  // 1 or 2 DFMA ranks (launch() makes a zero rank when R mod 4 is 0 or 3)
     const int CB = 8 * KD + 16 * n_tail;
     constexpr bool kChunked = KC_ > 0;
-    static_assert(!kChunked || (KD_ > KC_ && KD_ <= 2 * KC_ && JPS == 1), "k-chunked stages: two per tile");
+    constexpr bool SINGLE = SINGLE_;
+    static_assert(!kChunked || (KD_ > (NKC_ - 1) * KC_ && KD_ <= NKC_ * KC_ && JPS == 1),
+                  "k-chunked stages: NKC_ per tile");
+    static_assert(!SINGLE || (WARPS_ == 16 && kChunked), "single A1k buffer: 16-warp chunked shape");
     const int KCs = kChunked ? KC_ : KD;          // k-steps per stage
-    constexpr int n_kc = kChunked ? 2 : 1;        // stages per tile
+    constexpr int n_kc = kChunked ? NKC_ : 1;     // stages per tile
     const int frag_elems = JT * KCs * 32;
     const int stage_elems = frag_elems + JT * 8 * n_tail;
     const int n_ichunks = static_cast<int>(p.n_ichunks);
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         }
         cp_async_commit();
     };
-    const int n_seq = (my_units - 1) * n_tasks;  // fill tasks after the prologue's unit
+    const int n_seq = SINGLE ? 0 : (my_units - 1) * n_tasks;  // fill tasks after the prologue's unit
     int n_issued = 0;                             // cp.async groups committed (one per task)
     auto seq_issue = [&](int e) {
         if (e >= n_seq) return;
@@ -280,17 +289,18 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
     // The first ring stages load while the warps build the first unit's A1k.
     if (threadIdx.x == 0)
         for (int st = 0; st < kNS && st < n_stages; ++st) issue(st);
-    // Prologue: the first unit's A1k (buffer 0), all tasks now, with the global loads of up to
-    // four tasks in flight at once (no accumulators are live yet, so the registers are free);
-    // then the copy for the next unit's first task starts the one-ahead chain.
-    if (my_units > 0) {
-        const int u = unit_of(0);
+    // Fill of a whole unit's A1k into buffer buf by this warp, with the global loads of
+    // kBatch tasks in flight at once (no accumulators are live here, so the registers are
+    // free): the prologue's first unit, and every unit boundary of the single-buffer shape.
+    constexpr int kBatch = 4;
+    auto fill_all = [&](int u, int buf) {
         const int ib = (u % n_ichunks) * IC;
         const int64_t k = p.k0 + u / n_ichunks;
-        for (int t0 = 0; t0 < n_tasks; t0 += 4) {
-            double av[4][4], sv[4];
+        const uint32_t col = static_cast<uint32_t>(buf * CB);
+        for (int t0 = 0; t0 < n_tasks; t0 += kBatch) {
+            double av[kBatch][4], sv[kBatch];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 0; b < kBatch; ++b) {
                 const int task = t0 + b;
                 if (task >= n_tasks) break;
                 if (task < n_frag_tasks) {
@@ -314,31 +324,38 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 }
             }
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 0; b < kBatch; ++b) {
                 const int task = t0 + b;
                 if (task >= n_tasks) break;
                 double v[4];
 #pragma unroll
                 for (int it = 0; it < 4; ++it) v[it] = rn_mul(av[b][it], sv[b]);
                 if (task < n_frag_tasks) {
-                    tmem::st_x8(tq + 8 * (wj + WJ * task), v);
+                    tmem::st_x8(tq + col + 8 * (wj + WJ * task), v);
                 } else {
                     const int ht = task - n_frag_tasks;
-                    tmem::st_x8(tq + 8 * KD + 16 * (ht >> 1) + 8 * (ht & 1), v);
+                    tmem::st_x8(tq + col + 8 * KD + 16 * (ht >> 1) + 8 * (ht & 1), v);
                 }
             }
         }
+    };
+    // Prologue: the first unit's A1k (buffer 0), all tasks now; then the copies for the next
+    // unit's first two tasks start the two-ahead chain.
+    if (my_units > 0) {
+        fill_all(unit_of(0), 0);
         seq_issue(0);
         seq_issue(1);
         publish(0);
     }
     LS_TL(2);  // prologue fill published
 
-    double acc[kTM][kTN][2];
     double fsum = 0.0;
     int st = 0;
     for (int n = 0; n < my_units; ++n) {
         const int unit = unit_of(n);
+        // A tile's accumulators live within the unit's stages only (dead at the unit boundary,
+        // where the single-buffer shape refills A1k with its loads in flight).
+        double acc[kTM][kTN][2];
         // j-chunk range of this unit (partial only for the first and last unit of a split tail)
         const int jc_lo = (kSplitTail && n == n_full) ? t0 % per_unit : 0;
         const int jc_hi = (kSplitTail && n >= n_full && n == my_units - 1) ? (t1 - 1) % per_unit + 1 : per_unit;
@@ -352,14 +369,14 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         const int n_here = jc_hi - jc_lo;
         const int first_fill = (WARPS == 16 && n_here > 2) ? 2 : 0;
         auto fill_stage = [&](int task) {
-            if (WARPS == 8) return jc_lo;
+            if (WARPS == 8 || SINGLE) return jc_lo;
             return jc_lo + first_fill + ((task * WARPS + warp) * (n_here - first_fill)) / (WARPS * n_tasks);
         };
-        const int buf = n & 1;
+        const int buf = SINGLE ? 0 : (n & 1);
         const bool has_next = n + 1 < my_units;
         const int ib = (unit % n_ichunks) * IC;
         const int64_t kk = unit / n_ichunks;
-        mbar_wait(as_full + 4 * buf + wi, static_cast<unsigned>((n >> 1) & 1), p.fault);
+        mbar_wait(as_full + 4 * buf + wi, static_cast<unsigned>((SINGLE ? n : n >> 1) & 1), p.fault);
         tmem::fence_after();
         LS_TL(3);  // unit's A1k ready
         const uint32_t tb = tq + static_cast<uint32_t>(buf * CB);
@@ -384,7 +401,7 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
             const int kc = kChunked ? w % n_kc : 0;  // k-chunk of this stage
             // Fill task(s) for the next unit: loads now, product + TMEM store after the DMMAs.
             int target = next_task;
-            if (has_next && !lab_nofill)
+            if (has_next && !lab_nofill && !SINGLE)
                 while (target < n_tasks && fill_stage(target) <= w) ++target;
             const bool fill_now = target > next_task;
             if (fill_now && next_task == 0 && n >= 1)  // this quarter of buffer buf^1 was read by unit n-1
@@ -441,12 +458,12 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                             for (int nn = 0; nn < kTN; ++nn) dmma_884(acc[m][nn][0], acc[m][nn][1], a[m], b[nn]);
                     };
                     if constexpr (kChunked) {
-                        if (kc == 0) {
 #pragma unroll
-                            for (int ks = 0; ks < KC_; ++ks) kstep(ks);
-                        } else {
+                        for (int c = 0; c < NKC_; ++c) {
+                            if (kc == c) {
 #pragma unroll
-                            for (int ks = KC_; ks < (KD_ > 0 ? KD_ : 1); ++ks) kstep(ks);
+                                for (int ks = c * KC_; ks < ((c + 1) * KC_ < KD_ ? (c + 1) * KC_ : KD_); ++ks) kstep(ks);
+                            }
                         }
                     } else if constexpr (KD_ > 0) {
                         // compile-time k-step count: fully unrolled (2.2% faster at cfg1 than the
@@ -548,7 +565,14 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
         tmem::fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(as_empty + 4 * buf + wi);
-        if (has_next && (n_tasks == 0 || lab_nofill)) publish(buf ^ 1);  // no fill share (KD = 1, wj = 1): still arrive
+        if (SINGLE) {
+            if (has_next) {  // the quarter's WJ warps are done with the one buffer: refill it
+                mbar_wait(as_empty + wi, static_cast<unsigned>(n & 1), p.fault);
+                tmem::fence_after();
+                fill_all(unit_of(n + 1), 0);
+                publish(0);
+            }
+        } else if (has_next && (n_tasks == 0 || lab_nofill)) publish(buf ^ 1);  // no fill share (KD = 1, wj = 1): still arrive
         else if (has_next && next_task < n_tasks) {  // tiny units: finish the fill now
             if (next_task == 0 && n >= 1)
                 mbar_wait(as_empty + 4 * (buf ^ 1) + wi, static_cast<unsigned>(((n - 1) >> 1) & 1), p.fault);

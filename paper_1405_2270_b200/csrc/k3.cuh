@@ -149,6 +149,17 @@ KernelFn tmem8_kernel(bool store, bool func, int code, int kd, int nt);
 // rank stages (kc == kd) and for KD 24..30 with two stages of kc = ceil(kd / 2) k-steps.
 KernelFn tmem16_kernel(bool store, bool func, int kd, int kc);
 
+// Single-buffer 16-warp TMEM kernel for KD 31..62 (expand_tmem16s_{a,b}.cu); nullptr outside.
+// k-chunks per tile: the fewest whose 2-deep ring of 16-j-tile stages fits next to the fill
+// staging in one CTA's shared memory (KD <= 46: two, else three).
+__host__ __device__ constexpr int tmem16s_nkc(int kd) { return kd <= 46 ? 2 : 3; }
+__host__ __device__ constexpr int tmem16s_kc(int kd) { return (kd + tmem16s_nkc(kd) - 1) / tmem16s_nkc(kd); }
+KernelFn tmem16s_kernel_a(bool store, bool func, int kd);
+KernelFn tmem16s_kernel_b(bool store, bool func, int kd);
+inline KernelFn tmem16s_kernel(bool store, bool func, int kd) {
+    return kd <= 45 ? tmem16s_kernel_a(store, func, kd) : tmem16s_kernel_b(store, func, kd);
+}
+
 // Split-K TMEM plan for ranks beyond the double-buffered TMEM plans (expand_splitk.cu).
 bool fits_splitk(int KD, int n_tail);
 int launch_splitk(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_count,

@@ -93,14 +93,14 @@ def test_device_work_without_a_gpu_fails_loudly():
 
 def test_expansion_plan_names():
     """Plan selection is host logic (no device needed): BASELINE rank 41 takes the 8-warp TMEM
-    kernel compiled for KD 10; 2-charge rank 82 the 16-warp TMEM one; 160 the smem plan; 164 and
-    cfg3's 328 the split-K TMEM plan."""
+    kernel compiled for KD 10; 2-charge rank 82 the 16-warp TMEM one; 122-160 the single-buffer
+    16-warp TMEM one; cfg3's 328 the split-K TMEM plan."""
     assert L.expansion_plan(41).startswith("expand_tmem_kernel, 8 warps x 2 CTAs/SM")
     assert "KD 10 (compiled)" in L.expansion_plan(41)
     assert L.expansion_plan(82).startswith("expand_tmem_kernel, 16 warps x 1 CTA/SM")
     assert "two stages per tile" in L.expansion_plan(113)
-    assert "TileLR16" in L.expansion_plan(160)
-    assert L.expansion_plan(164).startswith("expand_splitk_kernel")
+    assert "single A1k buffer" in L.expansion_plan(122)
+    assert "single A1k buffer" in L.expansion_plan(160)
     assert L.expansion_plan(328).startswith("expand_splitk_kernel")
     assert "256-rank chunks" in L.expansion_plan(600)
     with pytest.raises(L.ValidationError):
