@@ -277,8 +277,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.empty_cache()
 
     # e2e through the host-level C-ABI call: host rule/charges in, pinned host grid out.
+    e2e_energy = None
     if not args.step_only:
         e2e = run_e2e(L, spec, rule, k0, k1, args, world, dev)
+        if world == 1:
+            e2e_energy = run_e2e_energy(L, spec, rule, args)
 
     cpu = None
     if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.step_only):
@@ -300,6 +303,7 @@ def run_ours(args, rank, world, local_rank):
             "unit charge at each cell centre; quadrature rule computed on the host)",
             "config": workload_config(spec, world, rule), "roofline": roofline, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": cpu, "energy": energy,
+            "e2e_energy": e2e_energy,
             "other_configs": configs,
             "assembly_note": "generator + assembly are inside every step (replicated per rank)",
         }
@@ -571,6 +575,27 @@ def run_e2e(L, spec, rule, k0, k1, args, world, dev):
             "api": "ls_h_lattice_potential (host tau/w/charges in; full grid out to host memory; value = the "
                    "faster of a pinned destination and an ordinary numpy array, which goes through the "
                    "library's bounded 256 MiB pinned ring)"}
+
+
+def run_e2e_energy(L, spec, rule, args):
+    """The energy <V, rho> end to end through one host-level call (ls_h_lattice_energy): host
+    rule, charges and separable density in, the scalar out; every grid point is evaluated on
+    the device, fused with the reduction. Same Gpts/s metric; informational beside `e2e`, whose
+    result is the whole grid in host memory."""
+    N = spec.target_dims()
+    sigma = energy_sigma(spec)
+    rho = [np.exp(-((np.arange(N[l]) + 0.5 - N[l] / 2.0) * spec.unit.h) ** 2 / (2 * sigma * sigma)) for l in range(3)]
+    L.lattice_energy(spec, rule, rho)  # warm-up
+    steps = max(3, min(args.steps, 20))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        e = L.lattice_energy(spec, rule, rho)
+    el = (time.perf_counter() - t0) / steps
+    pts = float(N[0]) * N[1] * N[2]
+    h2d = 8 * (2 * rule.node_count() + 4 * spec.charge_count() + sum(N))
+    return {"value": round(pts / el / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8,
+            "steps": steps, "energy": e, "ms": round(el * 1e3, 3),
+            "api": "lattice_energy -> ls_h_lattice_energy (host rule/charges/rho in, scalar out; host-timed)"}
 
 
 # ---------------------------------------------------------------- CPU reference

@@ -311,6 +311,14 @@ int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, co
                            int64_t k0, int64_t k1, double* grid_h, double* f0_h, double* f1_h,
                            double* f2_h, double* wout_h);
 
+/* End-to-end energy (BASELINE configs[2]'s functional): the same generator and assembled sum,
+ * then <V, rho> over slabs [k0, k1) for the separable density rho = r1 (x) r2 (x) r3 (host
+ * vectors of the full axis lengths), fused into the expansion so V never leaves the device;
+ * energy_h (host) receives the fixed-order sum. Inputs are host memory. */
+int ls_h_lattice_energy(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h, const double* w_h,
+                        int R, const double* charges_h, int M0, int periodic, int64_t k0, int64_t k1,
+                        const double* r1_h, const double* r2_h, const double* r3_h, double* energy_h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,6 +95,7 @@ SIGNATURES = {
     "ls_h_grid_functional": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]),
     "ls_h_lattice_potential": (_i, [_i, _vp, _i64, _d, _vp, _vp, _i, _vp, _i, _i, _i64, _i64, _vp, _vp, _vp, _vp,
                                     _vp]),
+    "ls_h_lattice_energy": (_i, [_i, _vp, _i64, _d, _vp, _vp, _i, _vp, _i, _i, _i64, _i64, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

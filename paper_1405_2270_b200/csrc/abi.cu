@@ -822,10 +822,16 @@ int ls_h_grid_functional(const int64_t dims[3], int R, const double* A_h, const 
     return LS_OK;
 }
 
-int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h,
-                           const double* w_h, int R, const double* charges_h, int M0, int periodic,
-                           int64_t k0, int64_t k1, double* grid_h, double* f0_h, double* f1_h,
-                           double* f2_h, double* wout_h) {
+}  // extern "C"
+
+namespace {
+// Generator -> assembled sum on the device, then either the expansion of slabs [k0, k1) into
+// host memory (grid_h) or the fused full-grid functional of those slabs against the separable
+// density rho_h (energy_h); the host-level entry points below.
+int lattice_impl(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h, const double* w_h, int R,
+                 const double* charges_h, int M0, int periodic, int64_t k0, int64_t k1, double* grid_h,
+                 double* f0_h, double* f1_h, double* f2_h, double* wout_h, const double* const* rho_h,
+                 double* energy_h) {
     // LatticeSpec::validate + charge snapping (lattice.hpp:33-68), then weights Z_nu * w_q
     // (lattice.hpp:284-287), on the host.
     std::vector<int64_t> ia(static_cast<size_t>(3 * std::max(M0, 0)));
@@ -870,12 +876,46 @@ int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, co
     for (int l = 0; l < 3; ++l)
         if (fh[l]) LS_CUDA(cudaMemcpyAsync(fh[l], fptr[l], sizeof(double) * d[l] * Rt, cudaMemcpyDeviceToHost, s));
     if (wout_h) std::memcpy(wout_h, wt.data(), sizeof(double) * wt.size());
-    if (grid_h) {
+    if (energy_h) {
+        // <V, rho> over slabs [k0, k1) fused into the expansion (V never stored), fixed-order sum.
+        DevBuf rho[3], part, out;
+        for (int l = 0; l < 3; ++l) LS_TRY(ls::upload(rho[l], rho_h[l], sizeof(double) * d[l], s));
+        const int64_t np = ls_expand_partial_count(d[0], d[1], Rt, k0, k1);
+        if (np < 0) return ls::fail(LS_EGUARD, "lattice energy: no tile plan for this rank");
+        LS_TRY(part.alloc(sizeof(double) * std::max<int64_t>(np, 1), s));
+        LS_TRY(out.alloc(sizeof(double), s));
+        LS_CUDA(cudaMemsetAsync(part.p, 0, sizeof(double) * std::max<int64_t>(np, 1), s));
+        LS_TRY(ls_expand(fptr[0], d[0], fptr[1], d[1], fptr[2], d[2], wd.d(), d[0], d[1], d[2], Rt, k0, k1, nullptr,
+                         0, 0, rho[0].d(), rho[1].d(), rho[2].d(), part.d(), s));
+        LS_TRY(ls_sum_partials(part.d(), np, out.d(), s));
+        LS_CUDA(cudaMemcpyAsync(energy_h, out.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+        LS_SYNC(s);
+    } else if (grid_h) {
         LS_TRY(ls::expand_to_host(fptr[0], fptr[1], fptr[2], wd.d(), d, Rt, k0, k1, grid_h, *st));
     } else {
         LS_SYNC(s);
     }
     return LS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h,
+                           const double* w_h, int R, const double* charges_h, int M0, int periodic,
+                           int64_t k0, int64_t k1, double* grid_h, double* f0_h, double* f1_h,
+                           double* f2_h, double* wout_h) {
+    return lattice_impl(mode, L, n, b, tau_h, w_h, R, charges_h, M0, periodic, k0, k1, grid_h, f0_h, f1_h, f2_h,
+                        wout_h, nullptr, nullptr);
+}
+
+int ls_h_lattice_energy(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h, const double* w_h,
+                        int R, const double* charges_h, int M0, int periodic, int64_t k0, int64_t k1,
+                        const double* r1_h, const double* r2_h, const double* r3_h, double* energy_h) {
+    if (!r1_h || !r2_h || !r3_h || !energy_h) return ls::fail(LS_EVALIDATION, "lattice energy: null density or output");
+    const double* rho[3] = {r1_h, r2_h, r3_h};
+    return lattice_impl(mode, L, n, b, tau_h, w_h, R, charges_h, M0, periodic, k0, k1, nullptr, nullptr, nullptr,
+                        nullptr, nullptr, rho, energy_h);
 }
 
 }  // extern "C"

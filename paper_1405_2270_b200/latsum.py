@@ -485,6 +485,28 @@ def lattice_potential(spec: LatticeSpec, rule: QuadratureRule, mode: str = "erf"
     return out
 
 
+def lattice_energy(spec: LatticeSpec, rule: QuadratureRule, rho: Sequence[np.ndarray], mode: str = "erf",
+                   periodic: bool = False, k0: int = 0, k1: int | None = None) -> float:
+    """End-to-end <V, rho> (BASELINE configs[2]'s energy) in one C-ABI call
+    (ls_h_lattice_energy): host rule, charges and separable density in, the scalar out; the
+    grid is evaluated point by point on the device, fused with the reduction, and never stored."""
+    spec.validate()
+    n = spec.unit.n
+    dims = (n, n, n) if periodic else spec.target_dims()
+    k1 = dims[2] if k1 is None else k1
+    if not (0 <= k0 <= k1 <= dims[2]):
+        raise ValidationError("lattice_energy: slab range outside [0, N3]")
+    r = [_f64(x).ravel() for x in rho]
+    _check_lengths(r, dims, "lattice_energy")
+    ch = np.array([[*c.pos, c.Z] for c in spec.charges], dtype=np.float64)
+    L = np.array(spec.L, dtype=np.int64)
+    out = np.zeros(1)
+    call("ls_h_lattice_energy", MODES[mode], _p(L), n, spec.unit.b, _p(_f64(rule.exponents).ravel()),
+         _p(_f64(rule.weights).ravel()), rule.node_count(), _p(ch), spec.charge_count(), int(periodic), k0, k1,
+         _p(r[0]), _p(r[1]), _p(r[2]), _p(out))
+    return float(out[0])
+
+
 # ----------------------------------------------------------------- project.hpp
 @dataclass
 class GaussianBasisSpec:

@@ -755,3 +755,20 @@ def test_watchdog_clear_and_product_build(L):
     spec, rule = cfg(L, 2, n=8)
     L.lattice_potential(spec, rule)
     assert lib.ls_fault_status(0) == 0
+
+
+@pytest.mark.parametrize("Lc,periodic", [(4, False), (16, False), (64, True)])
+def test_lattice_energy_end_to_end(L, orc, Lc, periodic):
+    """ls_h_lattice_energy (host inputs, scalar out, V never stored) against the 1D rank-term form
+    of the oracle's own assembled tensor (scalar_product, canonical.hpp:126-136)."""
+    n = 256 if periodic else 64
+    spec, rule = cfg(L, Lc, n=n)
+    N = (n,) * 3 if periodic else spec.target_dims()
+    sigma = (spec.unit.b if periodic else Lc * spec.unit.b) / 4
+    rho = [np.exp(-((np.arange(N[l]) + 0.5 - N[l] / 2) * spec.unit.h) ** 2 / (2 * sigma ** 2)) for l in range(3)]
+    e = L.lattice_energy(spec, rule, rho, periodic=periodic)
+    _, fo, wo = oracle_assembled(orc, spec, rule, "erf", periodic)
+    want = orc.scalar_product(fo, wo, [np.asfortranarray(r.reshape(-1, 1)) for r in rho], np.ones(1))
+    assert abs(e - want) <= 1e-12 * abs(want)
+    with pytest.raises(L.ValidationError):
+        L.lattice_energy(spec, rule, [rho[0], rho[1], rho[2][:-1]], periodic=periodic)
