@@ -738,22 +738,30 @@ int launch_plan(const Plan& pl, ExpandArgs& a, cudaStream_t s) {
     }
 }
 
-}  // namespace
-
 #ifdef LS_TIMELINE
+}  // namespace
 extern "C" int ls_lab_timeline(unsigned long long* host, int64_t n) {
     const size_t bytes = std::min<size_t>(kLabTimelineBytes, size_t(n) * sizeof(unsigned long long));
     LS_CUDA(cudaMemcpy(host, lab_timeline(), bytes, cudaMemcpyDeviceToHost));
     return LS_OK;
 }
+namespace {
 #endif
 
+// The small-N2 plan (expand_a2t.cu) takes a launch whenever it fits: A2 in TMEM for the whole
+// launch, no per-unit fill, 64-row units (256^3: 56.3 -> see DESIGN section 3).
+bool use_a2t(int64_t N2, int KD, int n_tail) {
+    return fits_a2t(N2, KD, tmem_tail(n_tail)) && !ls::dev_knob("LS_NO_A2T");
+}
+
+}  // namespace
+
 extern "C" int64_t ls_expand_partial_count(int64_t N1, int64_t N2, int R, int64_t k0, int64_t k1) {
-    (void)N2;
     int KD, n_tail;
     split_rank(std::max(R, 1), KD, n_tail);
     Plan pl;
     if (k1 < k0) return -1;
+    if (use_a2t(N2, KD, n_tail)) return a2t_units(N1, k0, k1) * 8;  // one partial per warp and unit
     if (!plan_for(KD, n_tail, pl) && !chunk_plan(pl)) return -1;
     const int64_t IC = pl.ic;
     // the TMEM variant writes one partial per warp (no CTA barrier per unit)
@@ -832,6 +840,10 @@ extern "C" int ls_expand(const double* A_d, int64_t lda, const double* B_d, int6
     }
 #endif
     const bool store = out_d != nullptr;
+    if (use_a2t(N2, a.KD, a.n_tail)) {
+        a.n_tail = tmem_tail(a.n_tail);
+        return launch_a2t(a, store, func, s, ls::sm_count(), kernel_setup);
+    }
     Plan pl;
     if (plan_for(a.KD, a.n_tail, pl)) {
         if (store && func) return launch_plan<true, true>(pl, a, s);

@@ -1,0 +1,368 @@
+// expand_a2t.cu -- K3 for small N2: the right factor A2 resident in TMEM for the whole launch,
+// the scaled left factor A1k streamed through the shared-memory ring.
+//
+// The TMEM kernels (expand_tmem.cuh) keep A1k(i, q) = A1(i, q) * S(k, q) of one (i-chunk, slab)
+// unit in TMEM and stream A2 through the ring; each unit's A1k is rebuilt by the warps (loads,
+// products, TMEM stores). With N2 = 256 a unit is only 4 ring stages, so that fill is ~10% of the
+// time, and the 512 units of a 256^3 grid on 296 CTAs leave the SMs with 4 units setting the
+// pace. Here the roles swap: all of A2 (N2 <= 256 at ranks <= 57) sits in TMEM, loaded once per
+// CTA, and a unit is a 64-row i-chunk of ONE slab. Its operand stage is the i-chunk's A1 in
+// MMA-fragment order (a pre-pass packs the few distinct i-chunks once, pack_a1_kernel) plus the
+// slab's scale row S(k, q) = w_q * A3(k, q): two TMA bulk copies per unit, both L2-resident.
+// Each k-step forms A1k = A1 * S in registers (four DMULs, the rounding of the TMEM kernel's
+// fill), so there is no per-unit fill, the units are half as large (1024 at 256^3: 6.9 per SM,
+// at most 7), and the DMMAs see exactly the operands of the TMEM kernel in the same order: the
+// grid is bit-identical to it.
+//
+// TMEM layout (per CTA, 256 columns, lanes = quarter wj = warp & 3 = the warp's j block):
+//   chunk c (128 j), column c*CBJ + 8 ks + 2 m + {0,1}: A2(j = 128 c + 32 wj + 8 m + g, q = 4 ks + t)
+//   column c*CBJ + 8 KD + 8 qt + 2 m + {0,1}: A2(j = ..., q = 4 KD + qt) (DFMA tail ranks)
+//   CBJ = 8 KD + 8 NT; n_jc chunks need n_jc * CBJ <= 256.
+// Ring slot (per unit (ic, k), shared memory): the i-chunk's packed A1
+//   [wi][ks][nn][lane] = A1(i = 64 ic + 32 wi + 8 nn + g, q = 4 ks + t), then
+//   [wi][qt][e][lane]  = A1(i = 64 ic + 32 wi + 8 (e >> 1) + 2 t + (e & 1), q = 4 KD + qt),
+// then the scale row S(k, 0 .. SR) (zero beyond R).
+#include <utility>
+
+#include "common.cuh"
+#include "expand_tmem.cuh"
+
+namespace ls_k3 {
+namespace {
+
+constexpr int kA2tWarps = 8, kA2tIC = 64, kA2tJC = 128, kA2tNS = 4, kA2tHdr = 32;
+
+__host__ __device__ constexpr int a2t_stage_elems(int KD, int NT) { return 2 * KD * 128 + 2 * NT * 256; }
+// scale-row length, padded to whole 16-byte TMA chunks
+__host__ __device__ constexpr int a2t_srow(int KD, int NT) { return (4 * KD + NT + 1) / 2 * 2; }
+
+// Pre-pass: the packed A1 of every 64-row i-chunk (n_ichunks stages, MMA-fragment order), and
+// the scale rows S[kk][q] = w_q * A3(k0 + kk, q) of slabs [k0, k1) (pack_b_kernel's rounding),
+// zero beyond R. Small: at 256^3 four stages of 24 KB and 256 rows of 42 doubles.
+__global__ void pack_a1_kernel(const double* __restrict__ A, int64_t lda, int64_t N1, const double* __restrict__ w,
+                               const double* __restrict__ C, int64_t ldc, int R, int KD, int NT, int64_t k0,
+                               int64_t n_slabs, int64_t n_ichunks, double* __restrict__ a1p, double* __restrict__ srows) {
+    pdl_wait();  // A, C, w may come from the preceding assembly / generator launches
+    pdl_trigger();
+    const int se = a2t_stage_elems(KD, NT), frag = 2 * KD * 128, sr = a2t_srow(KD, NT);
+    const int64_t n_a = n_ichunks * se, n_s = n_slabs * sr;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_a + n_s; x += (int64_t)gridDim.x * blockDim.x) {
+        if (x >= n_a) {
+            const int64_t y = x - n_a, kk = y / sr;
+            const int q = static_cast<int>(y - kk * sr);
+            srows[y] = q < R ? rn_mul(w[q], C[k0 + kk + ldc * q]) : 0.0;
+            continue;
+        }
+        const int64_t ic = x / se;
+        const int o = static_cast<int>(x - ic * se), r = o >> 5, lane = o & 31, g = lane >> 2, t = lane & 3;
+        int64_t i;
+        int q;
+        if (o < frag) {  // r = (wi * KD + ks) * 4 + nn
+            const int nn = r & 3, wk = r >> 2, wi = wk / KD, ks = wk - wi * KD;
+            i = kA2tIC * ic + 32 * wi + 8 * nn + g;
+            q = 4 * ks + t;
+        } else {  // r - frag / 32 = (wi * NT + qt) * 8 + e
+            const int rr = r - (frag >> 5), e = rr & 7, wq = rr >> 3, wi = wq / NT, qt = wq - wi * NT;
+            i = kA2tIC * ic + 32 * wi + 8 * (e >> 1) + 2 * t + (e & 1);
+            q = 4 * KD + qt;
+        }
+        a1p[x] = (i < N1 && q < R) ? A[i + lda * q] : 0.0;
+    }
+}
+
+template <bool STORE, bool FUNC, int KD, int NT>
+__global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const ExpandArgs p) {
+    constexpr int kThreads = kA2tWarps * 32, kNS = kA2tNS, kTM = 4, kTN = 4;
+    constexpr int CBJ = 8 * KD + 8 * NT;
+    constexpr int kA1 = a2t_stage_elems(KD, NT), kSR = a2t_srow(KD, NT);
+    constexpr int kStage = kA1 + kSR;  // ring slot: packed A1 of the unit's i-chunk, then its slab's scale row
+    constexpr int kFrag = 2 * KD * 128;
+    constexpr unsigned kA1Bytes = kA1 * sizeof(double), kSRBytes = kSR * sizeof(double);
+    extern __shared__ __align__(128) double smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // [kNS]
+    int* released = reinterpret_cast<int*>(smem + 8);           // [kNS]
+    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 16);
+    double* ring = smem + kA2tHdr;                              // [kNS][kStage]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int wj = warp & 3;   // j block within a 128-j chunk, and the TMEM lane quarter
+    const int wi = warp >> 2;  // i half of the 64-row unit
+    const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+    const int n_units = static_cast<int>(p.n_units), n_ichunks = static_cast<int>(p.n_ichunks);
+    const int n_jc = static_cast<int>(p.n_jc);
+    const int my_units = n_units > b ? (n_units - 1 - b) / G + 1 : 0;
+
+    auto issue = [&](int n) {  // this CTA's n-th unit into slot n % kNS
+        const int u = b + n * G;
+        uint64_t* bar = full + (n % kNS);
+        double* dst = ring + (n % kNS) * kStage;
+        mbar_arrive_expect_tx(bar, kA1Bytes + kSRBytes);
+        tma_bulk_g2s(dst, p.Bp + static_cast<int64_t>(u % n_ichunks) * kA1, kA1Bytes, bar);
+        tma_bulk_g2s(dst + kA1, p.S + static_cast<int64_t>(u / n_ichunks) * kSR, kSRBytes, bar);
+    };
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_s)),
+                     "r"(256)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kNS; ++s) {
+            mbar_init(full + s, 1);
+            released[s] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    pdl_wait();  // the packed A1k (pre-pass) and A2 come from the preceding launches
+    if (threadIdx.x == 0)
+        for (int n = 0; n < kNS && n < my_units; ++n) issue(n);
+    const uint32_t tq = *tmem_base_s + (static_cast<uint32_t>(32 * wj) << 16);
+
+    // A2 into TMEM, once: the two warps of quarter wj split the chunks (c = wi, wi + 2, ...);
+    // loads of four k-steps in flight at a time.
+    for (int c = wi; c < n_jc; c += 2) {
+        const int64_t jb = static_cast<int64_t>(kA2tJC) * c + 32 * wj + g;
+        for (int ks0 = 0; ks0 < KD + NT; ks0 += 4) {
+            double v[4][4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const int ks = ks0 + x;
+                if (ks >= KD + NT) break;
+                const int q = ks < KD ? 4 * ks + t : 4 * KD + (ks - KD);  // tail ranks: every t the same q
+#pragma unroll
+                for (int m = 0; m < kTM; ++m) {
+                    const int64_t j = jb + 8 * m;
+                    v[x][m] = (j < p.N2 && q < p.R) ? __ldg(p.B + j + p.ldb * q) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const int ks = ks0 + x;
+                if (ks >= KD + NT) break;
+                tmem::st_x8(tq + static_cast<uint32_t>(c * CBJ + 8 * ks), v[x]);
+            }
+        }
+    }
+    tmem::wait_st();
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+
+    double fsum = 0.0;
+    for (int n = 0; n < my_units; ++n) {
+        const int unit = b + n * G;
+        const int ic = unit % n_ichunks;
+        const int64_t kk = unit / n_ichunks;
+        const int slot = n % kNS;
+        mbar_wait(full + slot, static_cast<unsigned>((n / kNS) & 1), p.fault);
+        const double* stage = ring + slot * kStage;
+        const double* bfr = stage + (wi * KD) * 128 + lane;             // A1 of k-step ks at [ks * 128 + nn * 32]
+        const double* btl = stage + kFrag + (wi * NT) * 256 + lane;     // tail A1: [qt * 256 + e * 32]
+        const double* srow = stage + kA1;                               // S(k, q)
+        const int ibase = kA2tIC * ic + 32 * wi;
+        double r1[kTN][2];
+        if (FUNC) {
+            fsum = 0.0;
+#pragma unroll
+            for (int nn = 0; nn < kTN; ++nn)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = ibase + 8 * nn + 2 * t + e;
+                    r1[nn][e] = i < p.N1 ? __ldg(p.rho1 + i) : 0.0;
+                }
+        }
+        for (int c = 0; c < n_jc; ++c) {
+            const uint32_t ta = tq + static_cast<uint32_t>(c * CBJ);
+            double acc[kTM][kTN][2];
+#pragma unroll
+            for (int m = 0; m < kTM; ++m)
+#pragma unroll
+                for (int nn = 0; nn < kTN; ++nn) acc[m][nn][0] = acc[m][nn][1] = 0.0;
+            // Rank remainder on DFMA before the DMMAs (as in the TMEM kernel).
+#pragma unroll
+            for (int qt = 0; qt < NT; ++qt) {
+                double at[4];
+                tmem::ld_x8(ta + 8 * KD + 8 * qt, at);  // A2 tail, j = 8 m + g
+                double bt[8];
+                const double st = srow[4 * KD + qt];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) bt[e] = rn_mul(btl[qt * 256 + e * 32], st);  // A1k tail, i = 8 (e >> 1) + 2 t + (e & 1)
+#pragma unroll
+                for (int nn = 0; nn < kTN; ++nn)
+#pragma unroll
+                    for (int m = 0; m < kTM; ++m) {
+                        acc[m][nn][0] = fma(bt[2 * nn], at[m], acc[m][nn][0]);
+                        acc[m][nn][1] = fma(bt[2 * nn + 1], at[m], acc[m][nn][1]);
+                    }
+            }
+#pragma unroll
+            for (int ks = 0; ks < KD; ++ks) {
+                uint32_t ra[8];
+                double a[kTM], bb[kTN];
+                tmem::ld_x8_issue(ta + 8 * ks, ra);
+                const double sq = srow[4 * ks + t];
+#pragma unroll
+                for (int nn = 0; nn < kTN; ++nn) bb[nn] = rn_mul(bfr[ks * 128 + nn * 32], sq);  // A1k = A1 * S
+                tmem::wait_ld(ra);
+                tmem::unpack(ra, a);
+#pragma unroll
+                for (int m = 0; m < kTM; ++m)
+#pragma unroll
+                    for (int nn = 0; nn < kTN; ++nn) dmma_884(acc[m][nn][0], acc[m][nn][1], a[m], bb[nn]);
+            }
+            if (c == n_jc - 1) {
+                // Release the ring slot (every operand of this unit has been read into registers);
+                // the last warp refills it with this CTA's unit n + kNS.
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    if (atomicAdd(released + slot, 1) == kA2tWarps - 1) {
+                        released[slot] = 0;
+                        __threadfence_block();
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        if (n + kNS < my_units) issue(n + kNS);
+                    }
+                }
+            }
+            // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
+            const int jb = kA2tJC * c + 32 * wj;
+            if (ibase + 8 * kTN <= p.N1 && jb + 8 * kTM <= p.N2 && (!STORE || (p.vec_store && !p.accumulate))) {
+                double* row = STORE ? p.out + kk * p.ldz + static_cast<int64_t>(jb + g) * p.ldy + ibase + 2 * t : nullptr;
+#pragma unroll
+                for (int m = 0; m < kTM; ++m) {
+                    if (FUNC) {
+                        double sm = 0.0;
+#pragma unroll
+                        for (int nn = 0; nn < kTN; ++nn) {
+                            sm = fma(acc[m][nn][0], r1[nn][0], sm);
+                            sm = fma(acc[m][nn][1], r1[nn][1], sm);
+                        }
+                        fsum = fma(sm, __ldg(p.rho2 + jb + 8 * m + g), fsum);
+                    }
+                    if (STORE)
+#pragma unroll
+                        for (int nn = 0; nn < kTN; ++nn)
+                            __stcs(reinterpret_cast<double2*>(row + 8 * m * p.ldy + 8 * nn),
+                                   make_double2(acc[m][nn][0], acc[m][nn][1]));
+                }
+                continue;
+            }
+#pragma unroll
+            for (int m = 0; m < kTM; ++m) {
+                const int j = jb + 8 * m + g;
+                if (j >= p.N2) continue;
+                if (FUNC) {
+                    double sm = 0.0;
+#pragma unroll
+                    for (int nn = 0; nn < kTN; ++nn) {
+                        sm = fma(acc[m][nn][0], r1[nn][0], sm);
+                        sm = fma(acc[m][nn][1], r1[nn][1], sm);
+                    }
+                    fsum = fma(sm, __ldg(p.rho2 + j), fsum);
+                }
+                if (!STORE) continue;
+                double* row = p.out + kk * p.ldz + static_cast<int64_t>(j) * p.ldy;
+#pragma unroll
+                for (int nn = 0; nn < kTN; ++nn) {
+                    const int i = ibase + 8 * nn + 2 * t;
+                    if (i + 1 < p.N1) {
+                        if (p.accumulate) {
+                            row[i] += acc[m][nn][0];
+                            row[i + 1] += acc[m][nn][1];
+                        } else if (p.vec_store) {
+                            __stcs(reinterpret_cast<double2*>(row + i), make_double2(acc[m][nn][0], acc[m][nn][1]));
+                        } else {
+                            row[i] = acc[m][nn][0];
+                            row[i + 1] = acc[m][nn][1];
+                        }
+                    } else if (i < p.N1) {
+                        row[i] = p.accumulate ? row[i] + acc[m][nn][0] : acc[m][nn][0];
+                    }
+                }
+            }
+        }
+        if (FUNC) {
+            // Per-warp partials: partial[unit * 8 + warp], fixed-order xor tree (as the TMEM kernel).
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, off);
+            if (lane == 0) {
+                const double part = rn_mul(fsum, p.rho3[p.k0 + kk]);
+                double& sl = p.partial[static_cast<int64_t>(unit) * kA2tWarps + warp];
+                sl = p.accumulate ? sl + part : part;
+            }
+        }
+    }
+    tmem::fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_s), "r"(256) : "memory");
+}
+
+template <bool STORE, bool FUNC, int NT, int... KD>
+KernelFn pick(int kd, std::integer_sequence<int, KD...>) {
+    KernelFn k = nullptr;
+    ((kd == KD + 1 ? (k = expand_a2t_kernel<STORE, FUNC, KD + 1, NT>, 0) : 0), ...);
+    return k;
+}
+
+template <bool STORE, bool FUNC>
+KernelFn a2t_kernel(int kd, int nt) {
+    using S = std::make_integer_sequence<int, 14>;
+    return nt == 1 ? pick<STORE, FUNC, 1>(kd, S{}) : nt == 2 ? pick<STORE, FUNC, 2>(kd, S{}) : nullptr;
+}
+
+}  // namespace
+
+int a2t_smem_bytes(int KD, int NT) {
+    return static_cast<int>(sizeof(double)) * (kA2tHdr + kA2tNS * (a2t_stage_elems(KD, NT) + a2t_srow(KD, NT)));
+}
+
+bool fits_a2t(int64_t N2, int KD, int NT) {
+    if (KD < 1 || KD > 14 || NT < 1 || NT > 2) return false;
+    const int64_t n_jc = (N2 + kA2tJC - 1) / kA2tJC;
+    return n_jc * (8 * KD + 8 * NT) <= 256 && 2 * (a2t_smem_bytes(KD, NT) + 1024) <= 228 * 1024;
+}
+
+int64_t a2t_units(int64_t N1, int64_t k0, int64_t k1) { return (N1 + kA2tIC - 1) / kA2tIC * (k1 - k0); }
+
+// Launch for slabs [a.k0, a.k1): the pre-pass (packed A1 + scale rows), then the expansion.
+// a.KD / a.n_tail are the plan's (n_tail in {1, 2}; q >= R is a zero rank).
+int launch_a2t(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_count,
+               int (*setup)(const void*, int, size_t, int&)) {
+    const int KD = a.KD, NT = a.n_tail;
+    KernelFn kern = store && func ? a2t_kernel<true, true>(KD, NT)
+                    : store       ? a2t_kernel<true, false>(KD, NT)
+                                  : a2t_kernel<false, true>(KD, NT);
+    if (!kern) return ls::fail(LS_EVALIDATION, "expand: unsupported A2-in-TMEM shape");
+    const size_t smem = static_cast<size_t>(a2t_smem_bytes(KD, NT));
+    int per_sm = 0;
+    if (const int rc = setup(reinterpret_cast<const void*>(kern), kA2tWarps * 32, smem, per_sm)) return rc;
+    const int64_t se = a2t_stage_elems(KD, NT), sr = a2t_srow(KD, NT);
+    a.n_ichunks = (a.N1 + kA2tIC - 1) / kA2tIC;
+    a.n_units = a.n_ichunks * (a.k1 - a.k0);
+    a.n_jc = (a.N2 + kA2tJC - 1) / kA2tJC;
+    if (a.n_units >= (int64_t(1) << 31)) return ls::fail(LS_EGUARD, "expand: grid too large for one launch");
+    ls::ensure_pool();
+    ls::AsyncScratch scratch(s);
+    const int64_t n_a = a.n_ichunks * se, n_s = (a.k1 - a.k0) * sr;
+    LS_CUDA(scratch.alloc(sizeof(double) * (n_a + n_s)));
+    double* a1p = scratch.as<double>();
+    double* srows = a1p + n_a;
+    const int64_t pb = std::min<int64_t>((n_a + n_s + 255) / 256, 4096);
+    LS_CUDA(ls::launch_pdl(pack_a1_kernel, dim3((unsigned)pb), dim3(256), 0, s, a.A, a.lda, a.N1, a.w, a.C, a.ldc,
+                           a.R, KD, NT, a.k0, a.k1 - a.k0, a.n_ichunks, a1p, srows));
+    LS_LAUNCHED("pack_a1_kernel");
+    a.Bp = a1p;
+    a.S = srows;
+    const int64_t grid = std::min<int64_t>(a.n_units, static_cast<int64_t>(sm_count) * 2);
+    if (grid > 0) {
+        LS_CUDA(ls::launch_pdl(kern, dim3((unsigned)grid), dim3(kA2tWarps * 32), smem, s, a));
+        LS_LAUNCHED("expand_a2t_kernel");
+    }
+    return LS_OK;
+}
+
+}  // namespace ls_k3

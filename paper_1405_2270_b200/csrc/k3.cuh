@@ -160,6 +160,13 @@ inline KernelFn tmem16s_kernel(bool store, bool func, int kd) {
     return kd <= 45 ? tmem16s_kernel_a(store, func, kd) : tmem16s_kernel_b(store, func, kd);
 }
 
+// Small-N2 plan (expand_a2t.cu): A2 resident in TMEM, A1k of 64-row units streamed by TMA from
+// a pre-pass; for N2 <= 256 at ranks <= 57.
+bool fits_a2t(int64_t N2, int KD, int NT);
+int64_t a2t_units(int64_t N1, int64_t k0, int64_t k1);
+int launch_a2t(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_count,
+               int (*setup)(const void*, int, size_t, int&));
+
 // Split-K TMEM plan for ranks beyond the double-buffered TMEM plans (expand_splitk.cu).
 bool fits_splitk(int KD, int n_tail);
 int launch_splitk(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_count,
