@@ -9,10 +9,12 @@
 // CTA, and a unit is a 64-row i-chunk of ONE slab. Its operand stage is the i-chunk's A1 in
 // MMA-fragment order (a pre-pass packs the few distinct i-chunks once, pack_a1_kernel) plus the
 // slab's scale row S(k, q) = w_q * A3(k, q): two TMA bulk copies per unit, both L2-resident.
-// Each k-step forms A1k = A1 * S in registers (four DMULs, the rounding of the TMEM kernel's
-// fill), so there is no per-unit fill, the units are half as large (1024 at 256^3: 6.9 per SM,
-// at most 7), and the DMMAs see exactly the operands of the TMEM kernel in the same order: the
-// grid is bit-identical to it.
+// The landed A1 is scaled in place once (A1k = A1 * S, the rounding of the TMEM kernel's fill),
+// each warp of a 64-row half scaling one quarter of it (its nn = wj rows), handed over by a
+// per-(slot, half) mbarrier, and the next unit's share is scaled while the first j-chunk's DMMAs
+// drain. So there is no per-unit TMEM fill, the units are half as large (1024 at 256^3: 6.9 per
+// SM, at most 7), and the DMMAs see exactly the operands of the TMEM kernel in the same order:
+// the grid is bit-identical to it.
 //
 // TMEM layout (per CTA, 256 columns, lanes = quarter wj = warp & 3 = the warp's j block):
 //   chunk c (128 j), column c*CBJ + 8 ks + 2 m + {0,1}: A2(j = 128 c + 32 wj + 8 m + g, q = 4 ks + t)
@@ -82,6 +84,7 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // [kNS]
     int* released = reinterpret_cast<int*>(smem + 8);           // [kNS]
     uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 16);
+    uint64_t* scaled = reinterpret_cast<uint64_t*>(smem + 20);  // [kNS][2]: slot's half scaled by its 4 warps
     double* ring = smem + kA2tHdr;                              // [kNS][kStage]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -109,6 +112,8 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
     if (threadIdx.x == 0) {
         for (int s = 0; s < kNS; ++s) {
             mbar_init(full + s, 1);
+            mbar_init(scaled + 2 * s, 4);
+            mbar_init(scaled + 2 * s + 1, 4);
             released[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -116,9 +121,6 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
     tmem::fence_before();
     __syncthreads();
     tmem::fence_after();
-    pdl_wait();  // the packed A1k (pre-pass) and A2 come from the preceding launches
-    if (threadIdx.x == 0)
-        for (int n = 0; n < kNS && n < my_units; ++n) issue(n);
     const uint32_t tq = *tmem_base_s + (static_cast<uint32_t>(32 * wj) << 16);
 
     // A2 into TMEM, once: the two warps of quarter wj split the chunks (c = wi, wi + 2, ...);
@@ -146,10 +148,38 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
             }
         }
     }
+    // The pre-pass (the preceding launch) writes the packed A1 and the scale rows; A2 was written
+    // before it (it waits for that writer before it lets this launch start), so the A2 load above
+    // overlaps the pre-pass and only the ring needs the wait.
+    pdl_wait();
+    if (threadIdx.x == 0)
+        for (int n = 0; n < kNS && n < my_units; ++n) issue(n);
     tmem::wait_st();
     tmem::fence_before();
     __syncthreads();
     tmem::fence_after();
+
+    // This warp's quarter of half wi of unit n's operands: A1k = A1 * S in place (rows nn = wj
+    // of every k-step, tail rows e = wj, wj + 4), then the hand-over to the half's 4 warps.
+    auto scale_share = [&](int n) {
+        const int sl = n % kNS;
+        mbar_wait(full + sl, static_cast<unsigned>((n / kNS) & 1), p.fault);
+        double* st = ring + sl * kStage;
+        const double* sr = st + kA1;
+        double* fr = st + (wi * KD) * 128 + wj * 32 + lane;
+#pragma unroll
+        for (int ks = 0; ks < KD; ++ks) fr[ks * 128] = rn_mul(fr[ks * 128], sr[4 * ks + t]);
+        double* tl = st + kFrag + (wi * NT) * 256 + wj * 32 + lane;
+#pragma unroll
+        for (int qt = 0; qt < NT; ++qt) {
+            const double sq = sr[4 * KD + qt];
+            tl[qt * 256] = rn_mul(tl[qt * 256], sq);
+            tl[qt * 256 + 128] = rn_mul(tl[qt * 256 + 128], sq);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(scaled + 2 * sl + wi);
+    };
+    if (my_units > 0) scale_share(0);
 
     double fsum = 0.0;
     for (int n = 0; n < my_units; ++n) {
@@ -157,11 +187,10 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
         const int ic = unit % n_ichunks;
         const int64_t kk = unit / n_ichunks;
         const int slot = n % kNS;
-        mbar_wait(full + slot, static_cast<unsigned>((n / kNS) & 1), p.fault);
+        mbar_wait(scaled + 2 * slot + wi, static_cast<unsigned>((n / kNS) & 1), p.fault);
         const double* stage = ring + slot * kStage;
-        const double* bfr = stage + (wi * KD) * 128 + lane;             // A1 of k-step ks at [ks * 128 + nn * 32]
-        const double* btl = stage + kFrag + (wi * NT) * 256 + lane;     // tail A1: [qt * 256 + e * 32]
-        const double* srow = stage + kA1;                               // S(k, q)
+        const double* bfr = stage + (wi * KD) * 128 + lane;             // A1k of k-step ks at [ks * 128 + nn * 32]
+        const double* btl = stage + kFrag + (wi * NT) * 256 + lane;     // tail A1k: [qt * 256 + e * 32]
         const int ibase = kA2tIC * ic + 32 * wi;
         double r1[kTN][2];
         if (FUNC) {
@@ -187,9 +216,8 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
                 double at[4];
                 tmem::ld_x8(ta + 8 * KD + 8 * qt, at);  // A2 tail, j = 8 m + g
                 double bt[8];
-                const double st = srow[4 * KD + qt];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) bt[e] = rn_mul(btl[qt * 256 + e * 32], st);  // A1k tail, i = 8 (e >> 1) + 2 t + (e & 1)
+                for (int e = 0; e < 8; ++e) bt[e] = btl[qt * 256 + e * 32];  // A1k tail, i = 8 (e >> 1) + 2 t + (e & 1)
 #pragma unroll
                 for (int nn = 0; nn < kTN; ++nn)
 #pragma unroll
@@ -203,9 +231,8 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
                 uint32_t ra[8];
                 double a[kTM], bb[kTN];
                 tmem::ld_x8_issue(ta + 8 * ks, ra);
-                const double sq = srow[4 * ks + t];
 #pragma unroll
-                for (int nn = 0; nn < kTN; ++nn) bb[nn] = rn_mul(bfr[ks * 128 + nn * 32], sq);  // A1k = A1 * S
+                for (int nn = 0; nn < kTN; ++nn) bb[nn] = bfr[ks * 128 + nn * 32];
                 tmem::wait_ld(ra);
                 tmem::unpack(ra, a);
 #pragma unroll
@@ -213,6 +240,7 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
 #pragma unroll
                     for (int nn = 0; nn < kTN; ++nn) dmma_884(acc[m][nn][0], acc[m][nn][1], a[m], bb[nn]);
             }
+            if (c == 0 && n + 1 < my_units) scale_share(n + 1);  // while this chunk's DMMAs drain
             if (c == n_jc - 1) {
                 // Release the ring slot (every operand of this unit has been read into registers);
                 // the last warp refills it with this CTA's unit n + kNS.
