@@ -79,25 +79,33 @@ def build(verbose: bool = False) -> Path:
 
 RUNNER_SRC = PKG / "runner" / "latsum_shard_runner.cpp"
 RUNNER = PKG / "bin" / "latsum_shard_runner"
+CLI_SRC = PKG / "runner" / "latsum_cli.cpp"
+CLI = PKG / "bin" / "latsum"
 CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 
 
-def build_runner() -> Path:
-    """The C++ multi-GPU runner (one process per GPU, NCCL all-reduce through the C ABI),
-    linked against the in-tree liblatsum_cuda.so (rpath $ORIGIN/..)."""
-    build()
-    deps = [RUNNER_SRC, OUT, *(ROOT / "include" / "latsum").glob("*.hpp"), ROOT / "include" / "latsum_cuda.h"]
-    if RUNNER.exists() and all(d.stat().st_mtime <= RUNNER.stat().st_mtime for d in deps):
-        return RUNNER
-    RUNNER.parent.mkdir(exist_ok=True)
+def _host_tool(src: Path, out: Path) -> Path:
+    deps = [src, OUT, *(ROOT / "include" / "latsum").glob("*.hpp"), ROOT / "include" / "latsum_cuda.h"]
+    if out.exists() and all(d.stat().st_mtime <= out.stat().st_mtime for d in deps):
+        return out
+    out.parent.mkdir(exist_ok=True)
     cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", f"-I{ROOT / 'include'}",
-           f"-I{ROOT / 'include' / 'eigen_compat'}", f"-I{CUDA_HOME / 'include'}", str(RUNNER_SRC), "-o",
-           str(RUNNER), f"-L{PKG}", "-llatsum_cuda", f"-L{CUDA_HOME / 'lib64'}", "-lcudart", "-pthread",
+           f"-I{ROOT / 'include' / 'eigen_compat'}", f"-I{CUDA_HOME / 'include'}", str(src), "-o",
+           str(out), f"-L{PKG}", "-llatsum_cuda", f"-L{CUDA_HOME / 'lib64'}", "-lcudart", "-pthread",
            "-Wl,-rpath,$ORIGIN/.."]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"runner build failed:\n{r.stderr}")
-    return RUNNER
+        raise RuntimeError(f"{out.name} build failed:\n{r.stderr}")
+    return out
+
+
+def build_runner() -> Path:
+    """The C++ host tools, linked against the in-tree liblatsum_cuda.so (rpath $ORIGIN/..): the
+    multi-GPU runner (one process per GPU, NCCL all-reduce through the C ABI) and the `latsum`
+    command line (the reference CLI's kernel / sum-box / sum-periodic / series / project)."""
+    build()
+    _host_tool(CLI_SRC, CLI)
+    return _host_tool(RUNNER_SRC, RUNNER)
 
 
 if __name__ == "__main__":
