@@ -75,8 +75,10 @@ def runner_path():
     """The C++ multi-GPU runner (paper_1405_2270_b200/bin/latsum_shard_runner, built by
     ``python -m paper_1405_2270_b200.build``): one process per GPU, DevicePotential +
     Communicator (include/latsum/sharded.hpp), NCCL all-reduce through the C ABI."""
+    import os
     from pathlib import Path
-    p = Path(__file__).resolve().parent / "bin" / "latsum_shard_runner"
+    # LS_SHARD_RUNNER: another executable with the same command line (the CPU tests' stand-in).
+    p = Path(os.environ.get("LS_SHARD_RUNNER") or Path(__file__).resolve().parent / "bin" / "latsum_shard_runner")
     if not p.exists():
         raise FileNotFoundError(f"{p} not built (python -m paper_1405_2270_b200.build)")
     return p

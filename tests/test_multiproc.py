@@ -81,3 +81,27 @@ def test_sharded_energy_allreduce_gloo():
     for _, total, full, _, _ in res:
         assert abs(total - full) <= 1e-13 * abs(full)
     assert res[0][1] == res[1][1]  # every rank holds the same reduced value
+
+
+def test_bench_sharded_path_world2_gloo(tmp_path):
+    """bench.py --gpus 2 under torchrun on CPU, with a stand-in for the C++ runner: the ranks agree
+    on a fresh NCCL-id file over gloo, rank 0's runner writes it and the other waits for it, and
+    rank 0 prints one JSON line for cfg2 strong scaling (the N > 1 path of the driver's run)."""
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    env = dict(os.environ, LS_SHARD_RUNNER=str(ROOT / "tests" / "devtools" / "fake_shard_runner.py"),
+               CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"),
+                        "--gpus", "2", "--steps", "3", "--warmup", "3"], capture_output=True, text=True, env=env,
+                       timeout=300, cwd=str(tmp_path))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["metric"].startswith("lattice potential")
+    assert d["config"]["grid"] == [2048, 2048, 2048] and "cfg2 strong" in d["config"]["workload"]
+    assert d["value"] > 0 and d["roofline"]["frac"] > 0 and d["e2e"]["value"] > 0
+    assert d["weak_scaling"]["grid"] == [1024, 1024, 2048] and d["energy"] is not None
