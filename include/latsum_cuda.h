@@ -311,6 +311,22 @@ int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, co
                            int64_t k0, int64_t k1, double* grid_h, double* f0_h, double* f1_h,
                            double* f2_h, double* wout_h);
 
+/* ---- QTT (qtt.hpp) ---------------------------------------
+ * TT-SVD sweep of every column of V_d (N = 2^L rows, ld ldv), one CTA per column with a
+ * one-sided Jacobi SVD: cores of column c packed at cores_d + c * core_stride (core k is
+ * (2 r_{k-1}) x r_k column-major), ranks_d + c * (L + 1) = r_0 .. r_L, capped_d[c] = 1 if a rank
+ * hit rmax (<= 64). core_stride >= ls_qtt_core_stride(N, rmax). Truncation: qtt.hpp:49-86. */
+int64_t ls_qtt_core_stride(int64_t N, int rmax);
+int ls_qtt_compress(const double* V_d, int64_t ldv, int64_t N, int ncols, double eps, int rmax, double* cores_d,
+                    int64_t core_stride, int* ranks_d, int* capped_d, void* stream);
+/* eps-rank of every 2^k x 2^(L-k) unfolding, k = 1 .. L-1 (qtt.hpp:131-152): ranks_d + c * (L - 1). */
+int ls_qtt_unfolding_ranks(const double* V_d, int64_t ldv, int64_t N, int ncols, double eps, int* ranks_d,
+                           void* stream);
+/* Host-level forms (host buffers in and out). */
+int ls_h_qtt_compress(const double* V_h, int64_t N, int ncols, double eps, int rmax, double* cores_h,
+                      int64_t core_stride, int* ranks_h, int* capped_h);
+int ls_h_qtt_unfolding_ranks(const double* V_h, int64_t N, int ncols, double eps, int* ranks_h);
+
 /* End-to-end energy (BASELINE configs[2]'s functional): the same generator and assembled sum,
  * then <V, rho> over slabs [k0, k1) for the separable density rho = r1 (x) r2 (x) r3 (host
  * vectors of the full axis lengths), fused into the expansion so V never leaves the device;

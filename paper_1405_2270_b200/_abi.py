@@ -96,6 +96,11 @@ SIGNATURES = {
     "ls_h_lattice_potential": (_i, [_i, _vp, _i64, _d, _vp, _vp, _i, _vp, _i, _i, _i64, _i64, _vp, _vp, _vp, _vp,
                                     _vp]),
     "ls_h_lattice_energy": (_i, [_i, _vp, _i64, _d, _vp, _vp, _i, _vp, _i, _i, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "ls_qtt_core_stride": (_i64, [_i64, _i]),
+    "ls_qtt_compress": (_i, [_vp, _i64, _i64, _i, _d, _i, _vp, _i64, _vp, _vp, _vp]),
+    "ls_qtt_unfolding_ranks": (_i, [_vp, _i64, _i64, _i, _d, _vp, _vp]),
+    "ls_h_qtt_compress": (_i, [_vp, _i64, _i, _d, _i, _vp, _i64, _vp, _vp]),
+    "ls_h_qtt_unfolding_ranks": (_i, [_vp, _i64, _i, _d, _vp]),
 }
 
 _lib = None

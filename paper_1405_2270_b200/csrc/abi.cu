@@ -909,6 +909,54 @@ int ls_h_lattice_potential(int mode, const int64_t L[3], int64_t n, double b, co
                         wout_h, nullptr, nullptr);
 }
 
+// Host-level QTT (qtt.hpp): the columns of V_h (N x ncols, column-major) in, cores / ranks out.
+int ls_h_qtt_compress(const double* V_h, int64_t N, int ncols, double eps, int rmax, double* cores_h,
+                      int64_t core_stride, int* ranks_h, int* capped_h) {
+    if (ncols < 0) return ls::fail(LS_EVALIDATION, "qtt_compress: negative column count");
+    if (N < 2 || (N & (N - 1)) != 0)
+        return ls::fail(LS_EVALIDATION, "qtt_compress: length " + std::to_string(N) + " is not a power of two >= 2");
+    if (!(eps > 0.0)) return ls::fail(LS_EVALIDATION, "qtt_compress: eps must be positive");
+    int L = 0;
+    while ((int64_t(1) << L) < N && L < 62) ++L;
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    const cudaStream_t s = st->compute;
+    DevBuf v, cores, ranks, capped;
+    LS_TRY(ls::upload(v, V_h, sizeof(double) * static_cast<size_t>(std::max<int64_t>(N, 0)) * ncols, s));
+    LS_TRY(cores.alloc(sizeof(double) * std::max<int64_t>(core_stride, 1) * std::max(ncols, 1), s));
+    LS_TRY(ranks.alloc(sizeof(int) * (L + 1) * std::max(ncols, 1), s));
+    LS_TRY(capped.alloc(sizeof(int) * std::max(ncols, 1), s));
+    LS_TRY(ls_qtt_compress(v.d(), N, N, ncols, eps, rmax, cores.d(), core_stride, static_cast<int*>(ranks.p),
+                           static_cast<int*>(capped.p), s));
+    if (ncols > 0) {
+        LS_CUDA(cudaMemcpyAsync(cores_h, cores.p, sizeof(double) * core_stride * ncols, cudaMemcpyDeviceToHost, s));
+        LS_CUDA(cudaMemcpyAsync(ranks_h, ranks.p, sizeof(int) * (L + 1) * ncols, cudaMemcpyDeviceToHost, s));
+        LS_CUDA(cudaMemcpyAsync(capped_h, capped.p, sizeof(int) * ncols, cudaMemcpyDeviceToHost, s));
+    }
+    LS_SYNC(s);
+    return LS_OK;
+}
+
+int ls_h_qtt_unfolding_ranks(const double* V_h, int64_t N, int ncols, double eps, int* ranks_h) {
+    if (ncols < 0) return ls::fail(LS_EVALIDATION, "unfolding_rank_profile: negative column count");
+    if (N < 2 || (N & (N - 1)) != 0)
+        return ls::fail(LS_EVALIDATION, "unfolding_rank_profile: length is not a power of two >= 2");
+    if (!(eps > 0.0)) return ls::fail(LS_EVALIDATION, "unfolding_rank_profile: eps must be positive");
+    int L = 0;
+    while ((int64_t(1) << L) < N && L < 62) ++L;
+    Streams* st;
+    LS_TRY(ls::get_streams(st));
+    const cudaStream_t s = st->compute;
+    DevBuf v, ranks;
+    LS_TRY(ls::upload(v, V_h, sizeof(double) * static_cast<size_t>(std::max<int64_t>(N, 0)) * ncols, s));
+    LS_TRY(ranks.alloc(sizeof(int) * std::max(L - 1, 1) * std::max(ncols, 1), s));
+    LS_TRY(ls_qtt_unfolding_ranks(v.d(), N, N, ncols, eps, static_cast<int*>(ranks.p), s));
+    if (ncols > 0 && L > 1)
+        LS_CUDA(cudaMemcpyAsync(ranks_h, ranks.p, sizeof(int) * (L - 1) * ncols, cudaMemcpyDeviceToHost, s));
+    LS_SYNC(s);
+    return LS_OK;
+}
+
 int ls_h_lattice_energy(int mode, const int64_t L[3], int64_t n, double b, const double* tau_h, const double* w_h,
                         int R, const double* charges_h, int M0, int periodic, int64_t k0, int64_t k1,
                         const double* r1_h, const double* r2_h, const double* r3_h, double* energy_h) {

@@ -507,6 +507,86 @@ def lattice_energy(spec: LatticeSpec, rule: QuadratureRule, rho: Sequence[np.nda
     return float(out[0])
 
 
+# --------------------------------------------------------------------- qtt.hpp
+QTT_RANK_CAP = 64
+
+
+@dataclass
+class QTTVector:
+    """qtt.hpp:25-44: cores[k] is (2 r_{k-1}) x r_k (Fortran order)."""
+    cores: list
+    eps_used: float = 0.0
+
+    def levels(self) -> int:
+        return len(self.cores)
+
+    def ranks(self) -> list[int]:
+        return [int(c.shape[1]) for c in self.cores[:-1]]
+
+
+def qtt_compress_columns(V: np.ndarray, eps: float) -> list[QTTVector]:
+    """qtt_compress (qtt.hpp:49-86) of every column of V (N x ncols, N a power of two), one
+    batched GPU sweep (ls_h_qtt_compress)."""
+    V = _f64(V if np.ndim(V) == 2 else np.reshape(V, (-1, 1)))
+    N, ncols = V.shape
+    if N < 2 or N & (N - 1):
+        raise ValidationError(f"qtt_compress: length {N} is not a power of two >= 2")
+    if not eps > 0:
+        raise ValidationError("qtt_compress: eps must be positive")
+    L = N.bit_length() - 1
+    lib = _abi.load()
+    stride = int(lib.ls_qtt_core_stride(N, QTT_RANK_CAP))
+    cores = np.zeros(stride * max(ncols, 1))
+    ranks = np.zeros((L + 1) * max(ncols, 1), dtype=np.int32)
+    capped = np.zeros(max(ncols, 1), dtype=np.int32)
+    call("ls_h_qtt_compress", _p(V), N, ncols, float(eps), QTT_RANK_CAP, _p(cores), stride, _p(ranks), _p(capped))
+    out = []
+    for c in range(ncols):
+        if capped[c]:
+            raise ResourceGuardError(f"qtt_compress: a quantized rank exceeds the cap of {QTT_RANK_CAP}")
+        rk = ranks[(L + 1) * c:(L + 1) * (c + 1)]
+        off, cs = stride * c, []
+        for k in range(L):
+            rows, cols = 2 * int(rk[k]), int(rk[k + 1])
+            cs.append(cores[off:off + rows * cols].reshape((rows, cols), order="F").copy())
+            off += rows * cols
+        out.append(QTTVector(cs, eps))
+    return out
+
+
+def qtt_compress(v: np.ndarray, eps: float) -> QTTVector:
+    return qtt_compress_columns(np.asarray(v, dtype=np.float64).reshape(-1, 1), eps)[0]
+
+
+def qtt_reconstruct(t: QTTVector) -> np.ndarray:
+    """qtt.hpp:89-107 (host contraction)."""
+    if not t.cores:
+        raise ValidationError("qtt_reconstruct: empty train")
+    w = t.cores[0]
+    for k, core in enumerate(t.cores[1:], 1):
+        r = core.shape[0] // 2
+        if w.shape[1] != r:
+            raise ValidationError(f"qtt_reconstruct: rank profile mismatch at core {k}")
+        w = np.vstack([w @ core[:r], w @ core[r:]])
+    if t.cores[-1].shape[1] != 1:
+        raise ValidationError("qtt_reconstruct: boundary rank is not 1")
+    return w[:, 0]
+
+
+def unfolding_rank_profile(v: np.ndarray, eps: float) -> list[int]:
+    """qtt.hpp:131-152 on the GPU (ls_h_qtt_unfolding_ranks)."""
+    v = _f64(v).ravel()
+    N = v.size
+    if N < 2 or N & (N - 1):
+        raise ValidationError("unfolding_rank_profile: length is not a power of two >= 2")
+    if not eps > 0:
+        raise ValidationError("unfolding_rank_profile: eps must be positive")
+    L = N.bit_length() - 1
+    out = np.zeros(max(L - 1, 1), dtype=np.int32)
+    call("ls_h_qtt_unfolding_ranks", _p(v), N, 1, float(eps), _p(out))
+    return [int(x) for x in out[:L - 1]]
+
+
 # ----------------------------------------------------------------- project.hpp
 @dataclass
 class GaussianBasisSpec:

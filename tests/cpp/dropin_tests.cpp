@@ -1066,4 +1066,198 @@ TEST(Bundle, RankZeroAndLatticeResultsRoundTrip) {  // test_bundle.cpp (rank zer
     std::remove(path.c_str());
 }
 
+// ------------------------------------------------------------------ QTT (GPU TT-SVD sweep)
+Vector qtt_random(std::mt19937& gen, Index n) {
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    Vector v(n);
+    for (Index i = 0; i < n; ++i) v[i] = dist(gen);
+    return v;
+}
+double qtt_rel_err(const QTTVector& t, const Vector& v) {
+    const Vector r = qtt_reconstruct(t);
+    double num = 0.0, den = 0.0;
+    for (Index i = 0; i < v.size(); ++i) {
+        num += (r[i] - v[i]) * (r[i] - v[i]);
+        den += v[i] * v[i];
+    }
+    return std::sqrt(num / den);
+}
+
+TEST(QttBasics, HelpersAndBadInput) {  // test_qtt.cpp:22-39
+    EXPECT_TRUE(is_power_of_two(1024));
+    EXPECT_FALSE(is_power_of_two(3));
+    EXPECT_FALSE(is_power_of_two(-4));
+    EXPECT_EQ(log2_exact(4096), 12);
+    EXPECT_THROW(qtt_compress(Vector::Ones(6), 1e-8), validation_error);
+    EXPECT_THROW(qtt_compress(Vector::Ones(1), 1e-8), validation_error);
+    EXPECT_THROW(qtt_compress(Vector::Ones(8), 0.0), validation_error);
+    EXPECT_THROW(unfolding_rank_profile(Vector::Ones(6), 1e-8), validation_error);
+}
+
+TEST(QttRanks, KnownRanks) {  // test_qtt.cpp:41-89: constant, geometric, impulse, sinusoid, cubic
+    QTTVector t = qtt_compress(Vector::Constant(256, 3.25), 1e-12);
+    EXPECT_EQ(qtt_rank_profile(t).max_rank, 1);
+    EXPECT_LT(qtt_rel_err(t, Vector::Constant(256, 3.25)), 1e-12);
+    Vector g(512);
+    for (Index i = 0; i < 512; ++i) g[i] = std::pow(0.99, static_cast<double>(i));
+    t = qtt_compress(g, 1e-12);
+    EXPECT_EQ(qtt_rank_profile(t).max_rank, 1);
+    EXPECT_LT(qtt_rel_err(t, g), 1e-12);
+    for (Index pos : {Index{0}, Index{7}, Index{100}, Index{255}}) {
+        Vector v = Vector::Zero(256);
+        v[pos] = 1.0;
+        t = qtt_compress(v, 1e-12);
+        EXPECT_EQ(qtt_rank_profile(t).max_rank, 1);
+        EXPECT_LT(qtt_rel_err(t, v), 1e-13);
+    }
+    for (double omega : {0.01, 0.37, 2.1}) {
+        Vector v(1024);
+        for (Index i = 0; i < 1024; ++i) v[i] = std::sin(omega * static_cast<double>(i) + 0.3);
+        t = qtt_compress(v, 1e-10);
+        EXPECT_LE(qtt_rank_profile(t).max_rank, 2);
+        EXPECT_LT(qtt_rel_err(t, v), 1e-10);
+    }
+    Vector p(2048);
+    for (Index i = 0; i < 2048; ++i) {
+        const double x = static_cast<double>(i) / 2048.0;
+        p[i] = ((x - 0.4) * x + 0.25) * x - 1.0;
+    }
+    t = qtt_compress(p, 1e-11);
+    EXPECT_LE(qtt_rank_profile(t).max_rank, 4);
+    EXPECT_LT(qtt_rel_err(t, p), 1e-11);
+}
+
+TEST(QttRanks, RandomVectorHasMaximalRanks) {  // test_qtt.cpp:91-102
+    std::mt19937 gen(77);
+    Vector v = qtt_random(gen, 256);
+    QTTVector t = qtt_compress(v, 1e-14);
+    const std::vector<Index> ranks = t.ranks();
+    ASSERT_EQ(ranks.size(), 7u);
+    for (std::size_t k = 0; k < ranks.size(); ++k)
+        EXPECT_EQ(ranks[k], std::min(Index{1} << (k + 1), Index{256} >> (k + 1)));
+    EXPECT_LT(qtt_rel_err(t, v), 1e-12);
+}
+
+TEST(QttCompress, HonorsErrorContractAndCompresses) {  // test_qtt.cpp:104-130
+    std::mt19937 gen(78);
+    for (double eps : {1e-2, 1e-4, 1e-8}) {
+        for (int trial = 0; trial < 7; ++trial) {
+            Vector v = qtt_random(gen, 1024);
+            for (Index i = 0; i < 1024; ++i)
+                v[i] = std::exp(-std::pow((static_cast<double>(i) - 512.0) / 150.0, 2)) + 0.01 * v[i];
+            QTTVector t = qtt_compress(v, eps);
+            EXPECT_LE(qtt_rel_err(t, v), eps);
+        }
+    }
+    Vector s(4096);
+    for (Index i = 0; i < 4096; ++i) {
+        const double x = (static_cast<double>(i) + 0.5) / 4096.0 * 10.0 - 5.0;
+        s[i] = std::exp(-x * x);
+    }
+    QTTVector t = qtt_compress(s, 1e-6);
+    EXPECT_LE(qtt_rank_profile(t).max_rank, 25);
+    EXPECT_LT(qtt_rank_profile(t).avg_rank, 15.0);
+}
+
+TEST(UnfoldingRanks, KnownCasesAndSweepDominates) {  // test_qtt.cpp:132-160
+    for (Index r : unfolding_rank_profile(Vector::Constant(128, 2.0), 1e-10)) EXPECT_EQ(r, 1);
+    std::mt19937 gen(79);
+    Vector v = qtt_random(gen, 128);
+    std::vector<Index> rr = unfolding_rank_profile(v, 1e-14);
+    ASSERT_EQ(rr.size(), 6u);
+    for (std::size_t k = 0; k < rr.size(); ++k) EXPECT_EQ(rr[k], std::min(Index{1} << (k + 1), Index{128} >> (k + 1)));
+    EXPECT_EQ(max_unfolding_rank(v, 0.999), 1);
+    std::mt19937 gen2(80);
+    for (int trial = 0; trial < 5; ++trial) {
+        Vector w = qtt_random(gen2, 512);
+        for (Index i = 0; i < 512; ++i) w[i] += 3.0 * std::cos(0.02 * static_cast<double>(i));
+        std::vector<Index> sweep = qtt_compress(w, 1e-4).ranks(), intrinsic = unfolding_rank_profile(w, 1e-4);
+        ASSERT_EQ(sweep.size(), intrinsic.size());
+        for (std::size_t k = 0; k < sweep.size(); ++k) EXPECT_GE(sweep[k], intrinsic[k]);
+    }
+}
+
+TEST(Modulation, BoundsHoldAndShapesChecked) {  // test_qtt.cpp:162-201
+    const Index block = 64, n_blocks = 8, total = block * n_blocks;
+    Vector x0(block);
+    for (Index i = 0; i < block; ++i) x0[i] = std::exp(-std::pow((static_cast<double>(i) + 0.5 - 32.0) / 6.0, 2));
+    Vector F(total);
+    for (Index i = 0; i < total; ++i) {
+        const double tpos = (static_cast<double>(i) + 0.5) / static_cast<double>(total);
+        F[i] = std::sin(2.0 * M_PI * 3.0 * tpos + 0.4) + 1.2;
+    }
+    ModulationReport rep = block_modulated_vector(x0, n_blocks, F, 1e-10);
+    EXPECT_TRUE(rep.tiling_bound_ok);
+    EXPECT_TRUE(rep.product_bound_ok);
+    EXPECT_LE(rep.rfx, rep.rF * rep.r0);
+    for (Index blk = 0; blk < n_blocks; ++blk)
+        for (Index i = 0; i < block; ++i) EXPECT_EQ(rep.x[blk * block + i], x0[i]);
+    ModulationReport id = block_modulated_vector(x0, 1, Vector::Ones(64), 1e-10);
+    EXPECT_EQ(id.rF, 1);
+    EXPECT_EQ(id.rx, id.r0);
+    EXPECT_THROW(block_modulated_vector(Vector::Ones(6), 2, Vector::Ones(12), 1e-8), validation_error);
+    EXPECT_THROW(block_modulated_vector(Vector::Ones(64), 3, Vector::Ones(192), 1e-8), validation_error);
+    EXPECT_THROW(block_modulated_vector(Vector::Ones(64), 2, Vector::Ones(100), 1e-8), validation_error);
+}
+
+TEST(AssembledQtt, ReportsPaddingAndRebuild) {  // test_qtt.cpp:203-265
+    LatticeSpec spec = make_spec({2, 1, 1}, 8, 2.0, {Charge{}});
+    QuadratureRule rule = calibrate_for_lattice(spec, 1e-4);
+    CanonicalTensor3 master = build_lattice_master(spec, rule);
+    AssembledQttResult res = assembled_qtt_sum(spec, master, 1e-8, &rule);
+    const Index R = rule.node_count();
+    ASSERT_EQ(res.columns.size(), static_cast<std::size_t>(3 * R));
+    EXPECT_TRUE((res.padded_len == Dims3{16, 8, 8}));
+    for (const QttColumnReport& rep : res.reports) {
+        EXPECT_LE(rep.rec_err, 1e-8);
+        EXPECT_TRUE(rep.regime == 0 || rep.regime == 1);
+    }
+    for (const QttColumnReport& rep : assembled_qtt_sum(spec, master, 1e-8).reports) EXPECT_EQ(rep.regime, -1);
+    LatticeSpec s3 = make_spec({3, 1, 1}, 6, 2.0, {Charge{}});
+    QuadratureRule r3 = calibrate_for_lattice(s3, 1e-4);
+    CanonicalTensor3 m3 = build_lattice_master(s3, r3);
+    EXPECT_TRUE((assembled_qtt_sum(s3, m3, 1e-8, &r3).padded_len == Dims3{32, 8, 8}));
+    EXPECT_THROW(assembled_qtt_sum(s3, m3, 1e-8, &r3, 16), resource_guard_error);
+    // rebuilding the factors from the trains reproduces the assembled tensor (test_qtt.cpp:239-265)
+    const double eps = 1e-8;
+    LatticeSpec s2 = make_spec({2, 2, 2}, 4, 2.0, {Charge{}});
+    QuadratureRule r2 = calibrate_for_lattice(s2, 1e-4);
+    CanonicalTensor3 m2 = build_lattice_master(s2, r2);
+    SumResult assembled = assembled_box_sum(s2, m2);
+    AssembledQttResult q2 = assembled_qtt_sum(s2, m2, eps, &r2);
+    const Index R2 = r2.node_count();
+    std::array<Matrix, 3> factors;
+    for (int axis = 0; axis < 3; ++axis) {
+        const Index N = s2.target_cells(axis);
+        factors[static_cast<std::size_t>(axis)].resize(N, R2);
+        for (Index q = 0; q < R2; ++q) {
+            const Vector rec = qtt_reconstruct(q2.columns[static_cast<std::size_t>(axis * R2 + q)]);
+            for (Index i = 0; i < N; ++i) factors[static_cast<std::size_t>(axis)](i, q) = rec[i];
+        }
+    }
+    CanonicalTensor3 rebuilt(std::move(factors), Vector(assembled.tensor.weights()));
+    StreamDiff d = max_norm_diff_canonical(rebuilt, assembled.tensor);
+    EXPECT_LE(d.max_diff, 10.0 * eps * d.max_abs_b);
+}
+
+TEST(GaussianRankGrowth, LogarithmicInTolerance) {  // test_qtt.cpp:267-290
+    const Index N = Index{1} << 12;
+    std::vector<double> lx, mr;
+    for (double eps : {1e-3, 1e-5, 1e-7}) {
+        const double a = std::sqrt(2.0) * std::sqrt(std::log(1.0 / eps));
+        Vector v(N);
+        for (Index i = 0; i < N; ++i) {
+            const double x = (static_cast<double>(i) + 0.5) / static_cast<double>(N) * 2.0 * a - a;
+            v[i] = std::exp(-x * x / 2.0);
+        }
+        const Index r = max_unfolding_rank(v, eps);
+        lx.push_back(std::log(1.0 / eps));
+        mr.push_back(static_cast<double>(r));
+        EXPECT_LE(r, 25);
+    }
+    const double slope = (mr[2] - mr[0]) / (lx[2] - lx[0]);
+    EXPECT_GE(slope, 0.0);
+    EXPECT_LE(slope, 4.0);
+}
+
 int main(int argc, char** argv) { return minitest::run_all(argc, argv); }
