@@ -10,11 +10,13 @@
 //   latsum ... series [--kind line|plane|cube] --L l1,l2,... [--n N] [--b B] [--eps E]
 //                     [--extrapolate linear|quadratic|none] [--report CSV]
 //   latsum ... project --from BUNDLE --basis CSV --out CSV [--no-volume]
+//   latsum ... qtt-ranks --from BUNDLE [--eps E] [--report CSV]
+//   latsum ... qtt-gauss [--p p1,p2] [--eps-list e1,e2,...] [--levels L] [--report CSV]
 //
 // Same outputs as the reference: the LATSUMB1 bundle, the CSV reports, the console summary and
 // the resolved run configuration next to the primary output (<out>.run.json). Exit codes:
-// 0 ok, 2 validation error, 4 resource guard (proj/tools/latsum.cpp:25-31). The QTT, bench and
-// repro subcommands are out of this build's scope.
+// 0 ok, 2 validation error, 4 resource guard (proj/tools/latsum.cpp:25-31). The bench and repro
+// harness subcommands are out of this build's scope.
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -34,6 +36,7 @@
 #include "latsum/newton.hpp"
 #include "latsum/parallel.hpp"
 #include "latsum/project.hpp"
+#include "latsum/qtt.hpp"
 #include "latsum/quadrature.hpp"
 
 namespace {
@@ -89,6 +92,8 @@ const std::map<std::string, std::vector<std::string>>& known_options() {
         {"sum-periodic", {"--L", "--n", "--b", "--eps", "--charges", "--out", "--report"}},
         {"series", {"--kind", "--L", "--n", "--b", "--eps", "--extrapolate", "--report"}},
         {"project", {"--from", "--basis", "--out", "--no-volume"}},
+        {"qtt-ranks", {"--from", "--eps", "--report"}},
+        {"qtt-gauss", {"--p", "--eps-list", "--levels", "--report"}},
     };
     return m;
 }
@@ -368,6 +373,112 @@ int run_project(const Args& a, int threads, long seed) {  // proj/tools/latsum.c
     return exit_ok;
 }
 
+std::string dlist_json(const std::vector<double>& v) {
+    std::string o = "[";
+    for (size_t i = 0; i < v.size(); ++i) o += (i ? ", " : "") + Json::num(v[i]);
+    return o + "]";
+}
+std::vector<double> double_list(const std::string& k, const std::string& v) {
+    std::vector<double> out;
+    for (const std::string& x : split(v, ',')) out.push_back(to_double(k, x));
+    return out;
+}
+
+int run_qtt_ranks(const Args& a, int threads, long seed) {  // proj/tools/latsum.cpp:206-242
+    const std::string from = a.need("--from"), report = a.str("--report", "qtt_ranks.csv");
+    const double eps = to_double("--eps", a.str("--eps", "1e-08"));
+    Json params;
+    params.kv = {{"from", Json::q(from)}, {"eps", Json::num(eps)}, {"report", Json::q(report)}};
+    write_run_config(report, base_config("qtt-ranks", threads, seed, params));
+    const latsum::TensorBundle bundle = latsum::load_bundle(from);
+    if (bundle.tensor.rank() < 1) throw latsum::validation_error("qtt-ranks: bundle has rank 0, nothing to compress");
+    std::vector<std::vector<std::string>> rows;
+    double sum_max = 0.0;
+    Index count = 0;
+    for (int axis = 0; axis < 3; ++axis) {
+        const latsum::Matrix& factor = bundle.tensor.factor(axis);
+        const Index N = factor.rows();
+        Index padded = 2;
+        while (padded < N) padded *= 2;
+        latsum::Matrix V = latsum::Matrix::Zero(padded, bundle.tensor.rank());
+        for (Index q = 0; q < bundle.tensor.rank(); ++q)
+            for (Index i = 0; i < N; ++i) V(i, q) = factor(i, q);
+        const std::vector<latsum::QTTVector> trains = latsum::detail::qtt_compress_columns(V, eps);  // one launch
+        for (Index q = 0; q < bundle.tensor.rank(); ++q) {
+            const latsum::QTTVector& t = trains[static_cast<size_t>(q)];
+            const latsum::RankProfile prof = latsum::qtt_rank_profile(t);
+            const latsum::Vector rec = latsum::qtt_reconstruct(t);
+            double num = 0.0, den = 0.0;
+            for (Index i = 0; i < N; ++i) {
+                num += (rec[i] - factor(i, q)) * (rec[i] - factor(i, q));
+                den += factor(i, q) * factor(i, q);
+            }
+            const double err = den > 0.0 ? std::sqrt(num / den) : std::sqrt(num);
+            rows.push_back({std::to_string(axis), std::to_string(q), std::to_string(prof.max_rank),
+                            latsum::format_double(prof.avg_rank), latsum::format_double(err)});
+            sum_max += static_cast<double>(prof.max_rank);
+            ++count;
+        }
+    }
+    write_csv(report, {"axis", "q", "max_rank", "avg_rank", "err"}, rows);
+    std::cout << "qtt-ranks: " << count << " columns from " << from << ", average max rank "
+              << sum_max / static_cast<double>(count) << "\n"
+              << "report written to " << report << "\n";
+    return exit_ok;
+}
+
+// Least-squares slope of y against x (bench.hpp:41-51).
+double fit_slope(const std::vector<double>& x, const std::vector<double>& y) {
+    const double n = static_cast<double>(x.size());
+    double sx = 0.0, sy = 0.0, sxx = 0.0, sxy = 0.0;
+    for (size_t i = 0; i < x.size(); ++i) {
+        sx += x[i];
+        sy += y[i];
+        sxx += x[i] * x[i];
+        sxy += x[i] * y[i];
+    }
+    return (n * sxy - sx * sy) / (n * sxx - sx * sx);
+}
+
+int run_qtt_gauss(const Args& a, int threads, long seed) {  // proj/tools/latsum.cpp:244-281
+    const std::vector<double> p_list = double_list("--p", a.str("--p", "1"));
+    const std::vector<double> eps_list = double_list("--eps-list", a.str("--eps-list", "1e-3,1e-4,1e-5,1e-6,1e-7,1e-8,1e-9"));
+    const Index levels = to_long("--levels", a.str("--levels", "12"));
+    const std::string report = a.str("--report");
+    Json params;
+    params.kv = {{"p", dlist_json(p_list)}, {"eps_list", dlist_json(eps_list)}, {"levels", std::to_string(levels)},
+                 {"report", Json::q(report)}};
+    write_run_config(report.empty() ? "qtt-gauss" : report, base_config("qtt-gauss", threads, seed, params));
+    if (levels < 2 || levels > 24) throw latsum::validation_error("qtt-gauss: --levels must lie in [2, 24]");
+    for (double eps : eps_list)
+        if (!(eps > 0.0) || !(eps < 1.0)) throw latsum::validation_error("qtt-gauss: eps values must lie in (0, 1)");
+    const Index N = Index{1} << levels;
+    std::vector<std::vector<std::string>> rows;
+    for (double p : p_list) {
+        if (!(p > 0.0)) throw latsum::validation_error("qtt-gauss: p must be positive");
+        std::vector<double> lx, ly;
+        for (double eps : eps_list) {
+            const double aa = std::sqrt(2.0) * p * std::sqrt(std::log(1.0 / eps));
+            latsum::Vector v(N);
+            for (Index i = 0; i < N; ++i) {
+                const double x = (static_cast<double>(i) + 0.5) / static_cast<double>(N) * 2.0 * aa - aa;
+                v[i] = std::exp(-x * x / (2.0 * p * p));
+            }
+            const Index r = latsum::max_unfolding_rank(v, eps);
+            rows.push_back({latsum::format_double(p), latsum::format_double(eps), std::to_string(r)});
+            lx.push_back(std::log(1.0 / eps));
+            ly.push_back(static_cast<double>(r));
+        }
+        const double slope = lx.size() >= 2 ? fit_slope(lx, ly) : 0.0;
+        std::cout << "p=" << p << ": max rank vs ln(1/eps) slope " << slope << "\n";
+    }
+    if (!report.empty()) {
+        write_csv(report, {"p", "eps", "max_rank"}, rows);
+        std::cout << "report written to " << report << "\n";
+    }
+    return exit_ok;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -381,6 +492,8 @@ int main(int argc, char** argv) {
         if (a.command == "sum-periodic") return run_sum(a, true, threads, seed);
         if (a.command == "series") return run_series(a, threads, seed);
         if (a.command == "project") return run_project(a, threads, seed);
+        if (a.command == "qtt-ranks") return run_qtt_ranks(a, threads, seed);
+        if (a.command == "qtt-gauss") return run_qtt_gauss(a, threads, seed);
         std::cerr << "no subcommand given\n";
         return exit_validation;
     } catch (const latsum::resource_guard_error& e) {

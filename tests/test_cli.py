@@ -49,7 +49,8 @@ def test_cli_usage_errors_exit_2(cli, tmp_path):
     assert r.returncode == 2 and "n must be even" in r.stderr
     r = run(cli, "sum-box", "--L", "2,3", "--n", "8", "--b", "2", "--out", tmp_path / "x.bin")
     assert r.returncode == 2 and "--L expects" in r.stderr
-    assert run(cli, "qtt-ranks", "--from", "x").returncode == 2
+    assert run(cli, "bench", "--L", "2").returncode == 2  # harness subcommands are out of scope
+    assert run(cli, "qtt-gauss", "--levels", 30, cwd=tmp_path).returncode == 2  # writes qtt-gauss.run.json there
     assert run(cli, "sum-box", "--n", "8", "--b", "2", "--out", tmp_path / "x.bin").returncode == 2  # --L required
     cfg = json.loads((tmp_path / "x.bin.run.json").read_text())  # written before validation, as the reference
     assert cfg["command"] == "sum-box" and cfg["params"]["n"] == 8
@@ -114,3 +115,21 @@ def test_cli_kernel_series_project(cli, tmp_path):
     V = np.array([[float(x) for x in ln.split(",")] for ln in lines[1:]])
     assert V[0, 1] == V[1, 0] and np.all(V > 0)  # exactly symmetric (project.hpp:65-97)
     assert math.isfinite(V.sum())
+
+
+@pytest.mark.gpu
+def test_cli_qtt_subcommands(cli, tmp_path):
+    out = tmp_path / "b.bin"
+    assert run(cli, "sum-box", "--L", "4", "--n", 16, "--b", 2, "--eps", "1e-4", "--out", out).returncode == 0
+    r = run(cli, "qtt-ranks", "--from", out, "--eps", "1e-8", "--report", tmp_path / "q.csv")
+    assert r.returncode == 0, r.stderr
+    rows = (tmp_path / "q.csv").read_text().splitlines()
+    assert rows[0] == "axis,q,max_rank,avg_rank,err"
+    f, w, _ = read_bundle(out)
+    assert len(rows) == 1 + 3 * len(w)
+    assert all(float(x.split(",")[4]) <= 1e-8 for x in rows[1:])
+    r = run(cli, "qtt-gauss", "--p", "1,0.5", "--eps-list", "1e-3,1e-5,1e-7", "--levels", 10, "--report", tmp_path / "g.csv")
+    assert r.returncode == 0, r.stderr
+    g = (tmp_path / "g.csv").read_text().splitlines()
+    assert g[0] == "p,eps,max_rank" and len(g) == 7
+    assert "max rank vs ln(1/eps) slope" in r.stdout
