@@ -229,3 +229,47 @@ def test_pipeline_bitwise_run_to_run(env, n_charges):
     assert not torch.isnan(a).any()
     assert torch.equal(a, c)
     assert e1 == e2
+
+
+@pytest.mark.parametrize("R,dims,plan", [
+    (122, (256, 200, 300), "single A1k buffer"), (164, (300, 256, 200), "single A1k buffer"),
+    (199, (256, 130, 260), "single A1k buffer"), (249, (128, 256, 300), "single A1k buffer"),
+    (5, (256, 256, 300), None), (21, (200, 256, 300), None), (54, (256, 128, 300), None),
+    (57, (256, 250, 300), None)])
+def test_expand_many_units_per_cta(env, orc, R, dims, plan):
+    """Launches with several units per CTA: the single-buffer TMEM plan's unit-boundary refill
+    (ranks 122-249) and the A2-in-TMEM plan's ring reuse and next-unit scaling (N2 <= 256), which
+    the small fuzz shapes above never reach. Sampled slabs (first, last, in between) against the
+    oracle, and the fused functional against the stored grid."""
+    torch, _abi = env
+    import paper_1405_2270_b200 as L
+    if plan:
+        assert plan in L.expansion_plan(R)
+    rng = np.random.default_rng(R)
+    n1, n2, n3 = dims
+    f = [np.asfortranarray(rng.uniform(0.05, 1.0, (d, R))) for d in dims]
+    w = rng.uniform(0.05, 1.0, R)
+    dev = torch.device("cuda")
+    fac = [torch.as_tensor(x.T.copy(), device=dev) for x in f]
+    wd = torch.as_tensor(w, device=dev)
+    from paper_1405_2270_b200.latsum import _expand_device
+    out = torch.empty((n3, n2, n1), dtype=torch.float64, device=dev)
+    _expand_device(fac, wd, dims, 0, n3, out)
+    torch.cuda.synchronize()
+    for k in (0, 1, n3 // 3, n3 // 2 + 1, n3 - 2, n3 - 1):
+        want = orc.densify_slabs(f[0], f[1], f[2], w, k, k + 1)[:, :, 0]
+        got = out[k].cpu().numpy().T
+        assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want)), k
+    # fused functional (ls_expand with rho, partials, fixed-order sum) against the stored grid
+    rho = [torch.as_tensor(rng.uniform(0.1, 1.0, d), device=dev) for d in dims]
+    np_ = int(_abi.load().ls_expand_partial_count(n1, n2, R, 0, n3))
+    part = torch.zeros(max(np_, 1), dtype=torch.float64, device=dev)
+    e = torch.zeros(1, dtype=torch.float64, device=dev)
+    lib = _abi.load()
+    p = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.ls_expand(p(fac[0]), n1, p(fac[1]), n2, p(fac[2]), n3, p(wd), n1, n2, n3, R, 0, n3, None, 0, 0,
+                         p(rho[0]), p(rho[1]), p(rho[2]), p(part), s) == 0
+    assert lib.ls_sum_partials(p(part), np_, p(e), s) == 0
+    e_stored = float(torch.einsum("kji,i,j,k->", out, rho[0], rho[1], rho[2]))
+    assert abs(float(e.cpu()) - e_stored) <= 1e-12 * abs(e_stored)
