@@ -32,7 +32,7 @@
 namespace ls_k3 {
 namespace {
 
-constexpr int kA2tWarps = 8, kA2tIC = 64, kA2tJC = 128, kA2tNS = 4, kA2tHdr = 32;
+constexpr int kA2tWarps = 8, kA2tIC = 64, kA2tJC = 128, kA2tNS = 4, kA2tMaxJC = 16, kA2tHdr = 32 + 4 * kA2tMaxJC;
 
 __host__ __device__ constexpr int a2t_stage_elems(int KD, int NT) { return 2 * KD * 128 + 2 * NT * 256; }
 // scale-row length, padded to whole 16-byte TMA chunks
@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
     int* released = reinterpret_cast<int*>(smem + 8);           // [kNS]
     uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(smem + 16);
     uint64_t* scaled = reinterpret_cast<uint64_t*>(smem + 20);  // [kNS][2]: slot's half scaled by its 4 warps
+    uint64_t* a2r = reinterpret_cast<uint64_t*>(smem + 32);     // [kA2tMaxJC][4]: A2 chunk c of quarter q in TMEM
     double* ring = smem + kA2tHdr;                              // [kNS][kStage]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -116,15 +117,25 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
             mbar_init(scaled + 2 * s + 1, 4);
             released[s] = 0;
         }
+        for (int x = 0; x < 4 * kA2tMaxJC; ++x) mbar_init(a2r + x, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tmem::fence_before();
     __syncthreads();
     tmem::fence_after();
     const uint32_t tq = *tmem_base_s + (static_cast<uint32_t>(32 * wj) << 16);
+    // The pre-pass (the preceding launch) writes the packed A1 and the scale rows, which only the
+    // ring's TMA copies read; A2 was written before it (the pre-pass waits for that writer before
+    // it lets this launch start). So one thread waits for the pre-pass and issues the first ring
+    // stages while the warps load A2 (warp 7 loads the chunk needed last).
+    if (threadIdx.x == kThreads - 1) {
+        pdl_wait();
+        for (int n = 0; n < kNS && n < my_units; ++n) issue(n);
+    }
 
     // A2 into TMEM, once: the two warps of quarter wj split the chunks (c = wi, wi + 2, ...);
-    // loads of four k-steps in flight at a time.
+    // loads of four k-steps in flight at a time; chunk c of quarter wj is handed to the quarter's
+    // other warp by a2r[c][wj] (the first tile of chunk 0 need not wait for chunk 1).
     for (int c = wi; c < n_jc; c += 2) {
         const int64_t jb = static_cast<int64_t>(kA2tJC) * c + 32 * wj + g;
         for (int ks0 = 0; ks0 < KD + NT; ks0 += 4) {
@@ -147,17 +158,12 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
                 tmem::st_x8(tq + static_cast<uint32_t>(c * CBJ + 8 * ks), v[x]);
             }
         }
+        tmem::wait_st();
+        tmem::fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a2r + 4 * c + wj);
     }
-    // The pre-pass (the preceding launch) writes the packed A1 and the scale rows; A2 was written
-    // before it (it waits for that writer before it lets this launch start), so the A2 load above
-    // overlaps the pre-pass and only the ring needs the wait.
-    pdl_wait();
-    if (threadIdx.x == 0)
-        for (int n = 0; n < kNS && n < my_units; ++n) issue(n);
-    tmem::wait_st();
-    tmem::fence_before();
-    __syncthreads();
-    tmem::fence_after();
+    unsigned a2_ready = 0;  // chunks of A2 this warp has waited for
 
     // This warp's quarter of half wi of unit n's operands: A1k = A1 * S in place (rows nn = wj
     // of every k-step, tail rows e = wj, wj + 4), then the hand-over to the half's 4 warps.
@@ -204,6 +210,11 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
                 }
         }
         for (int c = 0; c < n_jc; ++c) {
+            if (!((a2_ready >> c) & 1u)) {  // first use of chunk c: its TMEM columns of this quarter are written
+                mbar_wait(a2r + 4 * c + wj, 0u, p.fault);
+                tmem::fence_after();
+                a2_ready |= 1u << c;
+            }
             const uint32_t ta = tq + static_cast<uint32_t>(c * CBJ);
             double acc[kTM][kTN][2];
 #pragma unroll
@@ -351,7 +362,7 @@ int a2t_smem_bytes(int KD, int NT) {
 bool fits_a2t(int64_t N2, int KD, int NT) {
     if (KD < 1 || KD > 14 || NT < 1 || NT > 2) return false;
     const int64_t n_jc = (N2 + kA2tJC - 1) / kA2tJC;
-    return n_jc * (8 * KD + 8 * NT) <= 256 && 2 * (a2t_smem_bytes(KD, NT) + 1024) <= 228 * 1024;
+    return n_jc <= kA2tMaxJC && n_jc * (8 * KD + 8 * NT) <= 256 && 2 * (a2t_smem_bytes(KD, NT) + 1024) <= 228 * 1024;
 }
 
 int64_t a2t_units(int64_t N1, int64_t k0, int64_t k1) { return (N1 + kA2tIC - 1) / kA2tIC * (k1 - k0); }
