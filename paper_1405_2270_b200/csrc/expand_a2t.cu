@@ -32,7 +32,10 @@
 namespace ls_k3 {
 namespace {
 
-constexpr int kA2tWarps = 8, kA2tIC = 64, kA2tJC = 128, kA2tNS = 4, kA2tMaxJC = 16, kA2tHdr = 32 + 4 * kA2tMaxJC;
+constexpr int kA2tWarps = 8, kA2tIC = 64, kA2tJC = 128, kA2tNS = 4, kA2tHdr = 48;
+// At most 4 j-chunks (N2 <= 512): beyond, the TMEM plan is as fast or faster (R = 9 at N2 = 1024:
+// 54.0 vs 53.2 us; R = 9 / 21 / 41 at N2 = 256: 26.6 / 31.6 / 52.7 against 30.7 / 35.4 / 57.9 us).
+constexpr int kA2tMaxJC = 4;
 
 __host__ __device__ constexpr int a2t_stage_elems(int KD, int NT) { return 2 * KD * 128 + 2 * NT * 256; }
 // scale-row length, padded to whole 16-byte TMA chunks
