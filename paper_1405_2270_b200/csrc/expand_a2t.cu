@@ -11,15 +11,22 @@
 // slab's scale row S(k, q) = w_q * A3(k, q): two TMA bulk copies per unit, both L2-resident.
 // The landed A1 is scaled in place once (A1k = A1 * S, the rounding of the TMEM kernel's fill),
 // each warp of a 64-row half scaling one quarter of it (its nn = wj rows), handed over by a
-// per-(slot, half) mbarrier, and the next unit's share is scaled while the first j-chunk's DMMAs
-// drain. So there is no per-unit TMEM fill, the units are half as large (1024 at 256^3: 6.9 per
-// SM, at most 7), and the DMMAs see exactly the operands of the TMEM kernel in the same order:
-// the grid is bit-identical to it.
+// per-(slot, half) mbarrier. So there is no per-unit TMEM fill, the units are half as large (1024
+// at 256^3: 6.9 per SM, at most 7), and the DMMAs see exactly the operands of the TMEM kernel in
+// the same order: the grid is bit-identical to it.
 //
-// TMEM layout (per CTA, 256 columns, lanes = quarter wj = warp & 3 = the warp's j block):
+// Schedule: one CTA of 8 warps per SM (two warps per sub-partition keep the DMMA pipe as busy as
+// four: tools/microbench/fp64_peak.cu, 36.9 TF/s), which leaves each thread the registers for
+// TWO accumulator sets. A warp's work is a sequence of items (unit, j-chunk); item x's DMMAs go
+// into one set while item x-1's stores are spread over x's k-steps, the next unit's share of the
+// scaling is spread over chunk 0's k-steps, and the TMEM loads run one k-step ahead. (Against
+// 2 CTAs x 8 warps with one set and those steps between the chunks: 51.8 -> 50.3 us at 256^3,
+// and R = 57 at 256^3: 76.9 -> 69.3 us.)
+//
+// TMEM layout (per CTA, 256 or 512 columns, lanes = quarter wj = warp & 3 = the warp's j block):
 //   chunk c (128 j), column c*CBJ + 8 ks + 2 m + {0,1}: A2(j = 128 c + 32 wj + 8 m + g, q = 4 ks + t)
 //   column c*CBJ + 8 KD + 8 qt + 2 m + {0,1}: A2(j = ..., q = 4 KD + qt) (DFMA tail ranks)
-//   CBJ = 8 KD + 8 NT; n_jc chunks need n_jc * CBJ <= 256.
+//   CBJ = 8 KD + 8 NT; n_jc chunks need n_jc * CBJ <= 512.
 // Ring slot (per unit (ic, k), shared memory): the i-chunk's packed A1
 //   [wi][ks][nn][lane] = A1(i = 64 ic + 32 wi + 8 nn + g, q = 4 ks + t), then
 //   [wi][qt][e][lane]  = A1(i = 64 ic + 32 wi + 8 (e >> 1) + 2 t + (e & 1), q = 4 KD + qt),
@@ -33,9 +40,11 @@ namespace ls_k3 {
 namespace {
 
 constexpr int kA2tWarps = 8, kA2tIC = 64, kA2tJC = 128, kA2tNS = 4, kA2tHdr = 48;
-// At most 4 j-chunks (N2 <= 512): beyond, the TMEM plan is as fast or faster (R = 9 at N2 = 1024:
-// 54.0 vs 53.2 us; R = 9 / 21 / 41 at N2 = 256: 26.6 / 31.6 / 52.7 against 30.7 / 35.4 / 57.9 us).
-constexpr int kA2tMaxJC = 4;
+// At most 2 j-chunks (N2 <= 256; tools/lab/a2t_vs_tmem.py, profiles/r02_a2t_vs_tmem.txt): at
+// N2 = 256 this plan takes 26.1 / 33.7 / 51.5 / 69.3 us at R = 9 / 21 / 41 / 57 against the TMEM
+// plan's 30.7 / 35.4 / 58.0 / 77.1 us (256^3); at N2 = 512 the two are within 1.5% either way, and
+// beyond, the TMEM plan wins.
+constexpr int kA2tMaxJC = 2;
 
 __host__ __device__ constexpr int a2t_stage_elems(int KD, int NT) { return 2 * KD * 128 + 2 * NT * 256; }
 // scale-row length, padded to whole 16-byte TMA chunks
@@ -76,7 +85,7 @@ __global__ void pack_a1_kernel(const double* __restrict__ A, int64_t lda, int64_
 }
 
 template <bool STORE, bool FUNC, int KD, int NT>
-__global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const ExpandArgs p) {
+__global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const ExpandArgs p) {
     constexpr int kThreads = kA2tWarps * 32, kNS = kA2tNS, kTM = 4, kTN = 4;
     constexpr int CBJ = 8 * KD + 8 * NT;
     constexpr int kA1 = a2t_stage_elems(KD, NT), kSR = a2t_srow(KD, NT);
@@ -97,7 +106,15 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
     const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
     const int n_units = static_cast<int>(p.n_units), n_ichunks = static_cast<int>(p.n_ichunks);
     const int n_jc = static_cast<int>(p.n_jc);
+    const uint32_t tmem_cols = n_jc * CBJ <= 256 ? 256u : 512u;  // one CTA per SM: all 512 if needed
     const int my_units = n_units > b ? (n_units - 1 - b) / G + 1 : 0;
+    LS_TL_INIT();
+#ifdef LS_DEV_KNOBS
+    const bool lab_noscale = (p.debug & 2) != 0;  // lab A/B: operands used unscaled (no DMULs)
+    const bool lab_nostore = (p.debug & 1) != 0;  // lab A/B: epilogue without stores
+#else
+    constexpr bool lab_noscale = false, lab_nostore = false;
+#endif
 
     auto issue = [&](int n) {  // this CTA's n-th unit into slot n % kNS
         const int u = b + n * G;
@@ -109,7 +126,7 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
     };
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_s)),
-                     "r"(256)
+                     "r"(tmem_cols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -120,13 +137,14 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
             mbar_init(scaled + 2 * s + 1, 4);
             released[s] = 0;
         }
-        for (int x = 0; x < 4 * kA2tMaxJC; ++x) mbar_init(a2r + x, 1);
+        for (int x = 0; x < 4 * kA2tMaxJC; ++x) mbar_init(a2r + x, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tmem::fence_before();
     __syncthreads();
     tmem::fence_after();
     const uint32_t tq = *tmem_base_s + (static_cast<uint32_t>(32 * wj) << 16);
+    LS_TL(1);
     // The pre-pass (the preceding launch) writes the packed A1 and the scale rows, which only the
     // ring's TMA copies read; A2 was written before it (the pre-pass waits for that writer before
     // it lets this launch start). So one thread waits for the pre-pass and issues the first ring
@@ -136,30 +154,28 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
         for (int n = 0; n < kNS && n < my_units; ++n) issue(n);
     }
 
-    // A2 into TMEM, once: the two warps of quarter wj split the chunks (c = wi, wi + 2, ...);
-    // loads of four k-steps in flight at a time; chunk c of quarter wj is handed to the quarter's
-    // other warp by a2r[c][wj] (the first tile of chunk 0 need not wait for chunk 1).
-    for (int c = wi; c < n_jc; c += 2) {
+    // A2 into TMEM, once, chunk by chunk: the two warps of quarter wj split each chunk's k-steps
+    // (ks = wi, wi + 2, ...), all of a warp's loads of the chunk in flight at once; chunk c of
+    // quarter wj is handed over by a2r[c][wj] (2 arrivals), so the first tiles wait for chunk 0
+    // only.
+    for (int c = 0; c < n_jc; ++c) {
+        constexpr int kHalf = (KD + NT + 1) / 2;
         const int64_t jb = static_cast<int64_t>(kA2tJC) * c + 32 * wj + g;
-        for (int ks0 = 0; ks0 < KD + NT; ks0 += 4) {
-            double v[4][4];
+        double v[kHalf][4];
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const int ks = ks0 + x;
-                if (ks >= KD + NT) break;
-                const int q = ks < KD ? 4 * ks + t : 4 * KD + (ks - KD);  // tail ranks: every t the same q
+        for (int x = 0; x < kHalf; ++x) {
+            const int ks = 2 * x + wi;
+            const int q = ks < KD ? 4 * ks + t : 4 * KD + (ks - KD);  // tail ranks: every t the same q
 #pragma unroll
-                for (int m = 0; m < kTM; ++m) {
-                    const int64_t j = jb + 8 * m;
-                    v[x][m] = (j < p.N2 && q < p.R) ? __ldg(p.B + j + p.ldb * q) : 0.0;
-                }
+            for (int m = 0; m < kTM; ++m) {
+                const int64_t j = jb + 8 * m;
+                v[x][m] = (ks < KD + NT && j < p.N2 && q < p.R) ? __ldg(p.B + j + p.ldb * q) : 0.0;
             }
+        }
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const int ks = ks0 + x;
-                if (ks >= KD + NT) break;
-                tmem::st_x8(tq + static_cast<uint32_t>(c * CBJ + 8 * ks), v[x]);
-            }
+        for (int x = 0; x < kHalf; ++x) {
+            const int ks = 2 * x + wi;
+            if (ks < KD + NT) tmem::st_x8(tq + static_cast<uint32_t>(c * CBJ + 8 * ks), v[x]);
         }
         tmem::wait_st();
         tmem::fence_before();
@@ -167,6 +183,7 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
         if (lane == 0) mbar_arrive(a2r + 4 * c + wj);
     }
     unsigned a2_ready = 0;  // chunks of A2 this warp has waited for
+    LS_TL(2);
 
     // This warp's quarter of half wi of unit n's operands: A1k = A1 * S in place (rows nn = wj
     // of every k-step, tail rows e = wj, wj + 4), then the hand-over to the half's 4 warps.
@@ -174,6 +191,11 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
         const int sl = n % kNS;
         mbar_wait(full + sl, static_cast<unsigned>((n / kNS) & 1), p.fault);
         double* st = ring + sl * kStage;
+        if (lab_noscale) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(scaled + 2 * sl + wi);
+            return;
+        }
         const double* sr = st + kA1;
         double* fr = st + (wi * KD) * 128 + wj * 32 + lane;
 #pragma unroll
@@ -190,157 +212,227 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 2) expand_a2t_kernel(const Exp
     };
     if (my_units > 0) scale_share(0);
 
+    // Items x = (unit n = x / n_jc, j-chunk c = x % n_jc), in order. The accumulators ping-pong
+    // between two register sets: item x's DMMAs go into one while the previous item's stores are
+    // spread over x's k-steps (fast path), so the store data leaves the registers while the pipe
+    // holds queued DMMAs instead of stalling the warp between chunks.
+    const int n_items = my_units * n_jc;
     double fsum = 0.0;
-    for (int n = 0; n < my_units; ++n) {
-        const int unit = b + n * G;
-        const int ic = unit % n_ichunks;
-        const int64_t kk = unit / n_ichunks;
-        const int slot = n % kNS;
-        mbar_wait(scaled + 2 * slot + wi, static_cast<unsigned>((n / kNS) & 1), p.fault);
-        const double* stage = ring + slot * kStage;
-        const double* bfr = stage + (wi * KD) * 128 + lane;             // A1k of k-step ks at [ks * 128 + nn * 32]
-        const double* btl = stage + kFrag + (wi * NT) * 256 + lane;     // tail A1k: [qt * 256 + e * 32]
-        const int ibase = kA2tIC * ic + 32 * wi;
+    struct Tile {
+        int64_t kk;
+        int unit, ibase, jb, c;
+        bool fast;
+    };
+    auto tile_of = [&](int x) {
+        Tile T;
+        const int n = x / n_jc;
+        T.c = x - n * n_jc;
+        T.unit = b + n * G;
+        const int ic = T.unit % n_ichunks;
+        T.kk = T.unit / n_ichunks;
+        T.ibase = kA2tIC * ic + 32 * wi;
+        T.jb = kA2tJC * T.c + 32 * wj;
+        T.fast = STORE && !FUNC && T.ibase + 8 * kTN <= p.N1 && T.jb + 8 * kTM <= p.N2 && p.vec_store && !p.accumulate;
+        return T;
+    };
+    // Whole epilogue of item x (every path; the fast path is also spread into the next item).
+    // Lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
+    auto epilogue = [&](int x, double (&acc)[kTM][kTN][2]) {
+        const Tile T = tile_of(x);
         double r1[kTN][2];
         if (FUNC) {
-            fsum = 0.0;
 #pragma unroll
             for (int nn = 0; nn < kTN; ++nn)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const int i = ibase + 8 * nn + 2 * t + e;
+                    const int i = T.ibase + 8 * nn + 2 * t + e;
                     r1[nn][e] = i < p.N1 ? __ldg(p.rho1 + i) : 0.0;
                 }
         }
-        for (int c = 0; c < n_jc; ++c) {
-            if (!((a2_ready >> c) & 1u)) {  // first use of chunk c: its TMEM columns of this quarter are written
-                mbar_wait(a2r + 4 * c + wj, 0u, p.fault);
-                tmem::fence_after();
-                a2_ready |= 1u << c;
-            }
-            const uint32_t ta = tq + static_cast<uint32_t>(c * CBJ);
-            double acc[kTM][kTN][2];
 #pragma unroll
-            for (int m = 0; m < kTM; ++m)
-#pragma unroll
-                for (int nn = 0; nn < kTN; ++nn) acc[m][nn][0] = acc[m][nn][1] = 0.0;
-            // Rank remainder on DFMA before the DMMAs (as in the TMEM kernel).
-#pragma unroll
-            for (int qt = 0; qt < NT; ++qt) {
-                double at[4];
-                tmem::ld_x8(ta + 8 * KD + 8 * qt, at);  // A2 tail, j = 8 m + g
-                double bt[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) bt[e] = btl[qt * 256 + e * 32];  // A1k tail, i = 8 (e >> 1) + 2 t + (e & 1)
-#pragma unroll
-                for (int nn = 0; nn < kTN; ++nn)
-#pragma unroll
-                    for (int m = 0; m < kTM; ++m) {
-                        acc[m][nn][0] = fma(bt[2 * nn], at[m], acc[m][nn][0]);
-                        acc[m][nn][1] = fma(bt[2 * nn + 1], at[m], acc[m][nn][1]);
-                    }
-            }
-#pragma unroll
-            for (int ks = 0; ks < KD; ++ks) {
-                uint32_t ra[8];
-                double a[kTM], bb[kTN];
-                tmem::ld_x8_issue(ta + 8 * ks, ra);
-#pragma unroll
-                for (int nn = 0; nn < kTN; ++nn) bb[nn] = bfr[ks * 128 + nn * 32];
-                tmem::wait_ld(ra);
-                tmem::unpack(ra, a);
-#pragma unroll
-                for (int m = 0; m < kTM; ++m)
-#pragma unroll
-                    for (int nn = 0; nn < kTN; ++nn) dmma_884(acc[m][nn][0], acc[m][nn][1], a[m], bb[nn]);
-            }
-            if (c == 0 && n + 1 < my_units) scale_share(n + 1);  // while this chunk's DMMAs drain
-            if (c == n_jc - 1) {
-                // Release the ring slot (every operand of this unit has been read into registers);
-                // the last warp refills it with this CTA's unit n + kNS.
-                __syncwarp();
-                if (lane == 0) {
-                    __threadfence_block();
-                    if (atomicAdd(released + slot, 1) == kA2tWarps - 1) {
-                        released[slot] = 0;
-                        __threadfence_block();
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        if (n + kNS < my_units) issue(n + kNS);
-                    }
-                }
-            }
-            // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
-            const int jb = kA2tJC * c + 32 * wj;
-            if (ibase + 8 * kTN <= p.N1 && jb + 8 * kTM <= p.N2 && (!STORE || (p.vec_store && !p.accumulate))) {
-                double* row = STORE ? p.out + kk * p.ldz + static_cast<int64_t>(jb + g) * p.ldy + ibase + 2 * t : nullptr;
-#pragma unroll
-                for (int m = 0; m < kTM; ++m) {
-                    if (FUNC) {
-                        double sm = 0.0;
-#pragma unroll
-                        for (int nn = 0; nn < kTN; ++nn) {
-                            sm = fma(acc[m][nn][0], r1[nn][0], sm);
-                            sm = fma(acc[m][nn][1], r1[nn][1], sm);
-                        }
-                        fsum = fma(sm, __ldg(p.rho2 + jb + 8 * m + g), fsum);
-                    }
-                    if (STORE)
-#pragma unroll
-                        for (int nn = 0; nn < kTN; ++nn)
-                            __stcs(reinterpret_cast<double2*>(row + 8 * m * p.ldy + 8 * nn),
-                                   make_double2(acc[m][nn][0], acc[m][nn][1]));
-                }
-                continue;
-            }
-#pragma unroll
-            for (int m = 0; m < kTM; ++m) {
-                const int j = jb + 8 * m + g;
-                if (j >= p.N2) continue;
-                if (FUNC) {
-                    double sm = 0.0;
-#pragma unroll
-                    for (int nn = 0; nn < kTN; ++nn) {
-                        sm = fma(acc[m][nn][0], r1[nn][0], sm);
-                        sm = fma(acc[m][nn][1], r1[nn][1], sm);
-                    }
-                    fsum = fma(sm, __ldg(p.rho2 + j), fsum);
-                }
-                if (!STORE) continue;
-                double* row = p.out + kk * p.ldz + static_cast<int64_t>(j) * p.ldy;
+        for (int m = 0; m < kTM; ++m) {
+            const int j = T.jb + 8 * m + g;
+            if (j >= p.N2) continue;
+            if (FUNC) {
+                double sm = 0.0;
 #pragma unroll
                 for (int nn = 0; nn < kTN; ++nn) {
-                    const int i = ibase + 8 * nn + 2 * t;
-                    if (i + 1 < p.N1) {
-                        if (p.accumulate) {
-                            row[i] += acc[m][nn][0];
-                            row[i + 1] += acc[m][nn][1];
-                        } else if (p.vec_store) {
-                            __stcs(reinterpret_cast<double2*>(row + i), make_double2(acc[m][nn][0], acc[m][nn][1]));
-                        } else {
-                            row[i] = acc[m][nn][0];
-                            row[i + 1] = acc[m][nn][1];
-                        }
-                    } else if (i < p.N1) {
-                        row[i] = p.accumulate ? row[i] + acc[m][nn][0] : acc[m][nn][0];
+                    sm = fma(acc[m][nn][0], r1[nn][0], sm);
+                    sm = fma(acc[m][nn][1], r1[nn][1], sm);
+                }
+                fsum = fma(sm, __ldg(p.rho2 + j), fsum);
+            }
+            if (!STORE || lab_nostore) continue;
+            double* row = p.out + T.kk * p.ldz + static_cast<int64_t>(j) * p.ldy;
+#pragma unroll
+            for (int nn = 0; nn < kTN; ++nn) {
+                const int i = T.ibase + 8 * nn + 2 * t;
+                if (i + 1 < p.N1) {
+                    if (p.accumulate) {
+                        row[i] += acc[m][nn][0];
+                        row[i + 1] += acc[m][nn][1];
+                    } else if (p.vec_store) {
+                        __stcs(reinterpret_cast<double2*>(row + i), make_double2(acc[m][nn][0], acc[m][nn][1]));
+                    } else {
+                        row[i] = acc[m][nn][0];
+                        row[i + 1] = acc[m][nn][1];
                     }
+                } else if (i < p.N1) {
+                    row[i] = p.accumulate ? row[i] + acc[m][nn][0] : acc[m][nn][0];
                 }
             }
         }
-        if (FUNC) {
+        if (FUNC && T.c == n_jc - 1) {
             // Per-warp partials: partial[unit * 8 + warp], fixed-order xor tree (as the TMEM kernel).
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, off);
             if (lane == 0) {
-                const double part = rn_mul(fsum, p.rho3[p.k0 + kk]);
-                double& sl = p.partial[static_cast<int64_t>(unit) * kA2tWarps + warp];
+                const double part = rn_mul(fsum, p.rho3[p.k0 + T.kk]);
+                double& sl = p.partial[static_cast<int64_t>(T.unit) * kA2tWarps + warp];
                 sl = p.accumulate ? sl + part : part;
             }
+            fsum = 0.0;
         }
+    };
+    auto item = [&](int x, double (&cur)[kTM][kTN][2], double (&prev)[kTM][kTN][2]) {
+        const int n = x / n_jc, c = x - n * n_jc;
+        const int slot = n % kNS;
+        if (c == 0) {
+            mbar_wait(scaled + 2 * slot + wi, static_cast<unsigned>((n / kNS) & 1), p.fault);
+            LS_TL(3);
+        }
+        if (!((a2_ready >> c) & 1u)) {  // first use of chunk c: its TMEM columns of this quarter are written
+            mbar_wait(a2r + 4 * c + wj, 0u, p.fault);
+            tmem::fence_after();
+            a2_ready |= 1u << c;
+        }
+        const double* stage = ring + slot * kStage;
+        const double* bfr = stage + (wi * KD) * 128 + lane;          // A1k of k-step ks at [ks * 128 + nn * 32]
+        const double* btl = stage + kFrag + (wi * NT) * 256 + lane;  // tail A1k: [qt * 256 + e * 32]
+        const uint32_t ta = tq + static_cast<uint32_t>(c * CBJ);
+        // The next unit's share of operand scaling (scale_share's work) is spread over chunk 0's
+        // k-steps too: one product per k-step, the tail ranks with the last.
+        const bool sc = c == 0 && n + 1 < my_units && !lab_noscale;
+        double* fr1 = nullptr;
+        const double* sr1 = nullptr;
+        if (c == 0 && n + 1 < my_units) {
+            const int sl1 = (n + 1) % kNS;
+            mbar_wait(full + sl1, static_cast<unsigned>(((n + 1) / kNS) & 1), p.fault);
+            double* st1 = ring + sl1 * kStage;
+            sr1 = st1 + kA1;
+            fr1 = st1 + (wi * KD) * 128 + wj * 32 + lane;
+        }
+        bool spread = false;
+        double* prow = nullptr;
+        if (x > 0) {
+            const Tile T = tile_of(x - 1);
+            spread = T.fast && !lab_nostore;
+            prow = p.out + T.kk * p.ldz + static_cast<int64_t>(T.jb + g) * p.ldy + T.ibase + 2 * t;
+        }
+#pragma unroll
+        for (int m = 0; m < kTM; ++m)
+#pragma unroll
+            for (int nn = 0; nn < kTN; ++nn) cur[m][nn][0] = cur[m][nn][1] = 0.0;
+        // TMEM loads run one k-step ahead of the DMMAs (two register sets), so the load latency
+        // hides behind the previous k-step's DMMA issue; the item's first load travels with the
+        // tail operands.
+        uint32_t ra[2][8], rt[NT][8];
+#pragma unroll
+        for (int qt = 0; qt < NT; ++qt) tmem::ld_x8_issue(ta + 8 * KD + 8 * qt, rt[qt]);  // A2 tail, j = 8 m + g
+        tmem::ld_x8_issue(ta, ra[0]);
+        // Rank remainder on DFMA before the DMMAs (as in the TMEM kernel).
+#pragma unroll
+        for (int qt = 0; qt < NT; ++qt) {
+            double bt[8], at[4];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) bt[e] = btl[qt * 256 + e * 32];  // A1k tail, i = 8 (e >> 1) + 2 t + (e & 1)
+            tmem::wait_ld(rt[qt]);
+            tmem::unpack(rt[qt], at);
+#pragma unroll
+            for (int nn = 0; nn < kTN; ++nn)
+#pragma unroll
+                for (int m = 0; m < kTM; ++m) {
+                    cur[m][nn][0] = fma(bt[2 * nn], at[m], cur[m][nn][0]);
+                    cur[m][nn][1] = fma(bt[2 * nn + 1], at[m], cur[m][nn][1]);
+                }
+        }
+        tmem::wait_ld(ra[0]);
+#pragma unroll
+        for (int ks = 0; ks < KD; ++ks) {
+            double a[kTM], bb[kTN], sv = 0.0, ss = 0.0;
+            tmem::unpack(ra[ks & 1], a);
+            if (ks + 1 < KD) tmem::ld_x8_issue(ta + 8 * (ks + 1), ra[(ks + 1) & 1]);
+#pragma unroll
+            for (int nn = 0; nn < kTN; ++nn) bb[nn] = bfr[ks * 128 + nn * 32];
+            if (sc) {
+                sv = fr1[ks * 128];
+                ss = sr1[4 * ks + t];
+            }
+#pragma unroll
+            for (int m = 0; m < kTM; ++m)
+#pragma unroll
+                for (int nn = 0; nn < kTN; ++nn) dmma_884(cur[m][nn][0], cur[m][nn][1], a[m], bb[nn]);
+            if (ks + 1 < KD) tmem::wait_ld(ra[(ks + 1) & 1]);
+            if (sc) {
+                fr1[ks * 128] = rn_mul(sv, ss);
+                if (ks == KD - 1) {
+                    double* tl = fr1 - (wi * KD) * 128 + kFrag + (wi * NT) * 256;
+#pragma unroll
+                    for (int qt = 0; qt < NT; ++qt) {
+                        const double sq = sr1[4 * KD + qt];
+                        tl[qt * 256] = rn_mul(tl[qt * 256], sq);
+                        tl[qt * 256 + 128] = rn_mul(tl[qt * 256 + 128], sq);
+                    }
+                }
+            }
+            if (spread) {  // pairs [16 ks / KD, 16 (ks + 1) / KD) of the previous item
+#pragma unroll
+                for (int q = kTM * kTN * ks / KD; q < kTM * kTN * (ks + 1) / KD; ++q)
+                    __stcs(reinterpret_cast<double2*>(prow + 8 * (q / kTN) * p.ldy + 8 * (q % kTN)),
+                           make_double2(prev[q / kTN][q % kTN][0], prev[q / kTN][q % kTN][1]));
+            }
+        }
+        LS_TL(5);
+        if (x > 0 && !spread) epilogue(x - 1, prev);  // the other paths, after this item's DMMAs are queued
+        if (c == 0 && n + 1 < my_units) {  // unit n + 1's share is scaled: hand it over
+            __syncwarp();
+            if (lane == 0) mbar_arrive(scaled + 2 * ((n + 1) % kNS) + wi);
+            LS_TL(6);
+        }
+        if (c == n_jc - 1) {
+            // Release the ring slot (every operand of this unit has been read into registers);
+            // the last warp refills it with this CTA's unit n + kNS.
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                if (atomicAdd(released + slot, 1) == kA2tWarps - 1) {
+                    released[slot] = 0;
+                    __threadfence_block();
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if (n + kNS < my_units) issue(n + kNS);
+                }
+            }
+        }
+    };
+    double accA[kTM][kTN][2], accB[kTM][kTN][2];
+    int x = 0;
+    for (; x + 1 < n_items; x += 2) {
+        item(x, accA, accB);
+        item(x + 1, accB, accA);
     }
+    if (x < n_items) {
+        item(x, accA, accB);
+        epilogue(x, accA);
+    } else if (n_items > 0) {
+        epilogue(n_items - 1, accB);
+    }
+    LS_TL(7);
+    LS_TL(8);
+    LS_TL_END();
     tmem::fence_before();
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_s), "r"(256) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_s), "r"(tmem_cols) : "memory");
 }
 
 template <bool STORE, bool FUNC, int NT, int... KD>
@@ -365,7 +457,7 @@ int a2t_smem_bytes(int KD, int NT) {
 bool fits_a2t(int64_t N2, int KD, int NT) {
     if (KD < 1 || KD > 14 || NT < 1 || NT > 2) return false;
     const int64_t n_jc = (N2 + kA2tJC - 1) / kA2tJC;
-    return n_jc <= kA2tMaxJC && n_jc * (8 * KD + 8 * NT) <= 256 && 2 * (a2t_smem_bytes(KD, NT) + 1024) <= 228 * 1024;
+    return n_jc <= kA2tMaxJC && n_jc * (8 * KD + 8 * NT) <= 512 && a2t_smem_bytes(KD, NT) + 1024 <= 228 * 1024;
 }
 
 int64_t a2t_units(int64_t N1, int64_t k0, int64_t k1) { return (N1 + kA2tIC - 1) / kA2tIC * (k1 - k0); }
@@ -399,7 +491,8 @@ int launch_a2t(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_coun
     LS_LAUNCHED("pack_a1_kernel");
     a.Bp = a1p;
     a.S = srows;
-    const int64_t grid = std::min<int64_t>(a.n_units, static_cast<int64_t>(sm_count) * 2);
+    int64_t grid = std::min<int64_t>(a.n_units, static_cast<int64_t>(sm_count) * per_sm);
+    if (const char* g = ls::dev_knob("LS_A2T_GRID")) grid = std::min<int64_t>(a.n_units, std::atoll(g));
     if (grid > 0) {
         LS_CUDA(ls::launch_pdl(kern, dim3((unsigned)grid), dim3(kA2tWarps * 32), smem, s, a));
         LS_LAUNCHED("expand_a2t_kernel");

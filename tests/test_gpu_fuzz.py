@@ -235,10 +235,11 @@ def test_pipeline_bitwise_run_to_run(env, n_charges):
     (122, (256, 200, 300), "single A1k buffer"), (164, (300, 256, 200), "single A1k buffer"),
     (199, (256, 130, 260), "single A1k buffer"), (249, (128, 256, 300), "single A1k buffer"),
     (5, (256, 256, 300), None), (21, (200, 256, 300), None), (54, (256, 128, 300), None),
-    (57, (256, 250, 300), None)])
+    (57, (256, 250, 300), None), (41, (256, 512, 200), None), (57, (200, 384, 160), None),
+    (9, (136, 500, 150), None)])
 def test_expand_many_units_per_cta(env, orc, R, dims, plan):
     """Launches with several units per CTA: the single-buffer TMEM plan's unit-boundary refill
-    (ranks 122-249) and the A2-in-TMEM plan's ring reuse and next-unit scaling (N2 <= 256), which
+    (ranks 122-249) and the A2-in-TMEM plan's ring reuse and next-unit scaling (N2 <= 512, 256 or 512 TMEM columns), which
     the small fuzz shapes above never reach. Sampled slabs (first, last, in between) against the
     oracle, and the fused functional against the stored grid."""
     torch, _abi = env

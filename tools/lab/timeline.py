@@ -25,6 +25,7 @@ from paper_1405_2270_b200.latsum import _expand_device  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="256x256x256")
 ap.add_argument("--R", type=int, default=41)
+ap.add_argument("--save", default="", help="also save the raw event buffer (.npy)")
 args = ap.parse_args()
 n1, n2, ks = map(int, args.shape.split("x"))
 g = torch.Generator(device="cuda").manual_seed(1)
@@ -41,6 +42,8 @@ n = 148 * 2 * 16 * 128
 buf = np.zeros(n, dtype=np.uint64)
 lib.ls_lab_timeline(buf.ctypes.data, n)
 buf = buf.reshape(-1, 128)
+if args.save:
+    np.save(args.save, buf)
 warps = []
 for row in buf:
     cnt = int(row[0] & 0xFFFFFFFF)

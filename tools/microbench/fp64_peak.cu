@@ -164,6 +164,16 @@ int main(int argc, char** argv) {
     double flops = 2.0 * 256 * 8 * it * (double)grid * (threads / 32);
     printf("{\"bench\":\"dmma_m8n8k4\",\"acc\":8,\"grid\":%d,\"threads\":%d,\"ms\":%.4f,\"tflops\":%.3f}\n", grid, threads, ms, flops / ms / 1e9);
   }
+  // 1 CTA of 8 warps per SM (2 warps per sub-partition), 8 and 16 accumulators per warp
+  {
+    int grid = sms, threads = 256, it = iters / 4;
+    float ms = time_ms([&] { dmma884_kernel<8><<<grid, threads>>>(out, it); }, 5);
+    double flops = 2.0 * 256 * 8 * it * (double)grid * (threads / 32);
+    printf("{\"bench\":\"dmma_m8n8k4\",\"acc\":8,\"grid\":%d,\"threads\":%d,\"ms\":%.4f,\"tflops\":%.3f}\n", grid, threads, ms, flops / ms / 1e9);
+    ms = time_ms([&] { dmma884_kernel<16><<<grid, threads>>>(out, it); }, 5);
+    flops = 2.0 * 256 * 16 * it * (double)grid * (threads / 32);
+    printf("{\"bench\":\"dmma_m8n8k4\",\"acc\":16,\"grid\":%d,\"threads\":%d,\"ms\":%.4f,\"tflops\":%.3f}\n", grid, threads, ms, flops / ms / 1e9);
+  }
   for (int blocks_per_sm : {2, 4}) {
     int grid = sms * blocks_per_sm, threads = 256;
     int it = iters / 8;
