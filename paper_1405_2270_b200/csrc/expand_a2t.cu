@@ -155,32 +155,39 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
     }
 
     // A2 into TMEM, once, chunk by chunk: the two warps of quarter wj split each chunk's k-steps
-    // (ks = wi, wi + 2, ...), all of a warp's loads of the chunk in flight at once; chunk c of
-    // quarter wj is handed over by a2r[c][wj] (2 arrivals), so the first tiles wait for chunk 0
-    // only.
-    for (int c = 0; c < n_jc; ++c) {
+    // (ks = wi, wi + 2, ...), all of a warp's loads of both chunks in flight at once (256^3:
+    // 50.9 -> 50.4 us against chunk by chunk); chunk c of quarter wj is handed over by a2r[c][wj]
+    // (2 arrivals), so the first tiles wait for chunk 0 only.
+    {
         constexpr int kHalf = (KD + NT + 1) / 2;
-        const int64_t jb = static_cast<int64_t>(kA2tJC) * c + 32 * wj + g;
-        double v[kHalf][4];
+        double v[kA2tMaxJC][kHalf][4];  // every chunk's loads in flight before the first TMEM store
 #pragma unroll
-        for (int x = 0; x < kHalf; ++x) {
-            const int ks = 2 * x + wi;
-            const int q = ks < KD ? 4 * ks + t : 4 * KD + (ks - KD);  // tail ranks: every t the same q
+        for (int c = 0; c < kA2tMaxJC; ++c) {
+            const int64_t jb = static_cast<int64_t>(kA2tJC) * c + 32 * wj + g;
 #pragma unroll
-            for (int m = 0; m < kTM; ++m) {
-                const int64_t j = jb + 8 * m;
-                v[x][m] = (ks < KD + NT && j < p.N2 && q < p.R) ? __ldg(p.B + j + p.ldb * q) : 0.0;
+            for (int x = 0; x < kHalf; ++x) {
+                const int ks = 2 * x + wi;
+                const int q = ks < KD ? 4 * ks + t : 4 * KD + (ks - KD);  // tail ranks: every t the same q
+#pragma unroll
+                for (int m = 0; m < kTM; ++m) {
+                    const int64_t j = jb + 8 * m;
+                    v[c][x][m] = (c < n_jc && ks < KD + NT && j < p.N2 && q < p.R) ? __ldg(p.B + j + p.ldb * q) : 0.0;
+                }
             }
         }
 #pragma unroll
-        for (int x = 0; x < kHalf; ++x) {
-            const int ks = 2 * x + wi;
-            if (ks < KD + NT) tmem::st_x8(tq + static_cast<uint32_t>(c * CBJ + 8 * ks), v[x]);
+        for (int c = 0; c < kA2tMaxJC; ++c) {
+            if (c >= n_jc) break;
+#pragma unroll
+            for (int x = 0; x < kHalf; ++x) {
+                const int ks = 2 * x + wi;
+                if (ks < KD + NT) tmem::st_x8(tq + static_cast<uint32_t>(c * CBJ + 8 * ks), v[c][x]);
+            }
+            tmem::wait_st();
+            tmem::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a2r + 4 * c + wj);
         }
-        tmem::wait_st();
-        tmem::fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(a2r + 4 * c + wj);
     }
     unsigned a2_ready = 0;  // chunks of A2 this warp has waited for
     LS_TL(2);

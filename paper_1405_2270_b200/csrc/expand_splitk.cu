@@ -12,7 +12,10 @@
 // deterministic. A2 streams through a 2-deep TMA ring of stages holding KC k-steps of both
 // halves for 16 j-tiles; a tile takes ceil(KH / KC) stages, its accumulators carried across
 // them. The next unit's A1k is written after a CTA barrier (single buffer): about 1% of a unit
-// at cfg3.
+// at cfg3. The DFMA rank remainder runs on half 1 when KD is odd (its half is a k-step shorter)
+// and otherwise on the tile's writer (the reducer has the add and the epilogue); with R mod 4 = 0
+// a zero rank still runs there: without it ranks 251 / 256 ran 7% / 6% slower, the effect the
+// TMEM kernel's zero rank shows too (r02 A/B at 1024^2 x 64: ranks 250-350 +0.7-7.8%, cfg3 +0.3%).
 #include <utility>
 
 #include "expand_tmem.cuh"
@@ -149,9 +152,16 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
     const int CB = 8 * KH + 16 * n_tail;
     const bool dbuf = 2 * CB <= 512;
     // This warp's fill tasks of a unit: frag task f writes k-step kl = wj + 4 f of its half (the
-    // four i-tiles of its rows); then (kh == 0, wj == 0) one task per tail rank.
+    // four i-tiles of its rows); then (wj == 0, in the halves that run the tail) one task per
+    // tail rank.
     const int n_frag_tasks = nks > wj ? (nks - wj + 3) / 4 : 0;
-    const int n_tasks = n_frag_tasks + ((kh == 0 && wj == 0) ? n_tail : 0);
+    // The DFMA rank remainder goes where it balances the pair: with KD odd half 1 (one k-step
+    // fewer) always takes it; with KD even the tile's writer does (the reducer has the add and
+    // the epilogue). Both halves' quarters then hold the tail columns.
+    const bool tail_fixed = (KD & 1) != 0;
+    auto tail_here = [&](int tl) { return tail_fixed ? kh == 1 : kh != (tl & 1); };
+    const bool holds_tail = tail_fixed ? kh == 1 : true;
+    const int n_tasks = n_frag_tasks + ((holds_tail && wj == 0) ? n_tail : 0);
     // Tasks [t0, t1) of unit u into buffer buf. Rounds like Eigen's A1 * scale.asDiagonal().
     auto fill = [&](int u, int buf, int t0, int t1) {
         const int ib = (u % n_ichunks) * kSkIC + 32 * rg;
@@ -234,8 +244,8 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
                 for (int m = 0; m < kTM; ++m)
 #pragma unroll
                     for (int nn = 0; nn < kTN; ++nn) acc[m][nn][0] = acc[m][nn][1] = 0.0;
-                if (kh == 0) {
-                    // the rank remainder on DFMA (half 0 only)
+                if (tail_here(tile)) {
+                    // the rank remainder on DFMA (one half per tile)
                     for (int qt = 0; qt < n_tail; ++qt) {
                         const double* tbp = stage + frag_elems + jt0 * 8 * n_tail + qt * 8 + g;
                         double bt[kTM];
@@ -276,11 +286,12 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) expand_splitk_kernel(const E
             }
             // release the ring slot; the last warp refills it
             __syncwarp();
+            // No CTA memory barrier here: it would wait for the warp's outstanding grid stores.
+            // The slot's operands were all read into registers (the DMMAs above consumed them),
+            // so the counter only has to order those reads before the refill.
             if (lane == 0) {
-                __threadfence_block();
                 if (atomicAdd(released + slot, 1) == WARPS - 1) {
                     released[slot] = 0;
-                    __threadfence_block();
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     if (st + kSkNS < n_stages) issue(st + kSkNS);
                 }
@@ -422,6 +433,7 @@ int launch_splitk(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_c
     a.n_jc = ls::ceil_div(a.N2, 8 * kSkJT);
     a.n_jt = a.n_jc * kSkJT;
     a.split_tail = 0;
+    if (a.n_tail == 0) a.n_tail = 1;  // a zero DFMA rank on the tile's writer (see the kernel)
     if (a.n_units * a.n_jc * n_kc >= (int64_t(1) << 31) || a.N1 + kSkIC >= (int64_t(1) << 31))
         return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
     const size_t stage_elems = static_cast<size_t>(2 * kSkJT * kSkKC * 32 + kSkJT * 8 * a.n_tail);

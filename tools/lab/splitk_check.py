@@ -9,7 +9,7 @@ import torch  # noqa: E402
 from paper_1405_2270_b200.latsum import _expand_device  # noqa: E402
 
 g = torch.Generator(device="cuda").manual_seed(3)
-for R in (176, 200, 240, 328, 332):
+for R in (176, 200, 240, 250, 251, 253, 255, 301, 328, 331, 332, 350):
     n1, n2, ks = 200, 136, 3
     fac = [torch.rand((R, m), dtype=torch.float64, device="cuda", generator=g) for m in (n1, n2, ks)]
     w = torch.rand(R, dtype=torch.float64, device="cuda", generator=g)

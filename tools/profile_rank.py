@@ -5,7 +5,7 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").environ.get("LS_LAB_ROOT", "/root/repo"))
 import paper_1405_2270_b200 as L  # noqa: E402
 
 rng = np.random.default_rng(20241019)
