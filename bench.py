@@ -220,8 +220,7 @@ def run_ours(args, rank, world, local_rank):
         clk.mark()
         t_start.record(stream)
         for s in range(args.steps):
-            pipe.generate(stream)
-            pipe.assemble(stream)
+            pipe.prepare(stream)  # generator + assembly (one launch on small lattices)
             ev[s][0].record(stream)
             pipe.expand(out, k0, k1, stream)
             ev[s][1].record(stream)
@@ -427,7 +426,7 @@ def run_other_configs(L, dev):
     N = pipe.dims
     k1 = N[2] // 8
     shard = torch.empty((k1, N[1], N[0]), dtype=torch.float64, device=dev)
-    t_asm, how_asm = _graph_ms(lambda: (pipe.generate(), pipe.assemble()))
+    t_asm, how_asm = _graph_ms(pipe.prepare)
     t_exp = _ev_ms(lambda: pipe.expand(shard, 0, k1))
     out["cfg3"] = {"grid": list(N), "rank": pipe.Rt, "generator_plus_assembly_ms": round(t_asm, 4),
                    "shard8_expand_ms": round(t_exp, 3),
@@ -440,7 +439,7 @@ def run_other_configs(L, dev):
     rule = L.sinc_quadrature(EPS, spec.unit.h, math.sqrt(3.0) * 256 * B, M_QUAD, C0)
     pipe = L.DevicePipeline(spec, rule, mode="erf", periodic=True, device=dev)
     grid = torch.empty(tuple(reversed(pipe.dims)), dtype=torch.float64, device=dev)
-    t_asm, how_asm = _graph_ms(lambda: (pipe.generate(), pipe.assemble()))
+    t_asm, how_asm = _graph_ms(pipe.prepare)
     t_exp = _ev_ms(lambda: pipe.expand(grid))
     rng = np.random.default_rng(4)
     F = 1024

@@ -63,6 +63,8 @@ public:
     // Stages on `stream` (a cudaStream_t; nullptr = default stream), asynchronous.
     void generate(void* stream = nullptr) { cuda::check(ls_pipeline_generate(h_, stream), "generate"); }
     void assemble(void* stream = nullptr) { cuda::check(ls_pipeline_assemble(h_, stream), "assemble"); }
+    // generate + assemble (one launch on small lattices); what step() runs before the expansion.
+    void prepare(void* stream = nullptr) { cuda::check(ls_pipeline_prepare(h_, stream), "prepare"); }
     // Slabs [k0, k1) into device memory out_d ((k1-k0)*N1*N2 doubles, i-fastest).
     void expand(Index k0, Index k1, double* out_d, void* stream = nullptr) {
         cuda::check(ls_pipeline_expand(h_, k0, k1, out_d, stream), "expand");

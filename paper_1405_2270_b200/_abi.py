@@ -79,6 +79,7 @@ SIGNATURES = {
     "ls_pipeline_info": (_i, [_vp, _vp, C.POINTER(_i), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
     "ls_pipeline_generate": (_i, [_vp, _vp]),
     "ls_pipeline_assemble": (_i, [_vp, _vp]),
+    "ls_pipeline_prepare": (_i, [_vp, _vp]),
     "ls_pipeline_expand": (_i, [_vp, _i64, _i64, _vp, _vp]),
     "ls_pipeline_step": (_i, [_vp, _i64, _i64, _vp, _vp]),
     "ls_pipeline_energy": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp]),

@@ -854,6 +854,8 @@ int lattice_impl(int mode, const int64_t L[3], int64_t n, double b, const double
     LS_TRY(ls::upload(wd, wt.data(), sizeof(double) * wt.size(), s));
     const double* fptr[3];
     double* fh[3] = {f0_h, f1_h, f2_h};
+    ls::GenAsmAxis ax[3];
+    int n_ax = 0;
     for (int l = 0; l < 3; ++l) {
         // Axes with equal L and equal charge indices yield bit-identical factors.
         int same = -1;
@@ -867,12 +869,12 @@ int lattice_impl(int mode, const int64_t L[3], int64_t n, double b, const double
         }
         const int64_t len = 2 * L[l] * n;
         LS_TRY(master[l].alloc(sizeof(double) * len * R, s));
-        LS_TRY(ls_gen_master(mode, tau.d(), R, len, h, master[l].d(), len, s));
         LS_TRY(fac[l].alloc(sizeof(double) * d[l] * Rt, s));
-        LS_TRY(ls_assemble_axis(master[l].d(), len, R, M0, iad.i() + l * M0, n, L[l], periodic,
-                                fac[l].d(), d[l], s));
+        ax[n_ax++] = {L[l], iad.i() + l * M0, master[l].d(), fac[l].d()};
         fptr[l] = fac[l].d();
     }
+    // generator + assembled sum (one launch on small lattices)
+    LS_TRY(ls::gen_assemble(mode, tau.d(), R, M0, n, h, periodic, ax, n_ax, s));
     for (int l = 0; l < 3; ++l)
         if (fh[l]) LS_CUDA(cudaMemcpyAsync(fh[l], fptr[l], sizeof(double) * d[l] * Rt, cudaMemcpyDeviceToHost, s));
     if (wout_h) std::memcpy(wout_h, wt.data(), sizeof(double) * wt.size());

@@ -25,10 +25,7 @@ constexpr int kAsmThreads = 256;
 constexpr int kJ = 8;  // outputs (consecutive j) per thread in the box kernel
 constexpr int kPGroups = 4;  // groups of 8 loads per chain in the periodic kernel's register ring
 
-// lattice.hpp:98 / :104-106 at k = 0; the window for shift k starts k*n lower.
-__device__ __forceinline__ int64_t window_start(int periodic, int64_t N, int64_t L, int64_t n, int64_t ia) {
-    return periodic ? N + (L / 2) * n - ia : N - ia;
-}
+using ls::window_start;  // lattice.hpp:98 / :104-106 at k = 0 (common.cuh)
 
 __global__ void assemble_box_kernel(const double* __restrict__ master, int64_t ld_master, int R,
                                     const int64_t* __restrict__ ia, int64_t n, int64_t L,

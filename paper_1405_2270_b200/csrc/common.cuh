@@ -104,6 +104,26 @@ struct AsyncScratch {
 // Number of SMs of the current device (cached per device).
 int sm_count();
 
+// Start of the master window of a charge at grid index ia for lattice shift 0 (the window of
+// shift k starts k*n lower): window_start_box (lattice.hpp:98) or window_start_periodic
+// (lattice.hpp:104-106), N = L*n.
+__host__ __device__ inline int64_t window_start(int periodic, int64_t N, int64_t L, int64_t n, int64_t ia) {
+    return periodic ? N + (L / 2) * n - ia : N - ia;
+}
+
+// Generator + assembled sum of up to three distinct axes (generator.cu). Axis a: master
+// (2 L n x R, leading dim 2 L n) and assembled factor (out_len x M0 R, leading dim out_len =
+// periodic ? n : L n) from the M0 charge grid indices ia_d. One launch when every master column
+// fits shared memory, else ls_gen_master + ls_assemble_axis per axis; bit-identical either way.
+struct GenAsmAxis {
+    int64_t L;
+    const int64_t* ia_d;
+    double* master_d;
+    double* out_d;
+};
+int gen_assemble(int mode, const double* tau_d, int R, int M0, int64_t n, double h, int periodic,
+                 const GenAsmAxis* ax, int n_ax, cudaStream_t s);
+
 // Keeps freed stream-ordered allocations cached in the current device's default
 // pool (no OS round trip per call). Idempotent per device.
 void ensure_pool();

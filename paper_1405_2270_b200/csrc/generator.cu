@@ -11,6 +11,8 @@
 #include "common.cuh"
 #include "glibc_math.cuh"
 
+#include <algorithm>
+
 namespace {
 
 constexpr int kGenThreads = 256;
@@ -70,6 +72,62 @@ __global__ void gen_erf_kernel(const double* __restrict__ tau, int64_t len, doub
     }
 }
 
+// Generator and assembled sum in one launch (small lattices: the step of cfg0 / cfg1 runs two
+// latency-bound launches less). Block (q, a) evaluates master column q of axis a into shared
+// memory with exactly the expressions of gen_erf_kernel / gen_midpoint_kernel, writes it to HBM
+// (ls_pipeline_assemble and the host calls still read it there), then forms every assembled
+// output of column q from it, one dependent left-to-right chain per output as in
+// assemble_box_kernel / assemble_axis_kernel (lattice.hpp:220-274): bit-identical factors.
+constexpr int kGaThreads = 512;
+struct GenAsmParams {
+    ls::GenAsmAxis ax[3];
+    const double* tau;
+    int R, M0, mode, periodic;
+    int64_t n;
+    double h;
+};
+
+__global__ void __launch_bounds__(kGaThreads) gen_assemble_kernel(const GenAsmParams p) {
+    pdl_wait();  // the previous step's launches may still read the master / factors
+    pdl_trigger();
+    extern __shared__ double sm[];
+    const ls::GenAsmAxis A = p.ax[blockIdx.y];
+    const int q = blockIdx.x;
+    const int64_t n = p.n, L = A.L, N = L * n, len = 2 * N, half = len / 2;
+    double* m = sm;         // [len] master column q
+    double* ev = sm + len;  // [half + 1] erf at the cell vertices
+    const double t = p.tau[q], h = p.h;
+    if (p.mode == LS_GEN_ERF) {
+        if (t == 0.0) {
+            for (int64_t i = threadIdx.x; i < len; i += blockDim.x) m[i] = h;
+        } else {
+            for (int64_t v = threadIdx.x; v <= half; v += blockDim.x)
+                ev[v] = ls::gm::erf(rn_mul(t, rn_mul(static_cast<double>(v - half), h)));
+            __syncthreads();
+            const double scale = __ddiv_rn(sqrt(CUDART_PI), rn_mul(2.0, t));
+            for (int64_t i = threadIdx.x; i < half; i += blockDim.x) m[i] = m[len - 1 - i] = rn_mul(scale, rn_sub(ev[i + 1], ev[i]));
+        }
+    } else {
+        const double half_len = static_cast<double>(len) / 2.0;
+        for (int64_t i = threadIdx.x; i < half; i += blockDim.x) {
+            const double x = rn_mul(t, rn_mul(rn_sub(rn_add(static_cast<double>(i), 0.5), half_len), h));
+            m[i] = m[len - 1 - i] = ls::gm::exp(-rn_mul(x, x));
+        }
+    }
+    __syncthreads();
+    double* mcol = A.master_d + len * q;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) mcol[i] = m[i];
+    const int64_t out_len = p.periodic ? n : N;
+    for (int64_t e = threadIdx.x; e < p.M0 * out_len; e += blockDim.x) {
+        const int64_t nu = e / out_len, o = e - nu * out_len;
+        const double* src = m + ls::window_start(p.periodic, N, L, n, A.ia_d[nu]) + o;
+        double acc = src[0];
+#pragma unroll 8
+        for (int64_t k = 1; k < L; ++k) acc = rn_add(acc, src[-k * n]);
+        A.out_d[out_len * (nu * p.R + q) + o] = acc;
+    }
+}
+
 __global__ void libm_eval_kernel(int fn, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = fn == LS_LIBM_ERF ? ls::gm::erf(x[i]) : ls::gm::exp(x[i]);
@@ -110,3 +168,59 @@ extern "C" int ls_gen_master(int mode, const double* tau_d, int R, int64_t len, 
     }
     return LS_OK;
 }
+
+namespace ls {
+
+// Shared memory of the fused launch and its bound: master + vertices of the longest axis, and
+// at most 8192 assembled outputs per column. Measured (tools/lab/gen_asm.py, back-to-back
+// calls): cfg1 7.5 us fused against 7.8 + 7.4 us for the two launches, the cfg0 step 59.9 ->
+// 54.9 us; at cfg3 (8 charges x 2048 outputs on 123 blocks) fusing gains nothing (31.5 us
+// against 13.3 + 20.0), so the many-block assembly kernels keep such lattices.
+constexpr int64_t kGaMaxSmem = 160 * 1024, kGaMaxOutputs = 8192;
+
+int gen_assemble(int mode, const double* tau_d, int R, int M0, int64_t n, double h, int periodic,
+                 const GenAsmAxis* ax, int n_ax, cudaStream_t s) {
+    if (n_ax < 1 || n_ax > 3 || R < 1 || M0 < 1) return fail(LS_EVALIDATION, "gen_assemble: bad axis count or rank");
+    int64_t len_max = 0;
+    bool fused = R <= 65535;
+    for (int a = 0; a < n_ax; ++a) {
+        const int64_t len = 2 * ax[a].L * n;
+        len_max = std::max(len_max, len);
+        if (static_cast<int64_t>(M0) * (periodic ? n : ax[a].L * n) > kGaMaxOutputs) fused = false;
+    }
+    const int64_t smem = sizeof(double) * (len_max + len_max / 2 + 1);
+    fused = fused && smem <= kGaMaxSmem && (mode == LS_GEN_ERF || mode == LS_GEN_MIDPOINT);
+    if (!fused) {
+        for (int a = 0; a < n_ax; ++a) {
+            const int64_t len = 2 * ax[a].L * n;
+            if (const int rc = ls_gen_master(mode, tau_d, R, len, h, ax[a].master_d, len, s)) return rc;
+            if (const int rc = ls_assemble_axis(ax[a].master_d, len, R, M0, ax[a].ia_d, n, ax[a].L, periodic, ax[a].out_d,
+                                                periodic ? n : ax[a].L * n, s))
+                return rc;
+        }
+        return LS_OK;
+    }
+    static std::atomic<bool> attr_set[64] = {};
+    int dev = 0;
+    LS_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && !attr_set[dev]) {
+        LS_CUDA(cudaFuncSetAttribute(gen_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kGaMaxSmem)));
+        attr_set[dev] = true;
+    }
+    GenAsmParams prm{};
+    for (int a = 0; a < n_ax; ++a) prm.ax[a] = ax[a];
+    prm.tau = tau_d;
+    prm.R = R;
+    prm.M0 = M0;
+    prm.mode = mode;
+    prm.periodic = periodic ? 1 : 0;
+    prm.n = n;
+    prm.h = h;
+    LS_CUDA(launch_pdl(gen_assemble_kernel, dim3(static_cast<unsigned>(R), static_cast<unsigned>(n_ax)),
+                       dim3(kGaThreads), static_cast<size_t>(smem), s, prm));
+    LS_LAUNCHED("gen_assemble_kernel");
+    return LS_OK;
+}
+
+}  // namespace ls

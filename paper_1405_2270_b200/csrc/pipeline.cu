@@ -162,6 +162,15 @@ int ls_pipeline_assemble(ls_pipeline* p, void* stream) {
     return LS_OK;
 }
 
+int ls_pipeline_prepare(ls_pipeline* p, void* stream) {
+    LS_PIPELINE_ENTRY(p);
+    ls::GenAsmAxis ax[3];
+    int n_ax = 0;
+    for (int l = 0; l < 3; ++l)
+        if (p->axis_src[l] == l) ax[n_ax++] = {p->L[l], p->ia + l * p->M0, p->master[l], p->fac[l]};
+    return ls::gen_assemble(p->mode, p->tau, p->R, p->M0, p->n, p->h, p->periodic, ax, n_ax, ls::as_stream(stream));
+}
+
 int ls_pipeline_expand(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void* stream) {
     LS_PIPELINE_ENTRY(p);
     return ls_expand(p->fac[0], p->dims[0], p->fac[1], p->dims[1], p->fac[2], p->dims[2], p->w, p->dims[0], p->dims[1],
@@ -170,8 +179,7 @@ int ls_pipeline_expand(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, vo
 
 int ls_pipeline_step(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void* stream) {
     LS_PIPELINE_ENTRY(p);
-    int rc = ls_pipeline_generate(p, stream);
-    if (!rc) rc = ls_pipeline_assemble(p, stream);
+    int rc = ls_pipeline_prepare(p, stream);
     if (!rc) rc = ls_pipeline_expand(p, k0, k1, out_d, stream);
     return rc;
 }

@@ -736,6 +736,10 @@ class DevicePipeline:
     def assemble(self, stream=None):
         call("ls_pipeline_assemble", self._h, self._stream(stream))
 
+    def prepare(self, stream=None):
+        """generate + assemble (one launch on small lattices, bit-identical); step() runs it."""
+        call("ls_pipeline_prepare", self._h, self._stream(stream))
+
     def _check_out(self, out, k0, k1):
         if not (0 <= k0 <= k1 <= self.dims[2]):
             raise ValidationError("expand: slab range outside [0, N3]")

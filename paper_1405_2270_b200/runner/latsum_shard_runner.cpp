@@ -209,8 +209,7 @@ int main(int argc, char** argv) try {
     CK(cudaEventRecord(total.a, s));
     latsum::DevicePotential& dp = pot.potential();
     for (int i = 0; i < a.steps; ++i) {
-        dp.generate(s);
-        dp.assemble(s);
+        dp.prepare(s);
         CK(cudaEventRecord(ev[static_cast<std::size_t>(i)].a, s));
         dp.expand(k0, k1, out, s);
         CK(cudaEventRecord(ev[static_cast<std::size_t>(i)].b, s));

@@ -169,6 +169,48 @@ def test_assembly_bitwise_at_config_scale(L, orc, Lc, n, M0, periodic):
     assert np.array_equal(got.tensor.weights(), w)
 
 
+FUSED_CASES = [  # (L, n, charges, periodic, mode): the fused generator + assembly launch and its fallback
+    ((4, 4, 4), 64, [(0, 0, 0, 1.0)], False, "erf"),                                 # cfg0
+    ((16, 16, 16), 64, [(0, 0, 0, 1.0)], False, "erf"),                              # cfg1
+    ((16, 16, 16), 64, [(0, 0, 0, 1.0)], False, "midpoint"),
+    ((3, 2, 5), 8, [(0, 0, 0, 1.0), (0.5, -0.25, 0.25, 2.0), (-0.75, 0.5, 0.0, 0.5)], False, "erf"),
+    ((3, 2, 5), 8, [(0, 0, 0, 1.0), (0.5, -0.25, 0.25, 2.0), (-0.75, 0.5, 0.0, 0.5)], True, "midpoint"),
+    ((1, 1, 1), 16, [(0.25, 0.0, -0.5, 1.0)], False, "erf"),                          # L = 1: no adds
+    ((9, 1, 2), 16, [(1.0, -1.0, 0.25, 3.0)], True, "erf"),
+    ((32, 32, 32), 64, "cfg3", False, "erf"),                                         # 8 charges x 2048
+    ((32, 32, 32), 64, "cfg3", True, "erf"),
+    ((64, 64, 64), 256, [(0, 0, 0, 1.0)], True, "erf"),                               # too long: fallback
+]
+
+
+@pytest.mark.parametrize("case", FUSED_CASES, ids=[f"{c[0][0]}x{c[0][1]}x{c[0][2]}-n{c[1]}-{'p' if c[3] else 'b'}-{c[4]}"
+                                                   for c in FUSED_CASES])
+def test_prepare_fused_generator_assembly_bitwise(L, orc, case):
+    """ls_pipeline_prepare (generator + assembled sum in one launch where the master column fits
+    shared memory) gives factors bit-identical to the oracle's ascending-k assembly of the
+    reference master and to the two-launch generate() + assemble() path."""
+    import torch
+    Lc, n, charges, periodic, mode = case
+    b = 10.0 if n >= 64 else 2.0
+    if charges == "cfg3":
+        rng = np.random.default_rng(20241019)
+        ia = rng.integers(7, 58, size=(8, 3))
+        charges = [(*(ia[c] * (b / n) - b / 2), float(c + 1)) for c in range(8)]
+    spec, rule = cfg(L, Lc, n=n, b=b, charges=charges, M=20 if n >= 64 else 10)
+    _, want, w = oracle_assembled(orc, spec, rule, mode, periodic)
+    pipe = L.DevicePipeline(spec, rule, mode=mode, periodic=periodic)
+    pipe.prepare()
+    torch.cuda.synchronize()
+    fused = [pipe.factor(l).cpu().numpy().T.copy() for l in range(3)]
+    pipe.generate()
+    pipe.assemble()
+    torch.cuda.synchronize()
+    split = [pipe.factor(l).cpu().numpy().T.copy() for l in range(3)]
+    for l in range(3):
+        assert np.array_equal(fused[l], want[l]), ("fused vs oracle", l)
+        assert np.array_equal(split[l], want[l]), ("two launches vs oracle", l)
+
+
 def test_assembly_matches_golden_bitwise(L, golden):
     g = golden
     ch = g["mc_charges"]

@@ -22,6 +22,7 @@ grid = torch.empty(tuple(reversed(pipe.dims)), dtype=torch.float64, device=dev)
 pipe.step(grid)
 torch.cuda.synchronize()
 for name, fn in (("step", lambda: pipe.step(grid)), ("generate", pipe.generate), ("assemble", pipe.assemble),
+                 ("prepare", pipe.prepare),
                  ("expand", lambda: pipe.expand(grid))):
     eager = bench._ev_ms(fn) * 1e3
     graph, how = bench._graph_ms(fn)

@@ -51,5 +51,7 @@ for name, Lc, n, M0, periodic in cases:
     pipe = L.DevicePipeline(spec, rule, mode="erf", periodic=periodic)
     tg = timed(pipe.generate)
     ta = timed(pipe.assemble)
-    print(f"{name}: master {2 * Lc * n} x {rule.node_count()}: generate {tg:.1f} us, assemble {ta:.1f} us "
+    tp = timed(pipe.prepare)
+    print(f"{name}: master {2 * Lc * n} x {rule.node_count()}: generate {tg:.1f} us, assemble {ta:.1f} us, "
+          f"prepare {tp:.1f} us "
           f"({pipe.Rt} columns of {n if periodic else Lc * n})", flush=True)

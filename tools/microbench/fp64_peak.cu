@@ -3,6 +3,7 @@
 // MEASURED_PEAKS.json lacks. Prints one JSON object per measurement.
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
@@ -143,6 +144,26 @@ int main(int argc, char** argv) {
   int sms = p.multiProcessorCount;
   double* out; CK(cudaMalloc(&out, (size_t)sms * 64 * 1024 * sizeof(double)));
   const int iters = 20000;
+  if (argc > 1 && std::string(argv[1]) == "sweep") {
+    // DMMA latency and occupancy: one CTA per SM, 1 or 2 warps per sub-partition, 1..16
+    // independent accumulators per warp. cycles_per_dmma = per-warp issue interval.
+    auto run = [&](auto kern, int acc, int threads) {
+      int grid = sms, it = iters / 4;
+      float ms = time_ms([&] { kern<<<grid, threads>>>(out, it); }, 5);
+      double flops = 2.0 * 256 * acc * it * (double)grid * (threads / 32);
+      double cyc = ms * 1e-3 * 1.965e9 / (double(it) * acc);
+      printf("{\"bench\":\"dmma_sweep\",\"acc\":%d,\"warps_per_sp\":%d,\"ms\":%.4f,\"tflops\":%.3f,"
+             "\"cycles_per_dmma_per_warp\":%.1f}\n", acc, threads / 128, ms, flops / ms / 1e9, cyc);
+    };
+    for (int threads : {128, 256, 384, 512}) {
+      run(dmma884_kernel<1>, 1, threads);
+      run(dmma884_kernel<2>, 2, threads);
+      run(dmma884_kernel<4>, 4, threads);
+      run(dmma884_kernel<8>, 8, threads);
+      run(dmma884_kernel<16>, 16, threads);
+    }
+    return 0;
+  }
   // DFMA sweeps
   for (int blocks_per_sm : {2, 4, 8}) {
     int threads = 256;
