@@ -411,14 +411,10 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
             // the last warp refills it with this CTA's unit n + kNS.
             __syncwarp();
             if (lane == 0) {
-#ifndef LS_A2T_RELAX
                 __threadfence_block();
-#endif
                 if (atomicAdd(released + slot, 1) == kA2tWarps - 1) {
                     released[slot] = 0;
-#ifndef LS_A2T_RELAX
                     __threadfence_block();
-#endif
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     if (n + kNS < my_units) issue(n + kNS);
                 }
