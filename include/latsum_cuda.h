@@ -210,8 +210,10 @@ int ls_pipeline_info(const ls_pipeline* p, int64_t dims[3], int* rank_total, con
                      const double** B_d, const double** C_d, const double** w_d);
 int ls_pipeline_generate(ls_pipeline* p, void* stream);
 int ls_pipeline_assemble(ls_pipeline* p, void* stream);
-/* generate + assemble, as one launch when every master column fits shared memory (small
- * lattices, e.g. cfg0 / cfg1; bit-identical to the two calls); ls_pipeline_step runs it. */
+/* generate + assemble: build_lattice_master (lattice.hpp:109-113) / the erf generator
+ * (newton.hpp:21-37) followed by assembled_box_sum / assembled_periodic_sum (lattice.hpp:276-312),
+ * as ONE launch when every master column fits shared memory (small lattices, e.g. cfg0 / cfg1;
+ * bit-identical to the two calls, which it falls back to otherwise); ls_pipeline_step runs it. */
 int ls_pipeline_prepare(ls_pipeline* p, void* stream);
 /* slabs [k0, k1) into out_d (dense, i-fastest, (k1-k0)*N1*N2 doubles). */
 int ls_pipeline_expand(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void* stream);
