@@ -203,10 +203,10 @@ int gen_assemble(int mode, const double* tau_d, int R, int M0, int64_t n, double
     static std::atomic<bool> attr_set[64] = {};
     int dev = 0;
     LS_CUDA(cudaGetDevice(&dev));
-    if (dev < 64 && !attr_set[dev]) {
+    if (dev >= 64 || !attr_set[dev]) {
         LS_CUDA(cudaFuncSetAttribute(gen_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kGaMaxSmem)));
-        attr_set[dev] = true;
+        if (dev < 64) attr_set[dev] = true;
     }
     GenAsmParams prm{};
     for (int a = 0; a < n_ax; ++a) prm.ax[a] = ax[a];
