@@ -433,7 +433,9 @@ int launch_splitk(ExpandArgs& a, bool store, bool func, cudaStream_t s, int sm_c
     a.n_jc = ls::ceil_div(a.N2, 8 * kSkJT);
     a.n_jt = a.n_jc * kSkJT;
     a.split_tail = 0;
-    if (a.n_tail == 0) a.n_tail = 1;  // a zero DFMA rank on the tile's writer (see the kernel)
+    // A zero DFMA rank on the tile's writer (see the kernel) where its TMEM columns fit: at KD 128
+    // (rank 512) the halves already fill all 512 columns.
+    if (a.n_tail == 0 && fits_splitk(a.KD, 1)) a.n_tail = 1;
     if (a.n_units * a.n_jc * n_kc >= (int64_t(1) << 31) || a.N1 + kSkIC >= (int64_t(1) << 31))
         return ls::fail(LS_EGUARD, "expand: grid too large for one launch (split the slab range)");
     const size_t stage_elems = static_cast<size_t>(2 * kSkJT * kSkKC * 32 + kSkJT * 8 * a.n_tail);

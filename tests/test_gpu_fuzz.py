@@ -98,6 +98,20 @@ def test_expand_fuzz(env, orc, case, R, dims, k0, k1, pad_y, pad_z, func):
         assert abs(float(e.cpu()) - e_want) <= 1e-13 * abs(e_want)
 
 
+# Split-K at its edges (ranks >= 250): R mod 4 = 0 / 1 / 2 / 3 (zero rank, one or two DFMA
+# ranks, a zero-padded k-step), odd and even KD (which half runs the remainder), and the largest
+# single-launch ranks, where the halves fill all 512 TMEM columns and no zero rank fits (512:
+# KD 128; a fuzz soak found the r02 zero rank overflowing TMEM there). 513+ chunks by 256 ranks.
+SPLITK_EDGES = [250, 251, 253, 256, 301, 333, 479, 480, 481, 495, 508, 509, 510, 511, 512, 513]
+
+
+@pytest.mark.parametrize("R", SPLITK_EDGES)
+@pytest.mark.parametrize("func", [False, True])
+def test_expand_splitk_edges(env, orc, R, func):
+    test_expand_fuzz(env, orc, 7000 + R, R, (150, 170, 3), 0, 3, 3, 8, func)
+    test_expand_fuzz(env, orc, 8000 + R, R, (70, 33, 4), 2, 4, 0, 0, func)
+
+
 def _lattices(n=40, seed=7):
     rng = np.random.default_rng(seed)
     for c in range(n):

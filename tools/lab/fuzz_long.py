@@ -20,6 +20,7 @@ from paper_1405_2270_b200 import _abi  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--cases", type=int, default=2000)
 ap.add_argument("--seed", type=int, default=7)
+ap.add_argument("--trace", action="store_true", help="print every case before running it (triage)")
 args = ap.parse_args()
 rng = np.random.default_rng(args.seed)
 lib = _abi.load()
@@ -37,6 +38,8 @@ for c in range(args.cases):
     k0 = int(rng.integers(0, n3))
     k1 = int(rng.integers(k0 + 1, n3 + 1))
     pad_y, pad_z = int(rng.choice([0, 0, 1, 2, 5])), int(rng.choice([0, 0, 2, 7]))
+    if args.trace:
+        print(f"case {c}: {R},{n1},{n2},{n3},{k0},{k1},{pad_y},{pad_z}", flush=True)
     fac = [torch.rand((R, m), dtype=torch.float64, device=dev) * 0.95 + 0.05 for m in (n1, n2, n3)]
     w = torch.rand(R, dtype=torch.float64, device=dev) * 0.95 + 0.05
     ldy, nk = n1 + pad_y, k1 - k0
