@@ -14,7 +14,54 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // 4: both, ping-pong unrolled by 2 (no moves)
 template <int MODE, int TM, int TN>
 __global__ void __launch_bounds__(256, 2) loop_kernel(const double* __restrict__ g, double* out, int KD, int NJ) {
-    if (MODE == 7 || MODE == 8) {
+    if (MODE == 12) {
+        // two accumulator sets: tile jb computes into one set while the previous tile's set is
+        // streamed out, one store pair per k-step (the a2t kernel's ping-pong)
+        __shared__ double sm3[4 * 11 * 32 * 4 + 64];
+        for (int e = threadIdx.x; e < 4 * 11 * 32 * 4; e += 256) sm3[e] = 1.0 + e * 1e-9;
+        __syncthreads();
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+        const double* asw = sm3 + lane;
+        double accA[TM][TN][2], accB[TM][TN][2];
+        auto tile = [&](int jb, double (&cur)[TM][TN][2], double (&prev)[TM][TN][2]) {
+#pragma unroll
+            for (int m = 0; m < TM; ++m)
+#pragma unroll
+                for (int n = 0; n < TN; ++n) cur[m][n][0] = cur[m][n][1] = 0.0;
+            const long base = ((long)(blockIdx.x * 8 + warp) * NJ + jb - 1) * (TM * 8) * 1024;
+#pragma unroll
+            for (int ks = 0; ks < 10; ++ks) {
+                double a[TM], b[TN];
+#pragma unroll
+                for (int m = 0; m < TM; ++m) a[m] = asw[(m * 11 + ks) * 32];
+#pragma unroll
+                for (int n = 0; n < TN; ++n) b[n] = asw[(n * 11 + ks) * 32 + 64];
+#pragma unroll
+                for (int m = 0; m < TM; ++m)
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) dmma(cur[m][n][0], cur[m][n][1], a[m], b[n]);
+                if (jb > 0) {
+#pragma unroll
+                    for (int q = TM * TN * ks / 10; q < TM * TN * (ks + 1) / 10; ++q)
+                        __stcs(reinterpret_cast<double2*>(out + 8 + base + (8 * (q / TN) + g) * 1024 + 8 * (q % TN) + 2 * t),
+                               make_double2(prev[q / TN][q % TN][0], prev[q / TN][q % TN][1]));
+                }
+            }
+        };
+        int jb = 0;
+        for (; jb + 1 < NJ; jb += 2) {
+            tile(jb, accA, accB);
+            tile(jb + 1, accB, accA);
+        }
+        double sink = 0.0;
+#pragma unroll
+        for (int m = 0; m < TM; ++m)
+#pragma unroll
+            for (int n = 0; n < TN; ++n) sink += accA[m][n][0] + accB[m][n][1];
+        if (sink == 1.2345) out[0] = sink;
+        return;
+    }
+    if (MODE == 7 || MODE == 8 || MODE == 10 || MODE == 11) {
         // smem operands + an epilogue every KD k-steps (MODE 7: streaming stores like the
         // expansion, MODE 8: drain into a register sink only)
         __shared__ double sm2[4 * 11 * 32 * 4 + 64];
@@ -29,6 +76,20 @@ __global__ void __launch_bounds__(256, 2) loop_kernel(const double* __restrict__
             for (int m = 0; m < TM; ++m)
 #pragma unroll
                 for (int n = 0; n < TN; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+            if (MODE == 10 || MODE == 11) {  // one DFMA rank at the tile start, as the expansion's rank tail
+                double bt[TM], at[2 * TN];
+#pragma unroll
+                for (int m = 0; m < TM; ++m) bt[m] = asw[(m * 11 + 10) * 32];
+#pragma unroll
+                for (int n = 0; n < 2 * TN; ++n) at[n] = asw[(n * 5 + 3) * 32 + 64];
+#pragma unroll
+                for (int n = 0; n < TN; ++n)
+#pragma unroll
+                    for (int m = 0; m < TM; ++m) {
+                        acc[m][n][0] = fma(at[2 * n], bt[m], acc[m][n][0]);
+                        acc[m][n][1] = fma(at[2 * n + 1], bt[m], acc[m][n][1]);
+                    }
+            }
 #pragma unroll 1
             for (int ks = 0; ks < KD; ++ks) {
                 double a[TM], b[TN];
@@ -41,7 +102,7 @@ __global__ void __launch_bounds__(256, 2) loop_kernel(const double* __restrict__
 #pragma unroll
                     for (int n = 0; n < TN; ++n) dmma(acc[m][n][0], acc[m][n][1], a[m], b[n]);
             }
-            if (MODE == 7) {
+            if (MODE == 7 || MODE == 11) {
                 const long base = ((long)(blockIdx.x * 8 + warp) * NJ + jb) * (TM * 8) * 1024;
 #pragma unroll
                 for (int m = 0; m < TM; ++m)
@@ -197,5 +258,15 @@ int main() {
     run<5, 4, 4>("smem both 4x4, no epilogue", g, out, 2);
     run<8, 4, 4>("smem both 4x4, drain to sink every 10 k-steps", g, out, 2);
     run<7, 4, 4>("smem both 4x4, streaming stores every 10 k-steps", g, out, 2);
+    run<10, 4, 4>("smem both 4x4, DFMA rank + drain to sink every 10 k-steps", g, out, 2);
+    run<11, 4, 4>("smem both 4x4, DFMA rank + streaming stores every 10 k-steps", g, out, 2);
+    run<5, 4, 2>("smem both 4x2, no epilogue", g, out, 2);
+    run<7, 4, 2>("smem both 4x2, streaming stores every 10 k-steps", g, out, 2);
+    run<12, 4, 2>("smem both 4x2, two accumulator sets, stores spread over the next tile", g, out, 2);
+    run<12, 2, 4>("smem both 2x4, two accumulator sets, stores spread over the next tile", g, out, 2);
+    run<12, 4, 4>("[1 CTA/SM] 4x4 two accumulator sets, stores spread over the next tile", g, out, 1);
+    run<5, 4, 4>("[1 CTA/SM] smem both 4x4, no epilogue", g, out, 1);
+    run<8, 4, 4>("[1 CTA/SM] drain to sink every 10 k-steps", g, out, 1);
+    run<10, 4, 4>("[1 CTA/SM] DFMA rank + drain to sink every 10 k-steps", g, out, 1);
     return 0;
 }
