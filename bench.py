@@ -315,10 +315,11 @@ def expand_plan_name(lib, R):
     return buf.value.decode() if lib.ls_expand_plan_name(R, buf, 256) == 0 else None
 
 
-def _ev_ms(fn, reps=3, batch_ms=2.0):
+def _ev_ms(fn, reps=3, batch_ms=10.0):
     """Device ms per call: best of `reps` batches of back-to-back calls between two events, each
-    batch at least `batch_ms` long, so a short call's host launch cost stays behind the queue
-    (the same convention as the K-step headline)."""
+    batch at least `batch_ms` long (up to 200 calls), so a short call's host launch cost stays
+    behind the queue and the first call's enqueue delay after the start event is amortized (the
+    same convention as the K-step headline)."""
     import torch
     fn()
     torch.cuda.synchronize()
