@@ -684,6 +684,10 @@ def run_reference(args, rank, world):
         "impl": "reference", "cpu_baseline": cb,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": round(time.perf_counter() - t_all, 2),
+        "sampling": "each step is a bounded sample of the workload's z-slabs (cpu_baseline.sample); value is the "
+                    "sampled rate and ms_per_step that rate extrapolated to the whole grid; "
+                    "ms_per_step_sampled is the wall time a step actually took",
+        "ms_per_step_sampled": round((time.perf_counter() - t_all) * 1e3 / max(1, args.steps + args.warmup), 3),
     }
     print(json.dumps(line), flush=True)
 
