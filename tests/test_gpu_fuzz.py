@@ -128,7 +128,9 @@ def _lattices(n=40, seed=7):
         yield pytest.param(c, Lc, nn, idx, Z, periodic, mode, M, id=f"c{c}-L{Lc}-n{nn}-M0{M0}-{mode}")
 
 
-@pytest.mark.parametrize("case,Lc,nn,idx,Z,periodic,mode,M", list(_lattices()))
+# LS_LATTICE_SOAK=N runs N lattices instead of 40 (a longer soak, e.g. after kernel changes)
+@pytest.mark.parametrize("case,Lc,nn,idx,Z,periodic,mode,M",
+                         list(_lattices(n=int(__import__("os").environ.get("LS_LATTICE_SOAK", "40")))))
 def test_lattice_fuzz(env, orc, case, Lc, nn, idx, Z, periodic, mode, M):
     """Random lattices (shape, cells per axis, charges on random vertices, box or periodic, both
     generators): the device pipeline's assembled factors are bit-identical to the oracle's
