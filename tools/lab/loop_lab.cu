@@ -12,8 +12,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 // MODE 0: constants; 1: b from smem, a const; 2: a from global, b const; 3: both (move-based prefetch);
 // 4: both, ping-pong unrolled by 2 (no moves)
-template <int MODE, int TM, int TN>
-__global__ void __launch_bounds__(256, 2) loop_kernel(const double* __restrict__ g, double* out, int KD, int NJ) {
+template <int MODE, int TM, int TN, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) loop_kernel(const double* __restrict__ g, double* out, int KD, int NJ) {
     if (MODE == 12) {
         // two accumulator sets: tile jb computes into one set while the previous tile's set is
         // streamed out, one store pair per k-step (the a2t kernel's ping-pong)
@@ -236,19 +236,19 @@ __global__ void __launch_bounds__(256, 2) loop_kernel(const double* __restrict__
     if (s == 1.2345) out[0] = s;
 }
 
-template <int MODE, int TM, int TN>
+template <int MODE, int TM, int TN, int MINB = 2>
 void run(const char* name, const double* g, double* out, int per_sm = 2) {
     int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const int KD = 10, NJ = 200, grid = sms * per_sm;
     cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
-    loop_kernel<MODE, TM, TN><<<grid, 256>>>(g, out, KD, NJ); CK(cudaDeviceSynchronize());
+    loop_kernel<MODE, TM, TN, MINB><<<grid, 256>>>(g, out, KD, NJ); CK(cudaDeviceSynchronize());
     float best = 1e9;
     for (int r = 0; r < 5; ++r) {
-        CK(cudaEventRecord(e0)); loop_kernel<MODE, TM, TN><<<grid, 256>>>(g, out, KD, NJ); CK(cudaEventRecord(e1));
+        CK(cudaEventRecord(e0)); loop_kernel<MODE, TM, TN, MINB><<<grid, 256>>>(g, out, KD, NJ); CK(cudaEventRecord(e1));
         CK(cudaEventSynchronize(e1)); float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); if (ms < best) best = ms;
     }
     double flops = 2.0 * 256 * TM * TN * (double)KD * NJ * grid * 8;
-    cudaFuncAttributes fa; CK(cudaFuncGetAttributes(&fa, loop_kernel<MODE, TM, TN>));
+    cudaFuncAttributes fa; CK(cudaFuncGetAttributes(&fa, loop_kernel<MODE, TM, TN, MINB>));
     printf("{\"loop\":\"%s\",\"ctas_per_sm\":%d,\"regs\":%d,\"ms\":%.4f,\"tflops\":%.3f}\n", name, per_sm, fa.numRegs, best, flops / best / 1e9);
 }
 
@@ -260,6 +260,9 @@ int main() {
     run<7, 4, 4>("smem both 4x4, streaming stores every 10 k-steps", g, out, 2);
     run<10, 4, 4>("smem both 4x4, DFMA rank + drain to sink every 10 k-steps", g, out, 2);
     run<11, 4, 4>("smem both 4x4, DFMA rank + streaming stores every 10 k-steps", g, out, 2);
+    run<5, 8, 4, 1>("[1 CTA/SM, 255 regs] 8x4 tiles, no epilogue", g, out, 1);
+    run<7, 8, 4, 1>("[1 CTA/SM, 255 regs] 8x4 tiles, streaming stores every 10 k-steps", g, out, 1);
+    run<11, 8, 4, 1>("[1 CTA/SM, 255 regs] 8x4 tiles, DFMA rank + stores every 10 k-steps", g, out, 1);
     run<5, 4, 2>("smem both 4x2, no epilogue", g, out, 2);
     run<7, 4, 2>("smem both 4x2, streaming stores every 10 k-steps", g, out, 2);
     run<12, 4, 2>("smem both 4x2, two accumulator sets, stores spread over the next tile", g, out, 2);
