@@ -130,6 +130,42 @@ __global__ void assemble_axis_kernel(const double* __restrict__ master, int64_t 
     }
 }
 
+// Periodic sums with long chains (cfg4: n = 256 residues x 41 columns, L = 64..256 shifts): the
+// per-chain kernel above keeps only 24 loads in flight per chain, and with 10.5K chains on 148
+// SMs it waits on L2 latency for every group (8 us at L = 256). Here a block stages the L x 32
+// master values of 32 consecutive residues of one column in shared memory with all its threads
+// (row k = 32 contiguous doubles, coalesced, all loads in flight at once), then one warp runs
+// the 32 chains out of shared memory, still strictly ascending in k: bit-identical sums.
+constexpr int kPerIB = 32;
+__global__ void __launch_bounds__(256) assemble_periodic_staged_kernel(const double* __restrict__ master,
+                                                                      int64_t ld_master, int R,
+                                                                      const int64_t* __restrict__ ia, int64_t n,
+                                                                      int64_t L, double* __restrict__ out,
+                                                                      int64_t ld_out) {
+    pdl_wait();  // the master comes from the preceding generator launch
+    pdl_trigger();
+    extern __shared__ double stage[];  // [L][kPerIB]
+    const int c = blockIdx.y;          // column nu*R + q
+    const int nu = c / R;
+    const int q = c % R;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kPerIB;
+    const double* base = master + ld_master * q + window_start(1, L * n, L, n, ia[nu]) + i0;
+    const int64_t cnt = L * kPerIB;
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const int64_t k = e / kPerIB;
+        const int ii = static_cast<int>(e - k * kPerIB);
+        stage[e] = i0 + ii < n ? __ldg(base + ii - k * n) : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < kPerIB && i0 + threadIdx.x < n) {
+        const double* col = stage + threadIdx.x;
+        double acc = col[0];
+#pragma unroll 8
+        for (int64_t k = 1; k < L; ++k) acc = rn_add(acc, col[k * kPerIB]);
+        out[i0 + threadIdx.x + ld_out * c] = acc;
+    }
+}
+
 }  // namespace
 
 extern "C" int ls_assemble_axis(const double* master_d, int64_t ld_master, int R, int M0,
@@ -150,6 +186,22 @@ extern "C" int ls_assemble_axis(const double* master_d, int64_t ld_master, int R
         LS_CUDA(ls::launch_pdl(assemble_box_kernel, dim3((unsigned)blocks, (unsigned)cols), dim3(kAsmThreads), 0, s,
                                master_d, ld_master, R, ia_d, n, L, out_d, ld_out));
         LS_LAUNCHED("assemble_box_kernel");
+        return LS_OK;
+    }
+    // periodic, long chains: stage each 32-residue block's L x 32 master values in shared memory
+    const size_t staged = sizeof(double) * static_cast<size_t>(L) * kPerIB;
+    if (periodic && L >= 32 && staged <= 96 * 1024) {
+        static std::atomic<bool> attr_set[64] = {};
+        int dev = 0;
+        LS_CUDA(cudaGetDevice(&dev));
+        if (dev >= 64 || !attr_set[dev]) {
+            LS_CUDA(cudaFuncSetAttribute(assemble_periodic_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         96 * 1024));
+            if (dev < 64) attr_set[dev] = true;
+        }
+        LS_CUDA(ls::launch_pdl(assemble_periodic_staged_kernel, dim3((unsigned)ls::ceil_div(out_len, kPerIB), (unsigned)cols),
+                               dim3(256), staged, s, master_d, ld_master, R, ia_d, n, L, out_d, ld_out));
+        LS_LAUNCHED("assemble_periodic_staged_kernel");
         return LS_OK;
     }
     // periodic: 64-thread blocks spread the few, long chains (n per column) over the SMs
