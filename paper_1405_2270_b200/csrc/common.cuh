@@ -121,8 +121,10 @@ struct GenAsmAxis {
     double* master_d;
     double* out_d;
 };
+// Periodic lattices with one charge and L >= 32 take a fused launch that never writes the
+// master (*master_written = false then); every other lattice gets its master written.
 int gen_assemble(int mode, const double* tau_d, int R, int M0, int64_t n, double h, int periodic,
-                 const GenAsmAxis* ax, int n_ax, cudaStream_t s);
+                 const GenAsmAxis* ax, int n_ax, cudaStream_t s, bool* master_written = nullptr);
 
 // Keeps freed stream-ordered allocations cached in the current device's default
 // pool (no OS round trip per call). Idempotent per device.

@@ -128,6 +128,61 @@ __global__ void __launch_bounds__(kGaThreads) gen_assemble_kernel(const GenAsmPa
     }
 }
 
+// Periodic lattices with long chains and one charge (cfg4: L = 64..256, n = 256): the
+// generator and the assembled sum fused WITHOUT materializing the master. Every master entry is
+// used by exactly one assembled output there, so block (32-residue block, q, axis) evaluates
+// the cells its 32 chains need straight from the reference's formula (erf mode: the 33 cell
+// vertices of each shift k; every cell directly, as the reference does -- equal, bit for bit,
+// to the generator's mirrored half), stages them in shared memory, and one warp runs the 32
+// ascending-k chains. The 43 MB master of cfg4 L = 256 is never written or read back.
+constexpr int kGpIB = 32;
+__global__ void __launch_bounds__(1024) gen_assemble_periodic_kernel(const GenAsmParams p) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ double ev[];  // [L][kGpIB + 1]: erf at the vertices (erf) or the cells (midpoint)
+    const ls::GenAsmAxis A = p.ax[blockIdx.z];
+    const int q = blockIdx.y;
+    const int64_t n = p.n, L = A.L, N = L * n, half = N;  // master length 2N, vertex v at (v - N) h
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kGpIB;
+    const double t = p.tau[q], h = p.h;
+    const int64_t s0 = ls::window_start(1, N, L, n, A.ia_d[0]) + i0;  // cell of chain i0, shift 0
+    constexpr int W = kGpIB + 1;
+    const bool erf_mode = p.mode == LS_GEN_ERF;
+    if (!(erf_mode && t == 0.0)) {
+        const double half_len = static_cast<double>(2 * N) / 2.0;
+        for (int64_t e = threadIdx.x; e < L * W; e += blockDim.x) {
+            const int64_t k = e / W;
+            const int c = static_cast<int>(e - k * W);
+            const int64_t v = s0 - k * n + c;  // vertex (erf) or cell (midpoint) index
+            if (erf_mode) {
+                ev[e] = ls::gm::erf(rn_mul(t, rn_mul(static_cast<double>(v - half), h)));
+            } else if (c < kGpIB) {
+                const double x = rn_mul(t, rn_mul(rn_sub(rn_add(static_cast<double>(v), 0.5), half_len), h));
+                ev[e] = ls::gm::exp(-rn_mul(x, x));
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < kGpIB && i0 + threadIdx.x < n) {
+        const double* col = ev + threadIdx.x;
+        double acc;
+        if (erf_mode && t == 0.0) {
+            acc = h;
+            for (int64_t k = 1; k < L; ++k) acc = rn_add(acc, h);
+        } else if (erf_mode) {
+            const double scale = __ddiv_rn(sqrt(CUDART_PI), rn_mul(2.0, t));
+            acc = rn_mul(scale, rn_sub(col[1], col[0]));
+#pragma unroll 8
+            for (int64_t k = 1; k < L; ++k) acc = rn_add(acc, rn_mul(scale, rn_sub(col[k * W + 1], col[k * W])));
+        } else {
+            acc = col[0];
+#pragma unroll 8
+            for (int64_t k = 1; k < L; ++k) acc = rn_add(acc, col[k * W]);
+        }
+        A.out_d[n * q + i0 + threadIdx.x] = acc;  // column q (M0 = 1), leading dim n
+    }
+}
+
 __global__ void libm_eval_kernel(int fn, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = fn == LS_LIBM_ERF ? ls::gm::erf(x[i]) : ls::gm::exp(x[i]);
@@ -179,8 +234,48 @@ namespace ls {
 constexpr int64_t kGaMaxSmem = 160 * 1024, kGaMaxOutputs = 8192;
 
 int gen_assemble(int mode, const double* tau_d, int R, int M0, int64_t n, double h, int periodic,
-                 const GenAsmAxis* ax, int n_ax, cudaStream_t s) {
+                 const GenAsmAxis* ax, int n_ax, cudaStream_t s, bool* master_written) {
+    if (master_written) *master_written = true;
     if (n_ax < 1 || n_ax > 3 || R < 1 || M0 < 1) return fail(LS_EVALIDATION, "gen_assemble: bad axis count or rank");
+    // Periodic, one charge, long chains: generator and assembly fused, master never written.
+    {
+        int64_t L_max = 0, L_min = INT64_MAX;
+        for (int a = 0; a < n_ax; ++a) {
+            L_max = std::max(L_max, ax[a].L);
+            L_min = std::min(L_min, ax[a].L);
+        }
+        const int64_t smem_p = sizeof(double) * L_max * (kGpIB + 1);
+        if (periodic && M0 == 1 && L_min >= 32 && smem_p <= kGaMaxSmem && R <= 65535 &&
+            (mode == LS_GEN_ERF || mode == LS_GEN_MIDPOINT)) {
+            static std::atomic<bool> attr_p[64] = {};
+            int dev = 0;
+            LS_CUDA(cudaGetDevice(&dev));
+            if (dev >= 64 || !attr_p[dev]) {
+                LS_CUDA(cudaFuncSetAttribute(gen_assemble_periodic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kGaMaxSmem)));
+                if (dev < 64) attr_p[dev] = true;
+            }
+            // about eight vertex evaluations per thread (tools/lab/gen_asm.py: L = 64 with 256
+            // threads, L = 256 with 1024)
+            const int64_t gp_threads = std::min<int64_t>(1024, std::max<int64_t>(256, (L_max * (kGpIB + 1) / 8 + 255) / 256 * 256));
+            GenAsmParams prm{};
+            for (int a = 0; a < n_ax; ++a) prm.ax[a] = ax[a];
+            prm.tau = tau_d;
+            prm.R = R;
+            prm.M0 = M0;
+            prm.mode = mode;
+            prm.periodic = 1;
+            prm.n = n;
+            prm.h = h;
+            LS_CUDA(launch_pdl(gen_assemble_periodic_kernel,
+                               dim3(static_cast<unsigned>(ceil_div(n, kGpIB)), static_cast<unsigned>(R),
+                                    static_cast<unsigned>(n_ax)),
+                               dim3(static_cast<unsigned>(gp_threads)), static_cast<size_t>(smem_p), s, prm));
+            LS_LAUNCHED("gen_assemble_periodic_kernel");
+            if (master_written) *master_written = false;
+            return LS_OK;
+        }
+    }
     int64_t len_max = 0;
     bool fused = R <= 65535;
     for (int a = 0; a < n_ax; ++a) {

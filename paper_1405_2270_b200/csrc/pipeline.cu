@@ -31,6 +31,7 @@ struct ls_pipeline {
     double* fac[3] = {nullptr, nullptr, nullptr};
     double* partial = nullptr;
     int64_t partial_cap = 0;
+    bool master_valid = false;  // the fused periodic prepare leaves the master unwritten
 };
 
 namespace {
@@ -148,11 +149,15 @@ int ls_pipeline_generate(ls_pipeline* p, void* stream) {
         const int rc = ls_gen_master(p->mode, p->tau, p->R, len, p->h, p->master[l], len, stream);
         if (rc) return rc;
     }
+    p->master_valid = true;
     return LS_OK;
 }
 
 int ls_pipeline_assemble(ls_pipeline* p, void* stream) {
     LS_PIPELINE_ENTRY(p);
+    if (!p->master_valid) {  // no generate() since creation or a fused prepare: build the master first
+        if (const int rc = ls_pipeline_generate(p, stream)) return rc;
+    }
     for (int l = 0; l < 3; ++l) {
         if (p->axis_src[l] != l) continue;
         const int rc = ls_assemble_axis(p->master[l], 2 * p->L[l] * p->n, p->R, p->M0, p->ia + l * p->M0, p->n, p->L[l],
@@ -168,7 +173,11 @@ int ls_pipeline_prepare(ls_pipeline* p, void* stream) {
     int n_ax = 0;
     for (int l = 0; l < 3; ++l)
         if (p->axis_src[l] == l) ax[n_ax++] = {p->L[l], p->ia + l * p->M0, p->master[l], p->fac[l]};
-    return ls::gen_assemble(p->mode, p->tau, p->R, p->M0, p->n, p->h, p->periodic, ax, n_ax, ls::as_stream(stream));
+    bool written = true;
+    const int rc =
+        ls::gen_assemble(p->mode, p->tau, p->R, p->M0, p->n, p->h, p->periodic, ax, n_ax, ls::as_stream(stream), &written);
+    if (rc == LS_OK) p->master_valid = written;
+    return rc;
 }
 
 int ls_pipeline_expand(ls_pipeline* p, int64_t k0, int64_t k1, double* out_d, void* stream) {

@@ -179,7 +179,10 @@ FUSED_CASES = [  # (L, n, charges, periodic, mode): the fused generator + assemb
     ((9, 1, 2), 16, [(1.0, -1.0, 0.25, 3.0)], True, "erf"),
     ((32, 32, 32), 64, "cfg3", False, "erf"),                                         # 8 charges x 2048
     ((32, 32, 32), 64, "cfg3", True, "erf"),
-    ((64, 64, 64), 256, [(0, 0, 0, 1.0)], True, "erf"),                               # too long: fallback
+    ((64, 64, 64), 256, [(0, 0, 0, 1.0)], True, "erf"),         # periodic, one charge, L >= 32: master never written
+    ((32, 48, 40), 64, [(1.25, -0.3125, 2.5, 1.5)], True, "erf"),
+    ((32, 32, 32), 64, [(0.46875, 0.0, -1.5625, 1.0)], True, "midpoint"),
+    ((40, 3, 36), 16, [(0.0, 0.0, 0.0, 1.0)], True, "erf"),    # one short axis: the per-block kernels
 ]
 
 
