@@ -61,3 +61,22 @@ def test_runner_id_file_rendezvous(runner, tmp_path):
                         "--warmup", "0"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     assert idf.exists() and idf.stat().st_size == 128
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", [["--periodic", "--L", "64", "--n", "16"],
+                                   ["--charges", "CSV", "--L", "6", "--n", "32"]])
+def test_runner_periodic_and_multi_charge(runner, tmp_path, extra):
+    """The runner's step and energy on the other prepare paths: a periodic lattice with one charge
+    and L >= 32 (generator fused into the assembly, master never written) and a box cell with
+    several charges from the reference's CSV format; the fused energy matches the 1D form."""
+    if "CSV" in extra:
+        csv = tmp_path / "cell.csv"
+        csv.write_text("x,y,z,Z\n0,0,0,1\n1.25,-0.3125,2.5,2\n-2.5,1.875,0.625,0.5\n")
+        extra = [str(csv) if a == "CSV" else a for a in extra]
+    r = subprocess.run([str(runner), *extra, "--world", "1", "--rank", "0", "--device", "0", "--steps", "2",
+                        "--warmup", "1", "--energy"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert res["value_gpts"] > 0
+    assert res["energy"]["rel_diff_vs_1d"] <= 1e-12
