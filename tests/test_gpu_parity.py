@@ -209,9 +209,17 @@ def test_prepare_fused_generator_assembly_bitwise(L, orc, case):
     pipe.assemble()
     torch.cuda.synchronize()
     split = [pipe.factor(l).cpu().numpy().T.copy() for l in range(3)]
+    # assemble() right after a prepare() that may have left the master unwritten (periodic fused
+    # path) rebuilds the master first
+    pipe2 = L.DevicePipeline(spec, rule, mode=mode, periodic=periodic)
+    pipe2.prepare()
+    pipe2.assemble()
+    torch.cuda.synchronize()
+    again = [pipe2.factor(l).cpu().numpy().T.copy() for l in range(3)]
     for l in range(3):
         assert np.array_equal(fused[l], want[l]), ("fused vs oracle", l)
         assert np.array_equal(split[l], want[l]), ("two launches vs oracle", l)
+        assert np.array_equal(again[l], want[l]), ("assemble after prepare", l)
 
 
 def test_assembly_matches_golden_bitwise(L, golden):
