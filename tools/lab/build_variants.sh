@@ -10,7 +10,7 @@ SRC=${SRC:-expand}  # which csrc/<SRC>.cu the flags apply to
 OTHERS=$(ls $ROOT/build/obj/*.o | grep -v "/$SRC.o$")
 for spec in "$@"; do
   name=${spec%%:*}; flags=${spec#*:}
-  d=$ROOT/lab_build/$name/paper_1405_2270_b200
+  d=$ROOT/${LAB_DIR:-lab_build}/$name/paper_1405_2270_b200
   mkdir -p $d
   cp $PKG/*.py $d/
   nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include $flags -c $PKG/csrc/$SRC.cu -o $d/$SRC.o &
@@ -18,7 +18,7 @@ done
 wait
 for spec in "$@"; do
   name=${spec%%:*}
-  d=$ROOT/lab_build/$name/paper_1405_2270_b200
+  d=$ROOT/${LAB_DIR:-lab_build}/$name/paper_1405_2270_b200
   nvcc $ARCH -shared -o $d/liblatsum_cuda.so $d/$SRC.o $OTHERS -lcudart
   rm $d/$SRC.o
 done

@@ -7,8 +7,8 @@ import math
 import os
 import sys
 
-sys.path.insert(0, os.environ.get("LS_LAB_ROOT", "/root/repo"))
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, "/root/repo")  # bench.py
+sys.path.insert(0, os.environ.get("LS_LAB_ROOT", "/root/repo"))  # the package under test comes first
 import torch  # noqa: E402
 
 import bench  # noqa: E402
