@@ -47,12 +47,18 @@ struct ExpandArgs {
 // SM id, so tools/lab/timeline.py can attribute a CTA's time to waits, DMMA issue, fills and
 // epilogues.
 #ifdef LS_TIMELINE
+__device__ __forceinline__ unsigned long long tl_globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #define LS_TL_INIT()                                                                         \
     int tl_n_ = 1;                                                                           \
-    unsigned long long* tl_ = p.timeline ? p.timeline + (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 128 : nullptr
+    unsigned long long* tl_ = p.timeline ? p.timeline + (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 128 : nullptr; \
+    if (tl_ && (threadIdx.x & 31) == 0) tl_[126] = ls_k3::tl_globaltimer()
 #define LS_TL(ev)                                                                            \
     do {                                                                                     \
-        if (tl_ && (threadIdx.x & 31) == 0 && tl_n_ < 128) {                                 \
+        if (tl_ && (threadIdx.x & 31) == 0 && tl_n_ < 126) {                                 \
             tl_[tl_n_++] = (static_cast<unsigned long long>(clock64()) << 8) | (ev);         \
         }                                                                                    \
     } while (0)
@@ -62,6 +68,7 @@ struct ExpandArgs {
             unsigned smid;                                                                   \
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                                \
             tl_[0] = (static_cast<unsigned long long>(smid) << 32) | static_cast<unsigned>(tl_n_); \
+            tl_[127] = ls_k3::tl_globaltimer();  /* slots 126/127: %globaltimer at warp start/end */ \
         }                                                                                    \
     } while (0)
 #else
