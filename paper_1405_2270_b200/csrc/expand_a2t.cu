@@ -225,27 +225,49 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
     // holds queued DMMAs instead of stalling the warp between chunks.
     const int n_items = my_units * n_jc;
     double fsum = 0.0;
+    // An item's place in the grid, advanced from item to item without divisions (the item loop
+    // used to divide by n_jc and n_ichunks twice per item: about 150 instructions with MUFU
+    // latencies at the head of every item, with only two warps per sub-partition to hide them).
     struct Tile {
         int64_t kk;
-        int unit, ibase, jb, c;
+        int n, c, unit, ic, ibase, jb;
         bool fast;
     };
-    auto tile_of = [&](int x) {
-        Tile T;
-        const int n = x / n_jc;
-        T.c = x - n * n_jc;
-        T.unit = b + n * G;
-        const int ic = T.unit % n_ichunks;
-        T.kk = T.unit / n_ichunks;
-        T.ibase = kA2tIC * ic + 32 * wi;
+    const int g_div = G / n_ichunks, g_mod = G - g_div * n_ichunks;
+    auto place = [&](Tile& T) {
+        T.ibase = kA2tIC * T.ic + 32 * wi;
         T.jb = kA2tJC * T.c + 32 * wj;
         T.fast = STORE && !FUNC && T.ibase + 8 * kTN <= p.N1 && T.jb + 8 * kTM <= p.N2 && p.vec_store && !p.accumulate;
+    };
+    auto first_tile = [&]() {
+        Tile T;
+        T.n = 0;
+        T.c = 0;
+        T.unit = b;
+        T.kk = b / n_ichunks;
+        T.ic = b - static_cast<int>(T.kk) * n_ichunks;
+        place(T);
         return T;
     };
-    // Whole epilogue of item x (every path; the fast path is also spread into the next item).
+    auto next_tile = [&](const Tile& P) {
+        Tile T = P;
+        if (++T.c == n_jc) {
+            T.c = 0;
+            ++T.n;
+            T.unit += G;
+            T.kk += g_div;
+            T.ic += g_mod;
+            if (T.ic >= n_ichunks) {
+                T.ic -= n_ichunks;
+                ++T.kk;
+            }
+        }
+        place(T);
+        return T;
+    };
+    // Whole epilogue of an item (every path; the fast path is also spread into the next item).
     // Lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
-    auto epilogue = [&](int x, double (&acc)[kTM][kTN][2]) {
-        const Tile T = tile_of(x);
+    auto epilogue = [&](const Tile& T, double (&acc)[kTM][kTN][2]) {
         double r1[kTN][2];
         if (FUNC) {
 #pragma unroll
@@ -301,8 +323,10 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
             fsum = 0.0;
         }
     };
-    auto item = [&](int x, double (&cur)[kTM][kTN][2], double (&prev)[kTM][kTN][2]) {
-        const int n = x / n_jc, c = x - n * n_jc;
+    // Item T into `cur`; P is the previous item (its accumulators in `prev`), if any.
+    auto item = [&](const Tile& T, const Tile& P, bool have_prev, double (&cur)[kTM][kTN][2],
+                    double (&prev)[kTM][kTN][2]) {
+        const int n = T.n, c = T.c;
         const int slot = n % kNS;
         if (c == 0) {
             mbar_wait(scaled + 2 * slot + wi, static_cast<unsigned>((n / kNS) & 1), p.fault);
@@ -331,10 +355,9 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
         }
         bool spread = false;
         double* prow = nullptr;
-        if (x > 0) {
-            const Tile T = tile_of(x - 1);
-            spread = T.fast && !lab_nostore;
-            prow = p.out + T.kk * p.ldz + static_cast<int64_t>(T.jb + g) * p.ldy + T.ibase + 2 * t;
+        if (have_prev) {
+            spread = P.fast && !lab_nostore;
+            prow = p.out + P.kk * p.ldz + static_cast<int64_t>(P.jb + g) * p.ldy + P.ibase + 2 * t;
         }
 #pragma unroll
         for (int m = 0; m < kTM; ++m)
@@ -400,7 +423,7 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
             }
         }
         LS_TL(5);
-        if (x > 0 && !spread) epilogue(x - 1, prev);  // the other paths, after this item's DMMAs are queued
+        if (have_prev && !spread) epilogue(P, prev);  // the other paths, after this item's DMMAs are queued
         if (c == 0 && n + 1 < my_units) {  // unit n + 1's share is scaled: hand it over
             __syncwarp();
             if (lane == 0) mbar_arrive(scaled + 2 * ((n + 1) % kNS) + wi);
@@ -424,15 +447,18 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
     };
     double accA[kTM][kTN][2], accB[kTM][kTN][2];
     int x = 0;
+    Tile Ta = first_tile(), Tb = Ta;  // Ta: the item going into accA; Tb: the one in accB
     for (; x + 1 < n_items; x += 2) {
-        item(x, accA, accB);
-        item(x + 1, accB, accA);
+        item(Ta, Tb, x > 0, accA, accB);
+        Tb = next_tile(Ta);
+        item(Tb, Ta, true, accB, accA);
+        Ta = next_tile(Tb);
     }
     if (x < n_items) {
-        item(x, accA, accB);
-        epilogue(x, accA);
+        item(Ta, Tb, x > 0, accA, accB);
+        epilogue(Ta, accA);
     } else if (n_items > 0) {
-        epilogue(n_items - 1, accB);
+        epilogue(Tb, accB);
     }
     LS_TL(7);
     LS_TL(8);

@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(256, 2) k(double* out, int NJ) {
 }
 
 template <int EXTRA, int WHERE, int KIND>
-void run(double* out, double base_ms = 0) {
-    const int NJ = 400, grid = 148 * 2;
+void run(double* out, int per_sm = 2) {
+    const int NJ = 400, grid = 148 * per_sm;
     cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
     k<EXTRA, WHERE, KIND><<<grid, 256>>>(out, NJ); CK(cudaDeviceSynchronize());
     float best = 1e9;
@@ -78,9 +78,9 @@ void run(double* out, double base_ms = 0) {
     }
     const double flops = 2.0 * 256 * 16 * 10.0 * NJ * grid * 8;
     // per-SMSP clocks per tile-round (4 warps' tiles): best_ms * 1.965e6 / NJ
-    printf("{\"extra\":%d,\"where\":\"%s\",\"kind\":\"%s\",\"ms\":%.4f,\"tflops\":%.3f,\"clk_per_warp_tile\":%.1f}\n", EXTRA,
+    printf("{\"ctas_per_sm\":%d,\"extra\":%d,\"where\":\"%s\",\"kind\":\"%s\",\"ms\":%.4f,\"tflops\":%.3f,\"clk_per_warp_tile\":%.1f}\n", per_sm, EXTRA,
            WHERE ? "spread over k-steps" : "tile end", KIND ? "dfma (dependent)" : "iadd", best, flops / best / 1e9,
-           best * 1.965e6 / NJ / 4);
+           best * 1.965e6 / NJ / (2 * per_sm));
 }
 
 int main() {
@@ -89,5 +89,8 @@ int main() {
     run<40, 0, 0>(out); run<80, 0, 0>(out); run<160, 0, 0>(out); run<320, 0, 0>(out); run<640, 0, 0>(out);
     run<40, 1, 0>(out); run<80, 1, 0>(out); run<160, 1, 0>(out); run<320, 1, 0>(out); run<640, 1, 0>(out);
     run<40, 0, 1>(out); run<40, 1, 1>(out);
+    // one CTA of 8 warps per SM (two warps per sub-partition, the A2-in-TMEM plan's shape)
+    run<0, 0, 0>(out, 1); run<40, 0, 0>(out, 1); run<160, 0, 0>(out, 1); run<320, 0, 0>(out, 1); run<640, 0, 0>(out, 1);
+    run<160, 1, 0>(out, 1); run<640, 1, 0>(out, 1);
     return 0;
 }
