@@ -394,6 +394,20 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 }
         }
         int next_task = 0;
+        // Epilogue addressing, strength-reduced: the unit's tiles are visited in ascending j, so
+        // the lane's first output row advances by JC rows per tile (ptxas otherwise rebuilds the
+        // whole 64-bit address, the lane ids included, in every tile).
+        // Measured at 1024^2 (profiles/r02_rowrun_ab.txt): cfg1 2.657 -> 2.634 ms, ranks 21 / 41 at
+        // 256 slabs +1.5%, 93 / 113 +0.5%; two DFMA ranks (KD 9: -1.7%, more spills) and the
+        // single-buffer shape (rank 164: -1.7%) keep the per-tile address.
+        constexpr bool kRowRun = STORE && !SINGLE && n_tail == 1;
+        const int ibase = ib + wi * (8 * kTN);
+        const bool fast_u = ibase + 8 * kTN <= p.N1 && (!STORE || (p.vec_store && !p.accumulate));
+        double* row_run = nullptr;
+        if (kRowRun) {
+            const int jb0 = ((kChunked ? jc_lo / n_kc : jc_lo) * JPS) * JC + wj * (8 * kTM);
+            row_run = p.out + kk * p.ldz + static_cast<int64_t>(jb0 + g) * p.ldy + ibase + 2 * t;
+        }
 
         for (int w = jc_lo; w < jc_hi; ++w, ++st) {
             LS_TL(7);  // stage loop top (previous epilogue done)
@@ -500,12 +514,16 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
                 if (kChunked && kc != n_kc - 1) continue;  // the tile continues in the next stage
                 // Epilogue: lane owns (j = jb + 8m + g, i = ibase + 8nn + 2t + {0,1}).
                 const int jb = (jc * JPS + h) * JC + wj * (8 * kTM);
-                const int ibase = ib + wi * (8 * kTN);
-                if (ibase + 8 * kTN <= p.N1 && jb + 8 * kTM <= p.N2 && (!STORE || (p.vec_store && !p.accumulate))) {
+                double* row;  // = out + kk ldz + (jb + g) ldy + ibase + 2 t
+                if constexpr (kRowRun) {
+                    row = row_run;
+                    row_run += static_cast<int64_t>(JC) * p.ldy;
+                }
+                if (fast_u && jb + 8 * kTM <= p.N2) {
+                    if constexpr (STORE && !kRowRun)
+                        row = p.out + kk * p.ldz + static_cast<int64_t>(jb + g) * p.ldy + ibase + 2 * t;
                     // Interior tile (the common case): no per-element bounds or mode checks. Measured
                     // 2.4% of the whole kernel at cfg1 (2.826 -> 2.760 ms).
-                    double* row = STORE ? p.out + kk * p.ldz + static_cast<int64_t>(jb + g) * p.ldy + ibase + 2 * t
-                                        : nullptr;
 #pragma unroll
                     for (int m = 0; m < kTM; ++m) {
                         if (lab_nostore) break;
