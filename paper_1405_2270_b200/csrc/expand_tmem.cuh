@@ -421,6 +421,17 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
             if (fill_now && next_task == 0 && n >= 1)  // this quarter of buffer buf^1 was read by unit n-1
                 mbar_wait(as_empty + 4 * (buf ^ 1) + wi, static_cast<unsigned>(((n - 1) >> 1) & 1), p.fault);
 
+            // The first tail rank's A1k (TMEM, fixed for the unit) does not depend on the ring
+            // stage: its loads go out before the stage wait, so their latency overlaps the wait
+            // and the loop bookkeeping instead of sitting in front of the tile's first DFMA
+            // (bit-identical; cfg1 step 2.6155 -> 2.6067 ms, ranks 9-53 at 1024^2 x 256 slabs +0.3 to
+            // +1.6%, profiles/r02_pretail_ab.txt).
+            constexpr bool kPreTail = !kChunked;
+            uint32_t pre0[8], pre1[8];
+            if constexpr (kPreTail) {
+                tmem::ld_x8_issue(tb + 8 * KD, pre0);
+                tmem::ld_x8_issue(tb + 8 * KD + 8, pre1);
+            }
             const int slot = st % kNS;
             mbar_wait(full + slot, static_cast<unsigned>((st / kNS) & 1), p.fault);
             LS_TL(4);  // stage landed
@@ -443,8 +454,15 @@ __global__ void __launch_bounds__(WARPS_ * 32, WARPS_ == 8 ? 2 : 1) expand_tmem_
 #pragma unroll
                     for (int m = 0; m < kTM; ++m) bt[m] = tbp[m * 8 * n_tail];
                     double at0[4], at1[4];
-                    tmem::ld_x8(tb + 8 * KD + 16 * qt, at0);
-                    tmem::ld_x8(tb + 8 * KD + 16 * qt + 8, at1);
+                    if (kPreTail && h == 0 && qt == 0) {
+                        tmem::wait_ld(pre0);
+                        tmem::wait_ld(pre1);
+                        tmem::unpack(pre0, at0);
+                        tmem::unpack(pre1, at1);
+                    } else {
+                        tmem::ld_x8(tb + 8 * KD + 16 * qt, at0);
+                        tmem::ld_x8(tb + 8 * KD + 16 * qt + 8, at1);
+                    }
                     const double atx[8] = {at0[0], at0[1], at0[2], at0[3], at1[0], at1[1], at1[2], at1[3]};
 #pragma unroll
                     for (int nn = 0; nn < kTN; ++nn)
