@@ -31,6 +31,7 @@
 //   [wi][ks][nn][lane] = A1(i = 64 ic + 32 wi + 8 nn + g, q = 4 ks + t), then
 //   [wi][qt][e][lane]  = A1(i = 64 ic + 32 wi + 8 (e >> 1) + 2 t + (e & 1), q = 4 KD + qt),
 // then the scale row S(k, 0 .. SR) (zero beyond R).
+#include <type_traits>
 #include <utility>
 
 #include "common.cuh"
@@ -324,8 +325,13 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
         }
     };
     // Item T into `cur`; P is the previous item (its accumulators in `prev`), if any.
-    auto item = [&](const Tile& T, const Tile& P, bool have_prev, double (&cur)[kTM][kTN][2],
+    // maysc (a std::bool_constant): whether this call site can carry the next unit's scaling share
+    // at all. With two j-chunks the items alternate chunk 0 / chunk 1 with the accumulator sets,
+    // so the chunk-1 call site drops the (predicated-off, but issued) scaling instructions of
+    // every k-step at compile time.
+    auto item = [&](auto maysc, const Tile& T, const Tile& P, bool have_prev, double (&cur)[kTM][kTN][2],
                     double (&prev)[kTM][kTN][2]) {
+        constexpr bool kMaySc = decltype(maysc)::value;
         const int n = T.n, c = T.c;
         const int slot = n % kNS;
         if (c == 0) {
@@ -343,10 +349,10 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
         const uint32_t ta = tq + static_cast<uint32_t>(c * CBJ);
         // The next unit's share of operand scaling (scale_share's work) is spread over chunk 0's
         // k-steps too: one product per k-step, the tail ranks with the last.
-        const bool sc = c == 0 && n + 1 < my_units && !lab_noscale;
+        const bool sc = kMaySc && c == 0 && n + 1 < my_units && !lab_noscale;
         double* fr1 = nullptr;
         const double* sr1 = nullptr;
-        if (c == 0 && n + 1 < my_units) {
+        if (kMaySc && c == 0 && n + 1 < my_units) {
             const int sl1 = (n + 1) % kNS;
             mbar_wait(full + sl1, static_cast<unsigned>(((n + 1) / kNS) & 1), p.fault);
             double* st1 = ring + sl1 * kStage;
@@ -424,7 +430,7 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
         }
         LS_TL(5);
         if (have_prev && !spread) epilogue(P, prev);  // the other paths, after this item's DMMAs are queued
-        if (c == 0 && n + 1 < my_units) {  // unit n + 1's share is scaled: hand it over
+        if (kMaySc && c == 0 && n + 1 < my_units) {  // unit n + 1's share is scaled: hand it over
             __syncwarp();
             if (lane == 0) mbar_arrive(scaled + 2 * ((n + 1) % kNS) + wi);
             LS_TL(6);
@@ -448,14 +454,25 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
     double accA[kTM][kTN][2], accB[kTM][kTN][2];
     int x = 0;
     Tile Ta = first_tile(), Tb = Ta;  // Ta: the item going into accA; Tb: the one in accB
-    for (; x + 1 < n_items; x += 2) {
-        item(Ta, Tb, x > 0, accA, accB);
-        Tb = next_tile(Ta);
-        item(Tb, Ta, true, accB, accA);
-        Ta = next_tile(Tb);
+    constexpr std::true_type kSc{};
+    constexpr std::false_type kNoSc{};
+    if (n_jc == 2) {  // even items are chunk 0 (accA), odd items chunk 1 (accB)
+        for (; x + 1 < n_items; x += 2) {
+            item(kSc, Ta, Tb, x > 0, accA, accB);
+            Tb = next_tile(Ta);
+            item(kNoSc, Tb, Ta, true, accB, accA);
+            Ta = next_tile(Tb);
+        }
+    } else {
+        for (; x + 1 < n_items; x += 2) {
+            item(kSc, Ta, Tb, x > 0, accA, accB);
+            Tb = next_tile(Ta);
+            item(kSc, Tb, Ta, true, accB, accA);
+            Ta = next_tile(Tb);
+        }
     }
     if (x < n_items) {
-        item(Ta, Tb, x > 0, accA, accB);
+        item(kSc, Ta, Tb, x > 0, accA, accB);
         epilogue(Ta, accA);
     } else if (n_items > 0) {
         epilogue(Tb, accB);
