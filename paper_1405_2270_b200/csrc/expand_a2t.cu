@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kA2tWarps * 32, 1) expand_a2t_kernel(const Exp
         tmem::wait_ld(ra[0]);
 #pragma unroll
         for (int ks = 0; ks < KD; ++ks) {
-            double a[kTM], bb[kTN], sv = 0.0, ss = 0.0;
+            double a[kTM], bb[kTN], sv, ss;  // sv, ss: set and used under `sc` only (no zeroing per k-step)
             tmem::unpack(ra[ks & 1], a);
             if (ks + 1 < KD) tmem::ld_x8_issue(ta + 8 * (ks + 1), ra[(ks + 1) & 1]);
 #pragma unroll
